@@ -1,0 +1,199 @@
+/*
+ * mxp_chol.h -- C ABI of the B200-native mixed-precision, out-of-core,
+ * left-looking tile Cholesky factorization of arxiv 2410.09819.
+ *
+ * Problem statement (Alg. 1): factor a symmetric
+ * positive-definite n x n matrix A = L L^T, A partitioned into Nt x Nt tiles
+ * of nb x nb (Nt = ceil(n/nb)); the lower tiles are traversed column by
+ * column (left-looking): SYRK+POTRF on the diagonal tile, GEMM+TRSM on each
+ * tile below it, every tile with its own precision.
+ *
+ * Conventions shared by every call:
+ *  - Matrices are column-major with a leading dimension (lda >= n); only the
+ *    lower triangle is referenced or written (LAPACK dpotrf('L') semantics).
+ *  - "host" pointers are CPU memory (pageable or pinned); "device" pointers
+ *    are CUDA global memory of the plan's device.  The caller owns every
+ *    buffer it passes; the plan owns everything it allocates itself.
+ *  - Precision codes: MXP_FP64 = 0, MXP_FP32 = 1, MXP_FP16 = 2, MXP_FP8 = 3
+ *    (OCP E4M3 "fn", saturating).  FP16/FP8 tiles carry a per-tile power-of-two
+ *    scale s: stored codes = RNE(x * s); value = code / s  (G11).
+ *  - Precision maps hold Nt(Nt+1)/2 codes in column-major lower-tile order
+ *    (0,0),(1,0),...,(Nt-1,0),(1,1),... ; diagonal tiles must be MXP_FP64.
+ *  - Return value: MXP_OK (0); -i when the i-th argument is invalid (LAPACK
+ *    style); or one of the negative MXP_E* codes below.
+ *  - `info` (LAPACK / cuSOLVER devInfo): 0 on success; j > 0 when the leading
+ *    minor of order j is not positive definite (global 1-based row of the
+ *    failing pivot).  On failure, tile columns before the failing one hold L;
+ *    later content is unspecified.
+ *  - Calls on one plan are not reentrant; different plans are independent.
+ */
+#ifndef MXP_CHOL_H
+#define MXP_CHOL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MXP_CHOL_ABI_VERSION 1
+
+enum mxp_status {
+    MXP_OK = 0,
+    MXP_ECUDA = -1001,    /* a CUDA runtime call failed (see mxp_last_error) */
+    MXP_ENOMEM = -1002,   /* device memory (or the HBM cap) below the working-set bound */
+    MXP_EHOSTPIN = -1003, /* pinning / registering host memory failed */
+    MXP_ESTATE = -1004,   /* call not valid in the plan's current state */
+    MXP_ENOTSUP = -1005,  /* configuration not supported by this build */
+    MXP_EZERO = -1006,    /* ||A||_F = 0 in the planner (SPEC S:296 ZeroMatrix) */
+    MXP_ENCCL = -1007     /* inter-GPU exchange failed */
+};
+
+enum mxp_precision { MXP_FP64 = 0, MXP_FP32 = 1, MXP_FP16 = 2, MXP_FP8 = 3 };
+
+typedef struct mxp_plan_s* mxp_plan_t;
+
+/* Plan attributes (mxp_chol_plan_set / _get). */
+typedef enum mxp_attr {
+    MXP_ATTR_DEVICE = 0,          /* CUDA device ordinal (default: current device at plan time) */
+    MXP_ATTR_STREAM = 1,          /* cudaStream_t (as int64) all work is ordered after/before; 0 = legacy default */
+    MXP_ATTR_HBM_BYTES_CAP = 2,   /* cap on the tile pool; forces out-of-core when the lower triangle exceeds it */
+    MXP_ATTR_SPLITK_TILES = 3,    /* GEMM-chain K chunk, in tiles (default 16); deterministic for a fixed value */
+    MXP_ATTR_LOOKAHEAD = 4,       /* 1 = overlap column k's panel with column k+1's bulk update (default 1) */
+    MXP_ATTR_DEBUG_SYNC = 5,      /* 1 = synchronize and check after every kernel (debug) */
+    MXP_ATTR_PROFILE = 6,         /* 1 = time every launch with CUDA events on its stream (mxp_chol_kernel_stats) */
+    MXP_ATTR_GPU_LAUNCHES = 100,  /* (get only) kernels launched by the last factorization */
+    MXP_ATTR_H2D_BYTES = 101,     /* (get only) host->device bytes moved by the last factorization */
+    MXP_ATTR_D2H_BYTES = 102,     /* (get only) device->host bytes moved by the last factorization */
+    MXP_ATTR_POOL_SLOTS = 103,    /* (get only) tile slots in the device pool */
+    MXP_ATTR_NT = 104             /* (get only) Nt = ceil(n/nb) */
+} mxp_attr_t;
+
+/*
+ * mxp_chol_plan -- describe one factorization problem (Alg. 1 P:117 "A ... of
+ * size n x n, partitioned into Nt x Nt tiles"; precision map P:335).
+ *   n             matrix order, n >= 1                              (arg 1)
+ *   nb            tile size; nb % 128 == 0, 128 <= nb <= 2048        (arg 2)
+ *   precision_map host array of Nt(Nt+1)/2 codes, copied; NULL = all FP64 (arg 3)
+ *   ngpus         GPUs the plan spans; this build supports 1 per process (arg 4)
+ *   out           receives the plan handle                           (arg 5)
+ * No device memory is allocated here; that happens on the first factor call
+ * (or mxp_chol_set_workspace).
+ */
+int mxp_chol_plan(int64_t n, int64_t nb, const uint8_t* precision_map, int ngpus, mxp_plan_t* out);
+
+/* Set / get a plan attribute.  Returns -2 for an unknown key, -3 for a bad value. */
+int mxp_chol_plan_set(mxp_plan_t plan, mxp_attr_t key, int64_t value);
+int mxp_chol_plan_get(mxp_plan_t plan, mxp_attr_t key, int64_t* value);
+
+/*
+ * Device workspace.  mxp_chol_workspace_size reports the bytes the plan needs
+ * on its device (tile pool + split-K partials + scratch) for the current
+ * attributes.  mxp_chol_set_workspace hands the plan a caller-owned device
+ * buffer of at least that size (e.g. a torch tensor); without it the plan
+ * cudaMallocs its own on first use and frees it in mxp_chol_plan_destroy.
+ */
+int mxp_chol_workspace_size(mxp_plan_t plan, size_t* bytes);
+int mxp_chol_set_workspace(mxp_plan_t plan, void* device_ptr, size_t bytes);
+
+/*
+ * mxp_chol_factor_device -- in-core factorization of a device-resident matrix
+ * (the like-for-like comparison with cusolverDnXpotrf).
+ *   A_dev  device pointer, n x n column-major, lda >= n; lower triangle is
+ *          overwritten by L (values of FP16/FP8/FP32 tiles are the
+ *          dequantized stored values); strict upper triangle untouched. (arg 2)
+ *   lda    leading dimension                                          (arg 3)
+ *   info   host pointer, receives info                                (arg 4)
+ * Ordered on MXP_ATTR_STREAM; returns after the result is complete.
+ */
+int mxp_chol_factor_device(mxp_plan_t plan, double* A_dev, int64_t lda, int64_t* info);
+
+/*
+ * mxp_chol_factor -- factorization of a host-resident matrix (Alg. 2
+ * P:240-278): tiles are streamed host->device on side streams, factored, and
+ * written back device->host (lower triangle only).  When the lower
+ * triangle at its storage precisions exceeds the device pool
+ * (MXP_ATTR_HBM_BYTES_CAP or HBM), tiles are cached and evicted out-of-core
+ * (V1 accumulator retention, V2 reuse/eviction, V3 diagonal pinning;
+ * P:235-238, Alg. 3).
+ *   A_host host pointer (pinned via mxp_host_alloc for full copy bandwidth;
+ *          pageable memory is registered for the call), column-major, lda >= n;
+ *          lower triangle overwritten by L as in mxp_chol_factor_device. (arg 2)
+ *   lda, info as above.
+ */
+int mxp_chol_factor(mxp_plan_t plan, double* A_host, int64_t lda, int64_t* info);
+
+/*
+ * mxp_chol_logdet -- log|A| = 2 sum_i log L_ii (Eq. 1) of the
+ * last successful factorization of this plan, reduced in fp64 on the device.
+ * Returns MXP_ESTATE if no factorization succeeded.
+ */
+int mxp_chol_logdet(mxp_plan_t plan, double* logdet);
+
+/*
+ * mxp_precision_map_from_matrix_device -- the MxP planner: per-tile
+ * Frobenius norms f_ij (fp64), F = ||A||_F with off-diagonal tiles counted
+ * twice, and for each off-diagonal tile the least precise allowed p with
+ *     Nt * f_ij / F < eps / u_p      (u_p the unit roundoff, G6);
+ * diagonal tiles and tiles where none qualifies get FP64.
+ *   n, nb        as in mxp_chol_plan                                (args 1-2)
+ *   A_dev        device pointer, column-major, lower triangle read   (arg 3)
+ *   lda          leading dimension                                   (arg 4)
+ *   eps          target accuracy, 0 < eps < 1                        (arg 5)
+ *   allowed_mask bit p set => precision p may be chosen; must include FP64 (arg 6)
+ *   map_out      host array of Nt(Nt+1)/2 codes                      (arg 7)
+ *   norms_out    optional host array of Nt(Nt+1)/2 tile norms, or NULL (arg 8)
+ * Runs on the current device and the legacy default stream.  Returns
+ * MXP_EZERO when ||A||_F = 0.
+ */
+int mxp_precision_map_from_matrix_device(int64_t n, int64_t nb, const double* A_dev, int64_t lda,
+                                         double eps, uint32_t allowed_mask, uint8_t* map_out,
+                                         double* norms_out);
+
+/*
+ * Synthetic input generators, bit-identical to the host
+ * generators in workloads/ (same counter hash), writing the full symmetric
+ * matrix (both triangles) into a device buffer on `stream` (cudaStream_t, may
+ * be NULL for the legacy default stream).  AUX: they are not part of the
+ * factorization; they exist so bench-sized inputs need no host copy.
+ *  plgsy: A_ij = A_ji = u(seed, max(i,j), min(i,j)) - 0.5, A_ii += n, where
+ *         u = (mix64(((i << 32) | j) ^ mix64(seed + 0x9E3779B97F4A7C15)) >> 11) * 2^-53
+ *         and mix64 is the splitmix64 finaliser.
+ *  kms:   A_ij = rho^|i-j|  (Kac-Murdock-Szego, config C1).
+ */
+int mxp_generate_plgsy_device(int64_t n, uint64_t seed, double* A_dev, int64_t lda, void* stream);
+int mxp_generate_kms_device(int64_t n, double rho, double* A_dev, int64_t lda, void* stream);
+
+/*
+ * Per-kernel-class statistics of the last factorization when MXP_ATTR_PROFILE
+ * is 1: launches, summed CUDA-event durations (ms, each measured on the
+ * launching stream), and algorithmic flops (the n^3/3 decomposition: 2 nb^3
+ * per GEMM update, nb^3 per SYRK update and per TRSM, nb^3/3 per POTRF).
+ *   kernel_class  MXP_KCLASS_CHAIN (GEMM/SYRK chains + split-K reduction),
+ *                 MXP_KCLASS_POTRF (diagonal tile), MXP_KCLASS_TRSM,
+ *                 MXP_KCLASS_OTHER (pack/unpack/log-det/conversion)   (arg 2)
+ *   launches, milliseconds, flops   host outputs (any may be NULL)     (args 3-5)
+ */
+enum mxp_kclass { MXP_KCLASS_CHAIN = 0, MXP_KCLASS_POTRF = 1, MXP_KCLASS_TRSM = 2, MXP_KCLASS_OTHER = 3 };
+int mxp_chol_kernel_stats(mxp_plan_t plan, int kernel_class, int64_t* launches, double* milliseconds,
+                          double* flops);
+
+/* Destroy a plan and every device resource it owns. NULL is a no-op. */
+void mxp_chol_plan_destroy(mxp_plan_t plan);
+
+/* Page-locked host buffers for full-bandwidth H2D/D2H. */
+int mxp_host_alloc(size_t bytes, void** ptr);
+int mxp_host_free(void* ptr);
+
+/* Human-readable text for a status code; detail of the last CUDA error. */
+const char* mxp_strerror(int status);
+const char* mxp_last_error(void);
+
+/* ABI version of the loaded library (MXP_CHOL_ABI_VERSION). */
+int mxp_chol_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MXP_CHOL_H */

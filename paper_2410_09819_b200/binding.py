@@ -1,0 +1,245 @@
+"""ctypes marshalling for libmxpchol.so (include/mxp_chol.h).  No arithmetic."""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+FP64, FP32, FP16, FP8 = 0, 1, 2, 3
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libmxpchol.so")
+_lib = None
+_lock = threading.Lock()
+
+ATTR = {
+    "device": 0, "stream": 1, "hbm_bytes_cap": 2, "splitk_tiles": 3, "lookahead": 4,
+    "debug_sync": 5, "profile": 6, "gpu_launches": 100, "h2d_bytes": 101, "d2h_bytes": 102,
+    "pool_slots": 103, "nt": 104,
+}
+
+# every symbol include/mxp_chol.h declares (tests check the library exports them)
+EXPORTS = [
+    "mxp_chol_plan", "mxp_chol_plan_set", "mxp_chol_plan_get", "mxp_chol_workspace_size",
+    "mxp_chol_set_workspace", "mxp_chol_factor_device", "mxp_chol_factor", "mxp_chol_logdet",
+    "mxp_precision_map_from_matrix_device", "mxp_generate_plgsy_device", "mxp_generate_kms_device",
+    "mxp_chol_plan_destroy", "mxp_host_alloc", "mxp_host_free", "mxp_strerror", "mxp_last_error",
+    "mxp_chol_abi_version", "mxp_chol_kernel_stats",
+]
+KCLASS = {"chain": 0, "potrf": 1, "trsm": 2, "other": 3}
+
+
+class MxpError(RuntimeError):
+    def __init__(self, call: str, status: int):
+        msg = lib().mxp_strerror(status).decode()
+        detail = lib().mxp_last_error().decode()
+        super().__init__(f"{call} -> {status} ({msg}){': ' + detail if detail else ''}")
+        self.status = status
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def lib():
+    """Load the in-tree CUDA library.  Raises if it is missing: no fallback."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"{_LIB_PATH} not built; run __graft_entry__.build() "
+                              "(python paper_2410_09819_b200/build.py)")
+        L = ctypes.CDLL(_LIB_PATH)
+        i64, u64, i32 = ctypes.c_int64, ctypes.c_uint64, ctypes.c_int
+        vp, pi64, psz = ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_size_t)
+        pd = ctypes.POINTER(ctypes.c_double)
+        L.mxp_chol_plan.argtypes = [i64, i64, vp, i32, ctypes.POINTER(vp)]
+        L.mxp_chol_plan_set.argtypes = [vp, i32, i64]
+        L.mxp_chol_plan_get.argtypes = [vp, i32, pi64]
+        L.mxp_chol_workspace_size.argtypes = [vp, psz]
+        L.mxp_chol_set_workspace.argtypes = [vp, vp, ctypes.c_size_t]
+        L.mxp_chol_factor_device.argtypes = [vp, vp, i64, pi64]
+        L.mxp_chol_factor.argtypes = [vp, vp, i64, pi64]
+        L.mxp_chol_logdet.argtypes = [vp, pd]
+        L.mxp_precision_map_from_matrix_device.argtypes = [i64, i64, vp, i64, ctypes.c_double,
+                                                            ctypes.c_uint32, vp, vp]
+        L.mxp_generate_plgsy_device.argtypes = [i64, u64, vp, i64, vp]
+        L.mxp_generate_kms_device.argtypes = [i64, ctypes.c_double, vp, i64, vp]
+        L.mxp_chol_plan_destroy.argtypes = [vp]
+        L.mxp_chol_plan_destroy.restype = None
+        L.mxp_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(vp)]
+        L.mxp_host_free.argtypes = [vp]
+        L.mxp_strerror.argtypes = [i32]
+        L.mxp_strerror.restype = ctypes.c_char_p
+        L.mxp_last_error.argtypes = []
+        L.mxp_last_error.restype = ctypes.c_char_p
+        L.mxp_chol_abi_version.argtypes = []
+        L.mxp_chol_kernel_stats.argtypes = [vp, i32, pi64, pd, pd]
+        _lib = L
+        return L
+
+
+def _check(call: str, rc: int):
+    if rc != 0:
+        raise MxpError(call, rc)
+
+
+def abi_version() -> int:
+    return lib().mxp_chol_abi_version()
+
+
+def _colmajor_ptr(A, n: int):
+    """(pointer, lda) of a Fortran-strided 2-D tensor/array with >= n rows."""
+    try:  # torch
+        import torch
+        if isinstance(A, torch.Tensor):
+            if A.dtype != torch.float64:
+                raise TypeError("A must be float64")
+            if A.dim() != 2 or A.shape[0] != n or A.shape[1] != n:
+                raise ValueError("A must be n x n")
+            if A.stride(0) != 1:
+                raise ValueError("A must be column-major (stride(0) == 1); pass S.T for a "
+                                 "row-major symmetric S")
+            return A.data_ptr(), max(A.stride(1), n), A.is_cuda
+    except ImportError:
+        pass
+    import numpy as np
+    if isinstance(A, np.ndarray):
+        if A.dtype != np.float64 or A.shape != (n, n) or not A.flags.f_contiguous:
+            raise ValueError("A must be an n x n Fortran-ordered float64 array")
+        return A.ctypes.data, n, False
+    raise TypeError("A must be a torch tensor or numpy array")
+
+
+class Plan:
+    """Owns an ``mxp_plan_t``.  ``Plan(n, nb, precision_map=None)``."""
+
+    def __init__(self, n: int, nb: int, precision_map=None, ngpus: int = 1):
+        self._h = ctypes.c_void_p()
+        self.n, self.nb = int(n), int(nb)
+        self._map = None
+        mp = None
+        if precision_map is not None:
+            import numpy as np
+            self._map = np.ascontiguousarray(precision_map, dtype=np.uint8)
+            mp = self._map.ctypes.data
+        _check("mxp_chol_plan", lib().mxp_chol_plan(self.n, self.nb, mp, ngpus, ctypes.byref(self._h)))
+        self._ws = None
+
+    def __del__(self):
+        self.close()
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib().mxp_chol_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def set(self, key: str, value: int):
+        _check(f"mxp_chol_plan_set({key})", lib().mxp_chol_plan_set(self._h, ATTR[key], int(value)))
+
+    def get(self, key: str) -> int:
+        v = ctypes.c_int64()
+        _check(f"mxp_chol_plan_get({key})", lib().mxp_chol_plan_get(self._h, ATTR[key], ctypes.byref(v)))
+        return v.value
+
+    def workspace_size(self) -> int:
+        v = ctypes.c_size_t()
+        _check("mxp_chol_workspace_size", lib().mxp_chol_workspace_size(self._h, ctypes.byref(v)))
+        return v.value
+
+    def set_workspace(self, tensor):
+        """Hand the plan a caller-owned device buffer (a torch uint8 CUDA tensor)."""
+        _check("mxp_chol_set_workspace",
+               lib().mxp_chol_set_workspace(self._h, tensor.data_ptr(), tensor.numel() * tensor.element_size()))
+        self._ws = tensor
+
+    def use_torch_workspace(self, device=None):
+        import torch
+        nbytes = self.workspace_size()
+        t = torch.empty(nbytes + 256, dtype=torch.uint8, device=device or "cuda")
+        off = (-t.data_ptr()) % 256
+        self.set_workspace(t[off:off + nbytes])
+        self._ws_keep = t
+        return t
+
+    def _stream_from_torch(self):
+        import torch
+        self.set("stream", torch.cuda.current_stream().cuda_stream)
+
+    def factor_device(self, A, stream_from_torch: bool = True) -> int:
+        """In-place factorization of a device-resident column-major fp64 matrix.
+        Returns info (0 = success, j > 0 = leading minor j not PD)."""
+        ptr, lda, is_cuda = _colmajor_ptr(A, self.n)
+        if not is_cuda:
+            raise ValueError("factor_device needs a CUDA tensor")
+        if stream_from_torch:
+            self._stream_from_torch()
+        info = ctypes.c_int64()
+        _check("mxp_chol_factor_device", lib().mxp_chol_factor_device(self._h, ptr, lda, ctypes.byref(info)))
+        return info.value
+
+    def factor(self, A_host, stream_from_torch: bool = True) -> int:
+        """In-place factorization of a host-resident column-major fp64 matrix
+        (torch CPU tensor, ideally pinned, or numpy Fortran array)."""
+        ptr, lda, is_cuda = _colmajor_ptr(A_host, self.n)
+        if is_cuda:
+            raise ValueError("factor needs a host buffer; use factor_device")
+        if stream_from_torch:
+            self._stream_from_torch()
+        info = ctypes.c_int64()
+        _check("mxp_chol_factor", lib().mxp_chol_factor(self._h, ptr, lda, ctypes.byref(info)))
+        return info.value
+
+    def kernel_stats(self) -> dict:
+        """{class: (launches, ms, flops)} of the last factorization (profile=1)."""
+        out = {}
+        for name, c in KCLASS.items():
+            n, ms, fl = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double()
+            _check("mxp_chol_kernel_stats", lib().mxp_chol_kernel_stats(
+                self._h, c, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(fl)))
+            out[name] = (n.value, ms.value, fl.value)
+        return out
+
+    def logdet(self) -> float:
+        v = ctypes.c_double()
+        _check("mxp_chol_logdet", lib().mxp_chol_logdet(self._h, ctypes.byref(v)))
+        return v.value
+
+
+def precision_map_from_matrix_device(A, nb: int, eps: float, allowed: int = 0xF):
+    """Planner on a device matrix -> (uint8 map, float64 tile norms)."""
+    import numpy as np
+    n = A.shape[0]
+    ptr, lda, is_cuda = _colmajor_ptr(A, n)
+    if not is_cuda:
+        raise ValueError("needs a CUDA tensor")
+    Nt = -(-n // nb)
+    m = np.empty(Nt * (Nt + 1) // 2, np.uint8)
+    f = np.empty(Nt * (Nt + 1) // 2, np.float64)
+    _check("mxp_precision_map_from_matrix_device",
+           lib().mxp_precision_map_from_matrix_device(n, nb, ptr, lda, float(eps), allowed,
+                                                      m.ctypes.data, f.ctypes.data))
+    return m, f
+
+
+def generate_plgsy_device(A, seed: int = 42, stream=None):
+    n = A.shape[0]
+    ptr, lda, is_cuda = _colmajor_ptr(A, n)
+    _check("mxp_generate_plgsy_device", lib().mxp_generate_plgsy_device(n, seed, ptr, lda, stream))
+
+
+def generate_kms_device(A, rho: float, stream=None):
+    n = A.shape[0]
+    ptr, lda, is_cuda = _colmajor_ptr(A, n)
+    _check("mxp_generate_kms_device", lib().mxp_generate_kms_device(n, float(rho), ptr, lda, stream))
+
+
+def host_alloc(nbytes: int) -> int:
+    p = ctypes.c_void_p()
+    _check("mxp_host_alloc", lib().mxp_host_alloc(nbytes, ctypes.byref(p)))
+    return p.value
+
+
+def host_free(ptr: int):
+    _check("mxp_host_free", lib().mxp_host_free(ptr))

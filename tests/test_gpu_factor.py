@@ -1,0 +1,153 @@
+"""-m gpu parity tests: the CUDA path (through the C ABI) vs the CPU oracle on
+the same seeded inputs.  Tolerances from BASELINE north_star:
+FP64 per-entry |L_gpu - L_oracle| <= 1e-10 ||L||_max, backward error <= 1e-13,
+bit-exact on the integer-L0 exact-recovery inputs."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as w
+from gpu_util import gpu_factor
+
+pytestmark = pytest.mark.gpu
+
+
+def _close(L, Lo, tol=1e-10):
+    err = np.max(np.abs(L - Lo))
+    assert err <= tol * np.max(np.abs(Lo)), err
+
+
+def test_c1_kms_against_oracle_and_closed_form():
+    n, nb, rho = 1024, 256, 0.5
+    A = w.kms(n, rho)
+    L, info, ld, plan = gpu_factor(A, nb)
+    assert info == 0
+    Lo, _ = oracle.factor(A, nb)
+    _close(L, Lo)
+    closed = (n - 1) * math.log(1 - rho * rho)
+    assert abs(ld - closed) <= 1e-12 * abs(closed)
+    be = np.linalg.norm(A - L @ L.T) / np.linalg.norm(A)
+    assert be <= 1e-13
+    assert plan.get("gpu_launches") > 0
+
+
+@pytest.mark.parametrize("n,nb", [(1024, 128), (1024, 256), (2048, 512), (1280, 256), (1000, 256), (700, 128)])
+def test_integer_l0_bitwise(n, nb):
+    L0 = w.integer_l0(n, seed=n + nb)
+    A = w.spd_from_l0(L0)
+    L, info, ld, _ = gpu_factor(A, nb)
+    assert info == 0
+    assert np.array_equal(L, L0)
+
+
+@pytest.mark.parametrize("n,nb", [(2048, 256), (1536, 512), (1100, 128), (3072, 1024)])
+def test_plgsy_against_oracle(n, nb):
+    A = w.plgsy(n, seed=42)
+    L, info, ld, _ = gpu_factor(A, nb)
+    assert info == 0
+    Lo, _ = oracle.factor(A, nb)
+    _close(L, Lo)
+    assert abs(ld - oracle.logdet(Lo)) <= 1e-12 * abs(ld)
+    be = np.linalg.norm(A - L @ L.T) / np.linalg.norm(A)
+    assert be <= 1e-13
+
+
+def test_matern_strong_correlation_fp64():
+    xy = w.matern_locations(2048, seed=1)
+    S = w.matern_cov(xy, 1.0, 0.210158)
+    L, info, ld, _ = gpu_factor(S, 256)
+    Lo, oinfo = oracle.factor(S, 256)
+    assert info == oinfo == 0
+    _close(L, Lo, 1e-9)
+    assert abs(ld - oracle.logdet(Lo)) <= 1e-9 * abs(ld)
+
+
+@pytest.mark.parametrize("n,nb,j", [(1024, 256, 700), (1024, 128, 0), (768, 256, 767), (1024, 256, 300)])
+def test_not_pd_info(n, nb, j):
+    L0 = w.integer_l0(n, seed=5)
+    A = w.spd_from_l0(L0)
+    A[j, j] = -1.0 + np.sum(L0[j, :j] ** 2)
+    L, info, ld, _ = gpu_factor(A, nb)
+    _, oinfo = oracle.factor(A, nb)
+    assert info == oinfo == j + 1
+    kfail = j // nb
+    assert np.array_equal(L[:, : kfail * nb], L0[:, : kfail * nb])
+
+
+def test_determinism_and_lookahead_invariance():
+    A = w.plgsy(2048, seed=3)
+    L1, _, _, _ = gpu_factor(A, 256)
+    L2, _, _, _ = gpu_factor(A, 256)
+    L3, _, _, _ = gpu_factor(A, 256, attrs={"lookahead": 0})
+    assert np.array_equal(L1, L2)
+    assert np.array_equal(L1, L3)
+
+
+def test_splitk_chunks_within_tolerance():
+    A = w.plgsy(4096, seed=5)
+    L1, _, _, _ = gpu_factor(A, 128)
+    L2, _, _, _ = gpu_factor(A, 128, attrs={"splitk_tiles": 1})
+    _close(L1, L2, 1e-13)
+
+
+def test_host_path_equals_device_path():
+    A = w.plgsy(1536, seed=11)
+    Ld, info_d, ld_d, _ = gpu_factor(A, 256)
+    Lh, info_h, ld_h, plan = gpu_factor(A, 256, host=True)
+    assert info_d == info_h == 0
+    assert np.array_equal(Ld, Lh)
+    assert ld_d == ld_h
+    assert plan.get("h2d_bytes") > 0 and plan.get("d2h_bytes") > 0
+
+
+def test_upper_triangle_untouched_and_lda():
+    import torch
+
+    import paper_2410_09819_b200 as m
+    n, nb, lda = 1024, 256, 1100
+    A = w.plgsy(n, seed=2)
+    M = np.full((lda, n), 7.0)
+    M[:n, :] = np.tril(A) + np.triu(np.full((n, n), 3.0), 1)
+    Md = torch.tensor(np.ascontiguousarray(M.T), device="cuda")  # (n, lda) row-major == M column-major
+    view = Md.T[:n, :]  # stride (1, lda)
+    plan = m.Plan(n, nb)
+    info = plan.factor_device(view)
+    torch.cuda.synchronize()
+    R = Md.T.cpu().numpy()
+    assert info == 0
+    assert np.all(np.triu(R[:n, :], 1) == np.triu(np.full((n, n), 3.0), 1))
+    assert np.all(R[n:, :] == 7.0)
+    Lo, _ = oracle.factor(A, nb)
+    _close(np.tril(R[:n, :]), Lo)
+
+
+def test_device_generators_match_host():
+    import torch
+
+    import paper_2410_09819_b200 as m
+    n = 777
+    Ad = torch.empty((n, n), dtype=torch.float64, device="cuda").T
+    m.generate_plgsy_device(Ad, seed=42)
+    torch.cuda.synchronize()
+    assert np.array_equal(Ad.cpu().numpy(), w.plgsy(n, 42))
+    m.generate_kms_device(Ad, 0.5)
+    torch.cuda.synchronize()
+    assert np.array_equal(Ad.cpu().numpy(), w.kms(n, 0.5))
+
+
+def test_planner_device_matches_oracle():
+    import torch
+
+    import paper_2410_09819_b200 as m
+    xy = w.matern_locations(2048, seed=1)
+    S = w.matern_cov(xy, 1.0, 0.02627)
+    Sd = torch.tensor(S, device="cuda").T
+    for eps in (1e-5, 1e-8):
+        mp, f = m.precision_map_from_matrix_device(Sd, 128, eps)
+        fo = oracle.tile_norms(S, 128)
+        assert np.max(np.abs(f - fo) / np.maximum(fo, 1e-300)) <= 1e-13
+        mo = oracle.plan(S, 128, eps)
+        # identical except where a norm sits within rounding of a threshold
+        assert np.mean(mp == mo) >= 0.999

@@ -50,9 +50,25 @@ def uniform(seed: int, i: np.ndarray, j: np.ndarray) -> np.ndarray:
     return (x >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
 
 
+def pow_by_squaring(rho: float, d: np.ndarray) -> np.ndarray:
+    """rho^d for integer d >= 0 by binary exponentiation (low bit first), the
+    exact operation sequence the device generator uses, so both sides agree
+    bit for bit (exact for rho = 0.5)."""
+    d = np.asarray(d, dtype=np.int64)
+    out = np.ones(d.shape, dtype=np.float64)
+    base = np.full(d.shape, float(rho))
+    e = d.copy()
+    while np.any(e > 0):
+        odd = (e & 1) == 1
+        out = np.where(odd, out * base, out)
+        e >>= 1
+        base = np.where(e > 0, base * base, base)
+    return out
+
+
 def kms(n: int, rho: float) -> np.ndarray:
     idx = np.arange(n)
-    return np.power(float(rho), np.abs(idx[:, None] - idx[None, :]).astype(np.float64))
+    return pow_by_squaring(rho, np.abs(idx[:, None] - idx[None, :]))
 
 
 def plgsy(n: int, seed: int = 42) -> np.ndarray:
