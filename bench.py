@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""Benchmark: factorization TFLOP/s (n^3/3) of the left-looking tile Cholesky
+(arxiv 2410.09819) on B200, vs cuSOLVER potrf and the roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "C2"): n = 65536, nb = 1024, FP64,
+PLASMA-plgsy random SPD (seed 42, generated on the device by the same counter
+hash as workloads/), in-core on one B200.  A step = one full factorization
+(restore the input from a resident copy, then mxp_chol_factor_device); inputs
+(34 GB) are far larger than L2 (126 MB).  Timed with CUDA events on the
+plan's stream, barrier + synchronize on both sides, max over ranks.
+
+`e2e` is the same metric through the host API mxp_chol_factor on a pinned host
+matrix (H2D + factor + D2H inside the timed region, every step).
+`--impl reference` times the CPU oracle (oracle/, test infrastructure) on a
+bounded sample of the same workload family on the host cores.
+
+For N > 1 this build runs N independent replicas (one per GPU); the 2D
+block-cyclic multi-GPU factorization is not built yet.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "factorization TFLOP/s (n^3/3) at 1/2/4/8 B200 vs cuSOLVER potrf & roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=65536)
+    ap.add_argument("--nb", type=int, default=1024)
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cusolver", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        loaded = [s for s in sm if s > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_oracle_sample(n=2048, nb=256, seed=42):
+    """Time the CPU oracle (as it stands) on a bounded sample of the workload."""
+    import oracle
+    import workloads as w
+    A = w.plgsy(n, seed)
+    oracle.build()
+    t0 = time.perf_counter()
+    L, info = oracle.factor(A, nb)
+    t = time.perf_counter() - t0
+    assert info == 0
+    return {"value": n ** 3 / 3 / t / 1e12, "unit": "TFLOP/s", "cores": os.cpu_count(),
+            "kind": "oracle", "seconds": t,
+            "sample": f"oracle.factor (plain C fp64, OpenMP over a column's tasks) on plgsy "
+                      f"n={n} nb={nb} FP64, the same matrix family at a size the oracle finishes in "
+                      f"seconds; rate = (n^3/3)/t"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    n, nb = 2048, 256
+    times = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_oracle_sample(n, nb, args.seed)
+        if i >= args.warmup:
+            times.append(r["seconds"])
+    t = sum(times) / len(times)
+    value = n ** 3 / 3 / t / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C2 family (plgsy random SPD, FP64) -- bounded sample n={n} nb={nb} "
+                               f"per step on the host cores (the reference arm is the CPU oracle)",
+                   "n": n, "nb": nb, "seed": args.seed},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "oracle",
+                         "sample": f"oracle.factor plgsy n={n} nb={nb} per step"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def load_traffic(nb):
+    """dram bytes per launch of the chain kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_chain_latest.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d
+    except Exception:
+        return None, None
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2410_09819_b200 as m
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n, nb = args.n, args.nb
+    flops = n ** 3 / 3
+
+    m.lib()  # the in-tree CUDA library must load: no fallback path exists
+    stream = torch.cuda.current_stream()
+    A = torch.empty((n, n), dtype=torch.float64, device=dev).T  # column-major
+    m.generate_plgsy_device(A, seed=args.seed, stream=stream.cuda_stream)
+    B = torch.empty((n, n), dtype=torch.float64, device=dev).T
+    plan = m.Plan(n, nb)
+    plan.use_torch_workspace(dev)
+    plan.set("profile", 1)
+
+    def step():
+        B.copy_(A)
+        return plan.factor_device(B)
+
+    for _ in range(args.warmup):
+        info = step()
+        assert info == 0, info
+    clocks = Clocks(local)
+    clocks.start()
+    stats_acc = {}
+    launches = 0
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        info = step()
+        assert info == 0, info
+        launches += plan.get("gpu_launches") + 0
+        for k, (nl, ms, fl) in plan.kernel_stats().items():
+            a = stats_acc.setdefault(k, [0, 0.0, 0.0])
+            a[0] += nl
+            a[1] += ms
+            a[2] += fl
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    ck = clocks.stop()
+    t_step = ev0.elapsed_time(ev1) / 1e3 / args.steps
+    if ws > 1:
+        tt = torch.tensor([t_step], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step = tt.item()
+    value = ws * flops / t_step / 1e12
+
+    # correctness probe on the last factor: ||(A - L L^T) x|| / (||A||_F ||x||)
+    L = torch.tril(B)
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    x = torch.randn(n, 4, dtype=torch.float64, device=dev, generator=g)
+    probe = ((A @ x - L @ (L.T @ x)).norm() / (torch.linalg.matrix_norm(A) * x.norm())).item()
+    del L, x
+    logdet = plan.logdet()
+    sched = plan.sched_diagnostics()
+    if sched:
+        pot = sched.pop("potrf_timeline_ms")
+        sched["potrf_mean_ms"] = sum(e - w for (_, w, e) in pot) / len(pot)
+        for key in ("gemm_busy_ms", "gemm_wait_ms", "trsm_busy_ms", "trsm_wait_ms"):
+            sched[key + "_per_cta"] = sched.pop(key) / max(sched["ctas"], 1)
+
+    # live FP64 peak: cuBLAS DGEMM on this box (MEASURED_PEAKS.json has no fp64 figure)
+    d = 8192
+    Xa = torch.randn(d, d, dtype=torch.float64, device=dev)
+    Xb = torch.randn(d, d, dtype=torch.float64, device=dev)
+    for _ in range(2):
+        torch.matmul(Xa, Xb)
+    best = 1e9
+    for _ in range(5):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(Xa, Xb)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1) / 1e3)
+    dgemm_peak = 2 * d ** 3 / best / 1e12
+    del Xa, Xb
+
+    chain = stats_acc.get("chain", [0, 0.0, 0.0])
+    achieved = chain[2] / (chain[1] / 1e3) / 1e12 if chain[1] > 0 else None
+    traffic, tinfo = load_traffic(nb)
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": dgemm_peak, "unit": "TFLOP/s",
+                "frac": achieved / dgemm_peak if achieved else None, "traffic": traffic,
+                "kernel": "k_sched (persistent static-schedule kernel: FP64 DMMA GEMM/SYRK + TRSM tasks, "
+                          "all flops but the diagonal POTRFs)",
+                "achieved_how": "algorithmic flops of k_sched (n^3/3 - Nt*nb^3/3 per launch) / its CUDA-event "
+                                "duration on its stream, summed over the timed steps",
+                "peak_how": "cuBLAS DGEMM 8192^3 measured live in this run (fp64 dense; "
+                            "MEASURED_PEAKS.json has no fp64 figure)",
+                "traffic_how": "dram__bytes_read.sum+dram__bytes_write.sum of one captured k_sched launch "
+                               "(profiles/ncu_chain_latest.json)" if traffic else None}
+    kstats = {k: {"launches": v[0], "ms": v[1], "tflops": (v[2] / (v[1] / 1e3) / 1e12) if v[1] > 0 and v[2] > 0
+                  else None} for k, v in stats_acc.items()}
+
+    # cuSOLVER potrf (cusolverDnXpotrf, fp64) on the same box (library baseline).
+    # Its lower-triangle path dies with an illegal address at exactly n = 65536
+    # (n^2 = 2^32; 65024 works), so it is timed lower at n - 512 (same family,
+    # same lda layout) and upper at n (the other cuSOLVER code path).
+    cusolver = None
+    if not args.no_cusolver:
+        from tools.cusolver_ref import Potrf
+        cusolver = {}
+        for label, nn, uplo in (("lower_n%d" % (n - 512 if n >= 65536 else n), n - 512 if n >= 65536 else n, 0),
+                                ("upper_n%d" % n, n, 1)):
+            Bv = B[:nn, :nn]
+            ref = Potrf(nn, B.stride(1), Bv.data_ptr(), stream.cuda_stream, uplo)
+            ts = []
+            for i in range(2):
+                B.copy_(A)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                ref(Bv.data_ptr())
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1) / 1e3)
+            cinfo = int(ref.info.item())
+            ref.close()
+            cusolver[label] = {"value": nn ** 3 / 3 / min(ts) / 1e12, "unit": "TFLOP/s", "ms": min(ts) * 1e3,
+                               "info": cinfo, "n": nn, "uplo": "L" if uplo == 0 else "U"}
+        cusolver["note"] = ("cusolverDnXpotrf lower crashes (illegal address) at n=65536 exactly on CUDA 12.9 "
+                            "(cuSOLVER 11.7.5); lower timed at n-512, upper at n; best of 2 each")
+    del B
+    plan.close()
+    del plan
+    torch.cuda.empty_cache()
+
+    # end-to-end through the host API: pinned host A, H2D + factor + D2H per step
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.empty_cache()
+        Ah_src = A.T.contiguous().cpu()  # row-major symmetric == column-major A
+        del A
+        torch.cuda.empty_cache()
+        Ah = torch.empty((n, n), dtype=torch.float64).pin_memory()
+        p2 = m.Plan(n, nb)
+        ts = []
+        hb = db = 0
+        for i in range(1 + args.e2e_steps):
+            Ah.copy_(Ah_src)
+            torch.cuda.synchronize()
+            if ws > 1:
+                dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(torch.cuda.current_stream())
+            info = p2.factor(Ah.T)
+            e1.record(torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            assert info == 0, info
+            if i >= 1:
+                ts.append(e0.elapsed_time(e1) / 1e3)
+            hb, db = p2.get("h2d_bytes"), p2.get("d2h_bytes")
+        t = sum(ts) / len(ts)
+        if ws > 1:
+            tt = torch.tensor([t], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = tt.item()
+        e2e = {"value": ws * flops / t / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": hb,
+               "d2h_bytes_per_step": db, "ms_per_step": t * 1e3,
+               "how": "mxp_chol_factor on a pinned host n x n matrix; CUDA events around the call"}
+        p2.close()
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cpu = cpu_oracle_sample(2048, 256, args.seed)
+        cpu.pop("seconds", None)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C2: plgsy random SPD n={n} nb={nb} FP64 in-core on B200, "
+                                   f"device-resident input", "n": n, "nb": nb, "seed": args.seed,
+                       "l2": "inputs (n^2*8 B = %.1f GB) larger than L2 (126 MB); no flush" % (n * n * 8 / 1e9),
+                       "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas "
+                                      "(multi-GPU 2D block-cyclic not built yet)"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": ck,
+            "baselines": {"cusolver_potrf": cusolver},
+            "sched": sched,
+            "check": {"backward_error_probe": probe, "logdet": logdet},
+            "kernels": kstats,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -59,9 +59,11 @@ typedef enum mxp_attr {
     MXP_ATTR_DEVICE = 0,          /* CUDA device ordinal (default: current device at plan time) */
     MXP_ATTR_STREAM = 1,          /* cudaStream_t (as int64) all work is ordered after/before; 0 = legacy default */
     MXP_ATTR_HBM_BYTES_CAP = 2,   /* cap on the tile pool; forces out-of-core when the lower triangle exceeds it */
-    MXP_ATTR_SPLITK_TILES = 3,    /* GEMM-chain K chunk, in tiles (default 16); deterministic for a fixed value */
-    MXP_ATTR_LOOKAHEAD = 4,       /* 1 = overlap column k's panel with column k+1's bulk update (default 1) */
-    MXP_ATTR_DEBUG_SYNC = 5,      /* 1 = synchronize and check after every kernel (debug) */
+    MXP_ATTR_SPLITK_TILES = 3,    /* K chunk of one GEMM task, in tiles (default 8); results are bitwise
+                                     deterministic for a fixed value */
+    MXP_ATTR_LOOKAHEAD = 4,       /* reserved (the task list always carries one column of lookahead) */
+    MXP_ATTR_DEBUG_SYNC = 5,      /* 1 = synchronize and check after every kernel; 2 = GEMM-throughput
+                                     probe (GEMM tasks only, Ready pre-set, no POTRF: result is garbage) */
     MXP_ATTR_PROFILE = 6,         /* 1 = time every launch with CUDA events on its stream (mxp_chol_kernel_stats) */
     MXP_ATTR_GPU_LAUNCHES = 100,  /* (get only) kernels launched by the last factorization */
     MXP_ATTR_H2D_BYTES = 101,     /* (get only) host->device bytes moved by the last factorization */
@@ -178,6 +180,18 @@ int mxp_generate_kms_device(int64_t n, double rho, double* A_dev, int64_t lda, v
 enum mxp_kclass { MXP_KCLASS_CHAIN = 0, MXP_KCLASS_POTRF = 1, MXP_KCLASS_TRSM = 2, MXP_KCLASS_OTHER = 3 };
 int mxp_chol_kernel_stats(mxp_plan_t plan, int kernel_class, int64_t* launches, double* milliseconds,
                           double* flops);
+
+/*
+ * Scheduler diagnostics of the last factorization when MXP_ATTR_PROFILE is 1
+ * (%globaltimer nanoseconds, summed over CTAs): [0] GEMM busy, [1] GEMM wait,
+ * [2] TRSM busy, [3] TRSM wait, [4] #GEMM tasks, [5] #TRSM tasks, [6] first
+ * CTA start, [7] last CTA end, [8] #CTAs that ran tasks; then for each column
+ * k at [16+3k]: POTRF kernel start, Ready-wait done, end.
+ *   out      host array of `count` entries (may be NULL when count = 0) (arg 2)
+ *   count    capacity of out                                           (arg 3)
+ *   written  receives the number of entries available (16 + 3 Nt)       (arg 4)
+ */
+int mxp_chol_sched_diagnostics(mxp_plan_t plan, uint64_t* out, int64_t count, int64_t* written);
 
 /* Destroy a plan and every device resource it owns. NULL is a no-op. */
 void mxp_chol_plan_destroy(mxp_plan_t plan);

@@ -24,7 +24,7 @@ EXPORTS = [
     "mxp_chol_set_workspace", "mxp_chol_factor_device", "mxp_chol_factor", "mxp_chol_logdet",
     "mxp_precision_map_from_matrix_device", "mxp_generate_plgsy_device", "mxp_generate_kms_device",
     "mxp_chol_plan_destroy", "mxp_host_alloc", "mxp_host_free", "mxp_strerror", "mxp_last_error",
-    "mxp_chol_abi_version", "mxp_chol_kernel_stats",
+    "mxp_chol_abi_version", "mxp_chol_kernel_stats", "mxp_chol_sched_diagnostics",
 ]
 KCLASS = {"chain": 0, "potrf": 1, "trsm": 2, "other": 3}
 
@@ -76,6 +76,7 @@ def lib():
         L.mxp_last_error.restype = ctypes.c_char_p
         L.mxp_chol_abi_version.argtypes = []
         L.mxp_chol_kernel_stats.argtypes = [vp, i32, pi64, pd, pd]
+        L.mxp_chol_sched_diagnostics.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64), i64, pi64]
         _lib = L
         return L
 
@@ -200,6 +201,23 @@ class Plan:
                 self._h, c, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(fl)))
             out[name] = (n.value, ms.value, fl.value)
         return out
+
+    def sched_diagnostics(self) -> dict:
+        """Device-side scheduler timing of the last factorization (profile=1)."""
+        n = ctypes.c_int64()
+        _check("mxp_chol_sched_diagnostics", lib().mxp_chol_sched_diagnostics(self._h, None, 0, ctypes.byref(n)))
+        if n.value == 0:
+            return {}
+        buf = (ctypes.c_uint64 * n.value)()
+        _check("mxp_chol_sched_diagnostics", lib().mxp_chol_sched_diagnostics(self._h, buf, n.value, ctypes.byref(n)))
+        v = list(buf)
+        nt = (len(v) - 16) // 3
+        span = (v[7] - v[6]) / 1e6 if v[7] > v[6] else 0.0
+        pot = [((v[16 + 3 * k] - v[6]) / 1e6, (v[17 + 3 * k] - v[6]) / 1e6, (v[18 + 3 * k] - v[6]) / 1e6)
+               for k in range(nt)]
+        return {"gemm_busy_ms": v[0] / 1e6, "gemm_wait_ms": v[1] / 1e6, "trsm_busy_ms": v[2] / 1e6,
+                "trsm_wait_ms": v[3] / 1e6, "gemm_tasks": v[4], "trsm_tasks": v[5], "span_ms": span,
+                "ctas": v[8], "potrf_timeline_ms": pot}
 
     def logdet(self) -> float:
         v = ctypes.c_double()

@@ -1,16 +1,10 @@
 // engine.cu -- host runtime of the B200 engine and the C ABI (include/mxp_chol.h).
 //
-// Static schedule (Alg. 1): tasks are enumerated column
-// by column; the dependency table `Ready` of the paper becomes CUDA events
-// between two streams:
-//   stream U ("update", normal priority):  bulk GEMM chain of column k over
-//       n in [0, k-1)  -- waits Ready(column k-2)
-//   stream P ("panel", high priority):     last chain term n = k-1, POTRF(k),
-//       TRSM(column k) -- waits the bulk of column k; records Ready(column k)
-// so column k's latency-bound panel runs under column k+1's bulk update
-// (lookahead).  The split of the chain into [0,k-1) + {k-1} and the split-K
-// chunking are functions of (k, Nt, nb) only, so the result is bitwise
-// identical with or without lookahead, for any stream timing.
+// Static schedule (Alg. 1): the host enumerates the task
+// list once per plan -- column by column, with one column of lookahead -- and
+// uploads it; the device executes it with persistent CTAs that busy-wait on a
+// device-resident Ready table (sched_f64.cu).  The diagonal POTRFs run as one
+// small kernel per column on a high-priority stream on reserved SMs.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -50,7 +44,7 @@ struct mxp_plan_s {
     int device = 0;
     cudaStream_t user_stream = 0;
     int64_t hbm_cap = 0;
-    int64_t splitk_tiles = 16;
+    int64_t splitk_tiles = 8;  // bulk K chunk of a GEMM task, in tiles (swept: 1,2,4,8 -> 8 best)
     int lookahead = 1;
     int debug_sync = 0;
 
@@ -62,9 +56,18 @@ struct mxp_plan_s {
     double* d_logdet = nullptr;
     double* d_logdet_parts = nullptr;
     int32_t* d_slot = nullptr;
-    double* d_partial = nullptr;
+    int* d_flags = nullptr;        // counter, err, ready[T], gemm_done[T], trsm_done[T], blk_chunk[T*NB]
+    size_t flags_bytes = 0;
+    int* d_expected = nullptr;     // gemm_expected[T]
+    int4* d_items = nullptr;
+    double* d_wbuf = nullptr;
+    unsigned long long* d_stats = nullptr;  // diagnostics (profile=1)
+    std::vector<unsigned long long> h_stats;
     double* pool = nullptr;
-    size_t partial_doubles = 0;
+    std::vector<int4> items;       // host copy of the static task list
+    std::vector<int> expected;
+    bool list_uploaded = false;
+    int reserved_sms = 1;
 
     bool streams_ready = false;
     cudaStream_t sU = 0, sP = 0;
@@ -107,71 +110,121 @@ mxp_plan_s::~mxp_plan_s() {
 
 namespace {
 
-// Split-K chunking of the bulk chain of column k: a function of (k, Nt, nb)
-// only (never of the GPU count or timing), so results are reproducible.
-void bulk_chunks(const mxp_plan_s* p, int64_t k, int64_t& nchunks, int64_t& chunk_tiles) {
-    int64_t nterms = k - 1;  // n in [0, k-1)
-    if (nterms <= 0) {
-        nchunks = 0;
-        chunk_tiles = 1;
-        return;
-    }
-    const int64_t S = p->nb / 128;
-    int64_t blocks = (p->Nt - k) * S * S;
-    const int64_t target = 2 * 148;
-    int64_t want = blocks >= target ? 1 : (target + blocks - 1) / blocks;
-    int64_t maxc = (nterms + p->splitk_tiles - 1) / p->splitk_tiles;  // at most this many
-    want = std::min(want, std::max<int64_t>(1, std::min(maxc * 4, nterms)));
-    chunk_tiles = (nterms + want - 1) / want;
-    nchunks = (nterms + chunk_tiles - 1) / chunk_tiles;
+int64_t blocks_per_tile(int64_t nb) { return (nb / 64) * (nb / 128); }
+
+// 64x128 blocks of tile (m,k) that are computed: all of them off the diagonal,
+// the lower(-intersecting) ones on it (strictly upper blocks are never read).
+bool block_needed(int64_t m, int64_t k, int64_t b, int64_t nb) {
+    if (m != k) return true;
+    int64_t SR = nb / 64, bi = b % SR, bj = b / SR;
+    return (bi + 1) * 64 > bj * 128;
 }
 
-size_t partial_need(const mxp_plan_s* p) {
-    const int64_t S = p->nb / 128;
-    size_t best = 0;
-    for (int64_t k = 1; k < p->Nt; ++k) {
-        int64_t nch, ct;
-        bulk_chunks(p, k, nch, ct);
-        if (nch > 1) best = std::max(best, (size_t)((p->Nt - k) * S * S * nch) * 128 * 128);
-    }
-    return best;
+// chunks of column k: ceil((k-1)/KC) fixed-size chunks over [0, k-1), then {k-1}
+int64_t nchunks(int64_t k, int64_t KC) {
+    if (k == 0) return 0;
+    int64_t nfull = k >= 2 ? (k - 1 + KC - 1) / KC : 0;
+    return nfull + 1;
 }
 
-size_t workspace_need(const mxp_plan_s* p, size_t* pool_off, size_t* partial_off, size_t* slot_off) {
-    size_t off = 0;
-    off += 256;                                   // info
-    off += align_up(sizeof(double) * (p->Nt + 2), 256);  // logdet + parts
-    *slot_off = off;
+// The static task list (Alg. 1 enumerated column by column):
+//   iteration k:  (a) last GEMM chunk (n = k-1) of column k, diagonal tile first
+//                 (b) bulk GEMM chunks (n < k) of column k+1   [lookahead]
+//                 (c) TRSM row tasks of column k
+// POTRF(k) runs beside it (k_potrf_tile) once (a) has finished on tile (k,k).
+void build_task_list(mxp_plan_s* p) {
+    const int64_t Nt = p->Nt, nb = p->nb, KC = p->splitk_tiles, NB = blocks_per_tile(nb);
+    p->items.clear();
+    p->expected.assign(p->T, 0);
+    auto gemm_col = [&](int64_t k, int64_t c0, int64_t c1) {
+        for (int64_t c = c0; c < c1; ++c)
+            for (int64_t m = k; m < Nt; ++m)
+                for (int64_t b = 0; b < NB; ++b)
+                    if (block_needed(m, k, b, nb)) {
+                        p->items.push_back(make_int4(ITEM_GEMM, (int)m, (int)k, (int)((b << 16) | c)));
+                        p->expected[tile_index(Nt, m, k)]++;
+                    }
+    };
+    for (int64_t k = 0; k < Nt; ++k) {
+        if (k >= 1) {
+            int64_t last = nchunks(k, KC) - 1;
+            gemm_col(k, last, last + 1);
+        }
+        if (k + 1 < Nt) {
+            int64_t nb1 = nchunks(k + 1, KC) - 1;  // bulk chunks of column k+1
+            gemm_col(k + 1, 0, nb1);
+        }
+        if (p->debug_sync == 2) continue;  // GEMM-throughput probe: no TRSM tasks
+        for (int64_t m = k + 1; m < Nt; ++m)
+            for (int64_t r = 0; r < nb / 64; ++r) p->items.push_back(make_int4(ITEM_TRSM, (int)m, (int)k, (int)r));
+    }
+}
+
+size_t list_bytes(const mxp_plan_s* p) {
+    // count without building: GEMM tasks + TRSM tasks
+    const int64_t Nt = p->Nt, nb = p->nb, NB = blocks_per_tile(nb);
+    int64_t diag_blocks = 0;
+    for (int64_t b = 0; b < NB; ++b) diag_blocks += block_needed(0, 0, b, nb);
+    int64_t cnt = 0;
+    for (int64_t k = 1; k < Nt; ++k) cnt += nchunks(k, p->splitk_tiles) * ((Nt - k - 1) * NB + diag_blocks);
+    cnt += (Nt * (Nt - 1) / 2) * (nb / 64);
+    return sizeof(int4) * (size_t)cnt;
+}
+
+struct Layout {
+    size_t slot, flags, flags_bytes, expected, items, wbuf, stats, pool, total;
+};
+
+Layout layout(const mxp_plan_s* p) {
+    Layout L{};
+    size_t off = 256 + align_up(sizeof(double) * (p->Nt + 2), 256);  // info, logdet parts
+    L.slot = off;
     off += align_up(sizeof(int32_t) * p->T, 256);
-    *partial_off = off;
-    off += align_up(sizeof(double) * partial_need(p), 256);
-    *pool_off = off;
+    L.flags = off;
+    L.flags_bytes = sizeof(int) * (size_t)(2 + 3 * p->T + p->T * blocks_per_tile(p->nb));
+    off += align_up(L.flags_bytes, 256);
+    L.expected = off;
+    off += align_up(sizeof(int) * p->T, 256);
+    L.items = off;
+    off += align_up(list_bytes(p), 256);
+    L.wbuf = off;
+    off += align_up(sizeof(double) * (size_t)p->Nt * p->nb * 128, 256);
+    L.stats = off;
+    off += align_up(sizeof(unsigned long long) * (size_t)(16 + 3 * p->Nt), 256);
+    L.pool = off;
     off += sizeof(double) * (size_t)p->T * p->nb * p->nb;
-    return off;
+    L.total = off;
+    return L;
 }
+
+size_t workspace_need(const mxp_plan_s* p) { return layout(p).total; }
 
 void bind_workspace(mxp_plan_s* p) {
-    size_t pool_off, partial_off, slot_off;
-    size_t need = workspace_need(p, &pool_off, &partial_off, &slot_off);
+    Layout L = layout(p);
     if (!p->ws) {
         void* ptr = nullptr;
-        cudaError_t e = cudaMalloc(&ptr, need);
+        cudaError_t e = cudaMalloc(&ptr, L.total);
         if (e != cudaSuccess) {
             cudaGetLastError();
             g_last_error = std::string("cudaMalloc workspace: ") + cudaGetErrorString(e);
             throw CudaError{cudaErrorMemoryAllocation};
         }
         p->ws = (char*)ptr;
-        p->ws_bytes = need;
+        p->ws_bytes = L.total;
         p->ws_owned = true;
+        p->list_uploaded = false;
     }
     p->d_info = (int64_t*)p->ws;
     p->d_logdet = (double*)(p->ws + 256);
     p->d_logdet_parts = p->d_logdet + 1;
-    p->d_slot = (int32_t*)(p->ws + slot_off);
-    p->d_partial = (double*)(p->ws + partial_off);
-    p->pool = (double*)(p->ws + pool_off);
-    p->partial_doubles = partial_need(p);
+    p->d_slot = (int32_t*)(p->ws + L.slot);
+    p->d_flags = (int*)(p->ws + L.flags);
+    p->flags_bytes = L.flags_bytes;
+    p->d_expected = (int*)(p->ws + L.expected);
+    p->d_items = (int4*)(p->ws + L.items);
+    p->d_wbuf = (double*)(p->ws + L.wbuf);
+    p->d_stats = (unsigned long long*)(p->ws + L.stats);
+    p->pool = (double*)(p->ws + L.pool);
 }
 
 void ensure_streams(mxp_plan_s* p) {
@@ -188,13 +241,12 @@ void ensure_streams(mxp_plan_s* p) {
     }
     CK(cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
-    configure_kernels();
     p->streams_ready = true;
 }
 
 void dbg(mxp_plan_s* p, cudaStream_t s, const char* what) {
     CK(cudaGetLastError());
-    if (p->debug_sync) {
+    if (p->debug_sync == 1) {
         cudaError_t e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) {
             g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
@@ -250,92 +302,74 @@ void prof_collect(mxp_plan_s* p) {
     p->recs.clear();
 }
 
-// In-core FP64 factorization of the tiles already packed in the pool.
-// Streams sU / sP must already be ordered after the packing.
-void factor_incore_f64(mxp_plan_s* p) {
-    const int64_t Nt = p->Nt, nb = p->nb;
-    cudaStream_t sU = p->lookahead ? p->sU : p->sP;
-    cudaStream_t sP = p->sP;
-    for (int64_t k = 0; k < Nt; ++k) {
-        // ---- bulk chain of column k on U: n in [0, k-1), rows m in [k, Nt)
-        if (k >= 2 && p->lookahead) CK(cudaStreamWaitEvent(sU, p->ev_panel[k - 2], 0));
-        int64_t nch, ct;
-        bulk_chunks(p, k, nch, ct);
-        if (nch > 0) {
-            ChainArgs a{};
-            a.pool = p->pool;
-            a.slot = p->d_slot;
-            a.dinfo = p->d_info;
-            a.partial = p->d_partial;
-            a.Nt = Nt;
-            a.nb = nb;
-            a.k = k;
-            a.m0 = k;
-            a.mstride = 1;
-            a.mcount = Nt - k;
-            a.n0 = 0;
-            a.n1 = k - 1;
-            a.nchunks = nch;
-            a.chunk_tiles = ct;
-            const double nb3 = (double)nb * nb * nb;
-            {
-                Prof pr(p, sU, MXP_KCLASS_CHAIN, (double)(k - 1) * (2.0 * nb3 * (Nt - k - 1) + nb3),
-                        nch > 1 ? 2 : 1);
-                launch_chain_f64(a, sU);
-                ++p->launches;
-                dbg(p, sU, "chain bulk");
-                if (nch > 1) {
-                    launch_reduce_partials(a, sU);
-                    ++p->launches;
-                    dbg(p, sU, "reduce");
-                }
-            }
-        }
-        CK(cudaEventRecord(p->ev_bulk[k], sU));
-        // ---- panel of column k on P
-        CK(cudaStreamWaitEvent(sP, p->ev_bulk[k], 0));
-        if (k >= 1) {
-            ChainArgs a{};
-            a.pool = p->pool;
-            a.slot = p->d_slot;
-            a.dinfo = p->d_info;
-            a.partial = p->d_partial;
-            a.Nt = Nt;
-            a.nb = nb;
-            a.k = k;
-            a.m0 = k;
-            a.mstride = 1;
-            a.mcount = Nt - k;
-            a.n0 = k - 1;
-            a.n1 = k;
-            a.nchunks = 1;
-            a.chunk_tiles = 1;
-            const double nb3 = (double)nb * nb * nb;
-            Prof pr(p, sP, MXP_KCLASS_CHAIN, 2.0 * nb3 * (Nt - k - 1) + nb3);
-            launch_chain_f64(a, sP);
-            ++p->launches;
-            dbg(p, sP, "chain last");
-        }
-        {
-            PotrfArgs pa{p->pool, p->d_slot, p->d_info, Nt, nb, k};
-            const int S = (int)(nb / 128);
-            Prof pr(p, sP, MXP_KCLASS_POTRF, (double)nb * nb * nb / 3.0, 3 * S - 2);
-            p->launches += launch_potrf_tile_f64(pa, sP);
-            dbg(p, sP, "potrf");
-        }
-        if (k + 1 < Nt) {
-            TrsmArgs ta{p->pool, p->d_slot, p->d_info, Nt, nb, k, k + 1, 1, Nt - k - 1};
-            Prof pr(p, sP, MXP_KCLASS_TRSM, (double)nb * nb * nb * (Nt - k - 1));
-            launch_trsm_f64(ta, sP);
-            ++p->launches;
-            dbg(p, sP, "trsm");
-        }
-        CK(cudaEventRecord(p->ev_panel[k], sP));
+// In-core FP64 factorization of the tiles already packed in the pool: one
+// persistent static-schedule kernel on U + the POTRF kernels on P.
+void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0) {
+    const int64_t Nt = p->Nt, T = p->T;
+    if (!p->list_uploaded) {
+        build_task_list(p);
+        CK(cudaMemcpyAsync(p->d_items, p->items.data(), sizeof(int4) * p->items.size(), cudaMemcpyHostToDevice, s0));
+        CK(cudaMemcpyAsync(p->d_expected, p->expected.data(), sizeof(int) * T, cudaMemcpyHostToDevice, s0));
+        CK(cudaStreamSynchronize(s0));
+        p->list_uploaded = true;
     }
-    if (p->lookahead) {
-        // U has nothing left after the final panel; make P's tail the join point
-        CK(cudaStreamWaitEvent(sP, p->ev_bulk[Nt - 1], 0));
+    CK(cudaMemsetAsync(p->d_flags, 0, p->flags_bytes, s0));
+    if (p->debug_sync == 2)  // GEMM-throughput probe: every tile "ready", no POTRF (values are garbage)
+        CK(cudaMemsetAsync(p->d_flags + 2, 1, sizeof(int) * T, s0));
+    CK(cudaEventRecord(p->ev_start, s0));
+    CK(cudaStreamWaitEvent(p->sU, p->ev_start, 0));
+    CK(cudaStreamWaitEvent(p->sP, p->ev_start, 0));
+
+    SchedArgs a{};
+    a.pool = p->pool;
+    a.slot = p->d_slot;
+    a.dinfo = p->d_info;
+    a.counter = p->d_flags;
+    a.err = p->d_flags + 1;
+    a.ready = p->d_flags + 2;
+    a.gemm_done = a.ready + T;
+    a.trsm_done = a.gemm_done + T;
+    a.blk_chunk = a.trsm_done + T;
+    a.gemm_expected = p->d_expected;
+    a.Nt = Nt;
+    a.nb = p->nb;
+    a.KC = p->splitk_tiles;
+    a.NB = blocks_per_tile(p->nb);
+    a.items = p->d_items;
+    a.nitems = (int)p->items.size();
+    a.wbuf = p->d_wbuf;
+    a.reserved_sms = p->reserved_sms;
+    a.stats = nullptr;
+    const size_t nstat = 16 + 3 * (size_t)Nt;
+    if (p->profile) {
+        std::vector<unsigned long long> init(nstat, 0ull);
+        init[STAT_T0] = ~0ull;
+        CK(cudaMemcpyAsync(p->d_stats, init.data(), sizeof(unsigned long long) * nstat, cudaMemcpyHostToDevice, s0));
+        CK(cudaStreamSynchronize(s0));
+        a.stats = p->d_stats;
     }
+
+    int dev = p->device, nsm = 0;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    int occ = sched_ctas_per_sm();
+    const double nb3 = (double)p->nb * p->nb * p->nb;
+    const double total = (double)Nt * Nt * Nt * nb3 / 3.0;
+    {
+        Prof pr(p, p->sU, MXP_KCLASS_CHAIN, total - (double)Nt * nb3 / 3.0);
+        launch_sched(a, occ * nsm, p->sU);
+        ++p->launches;
+        dbg(p, p->sU, "sched");
+    }
+    {
+        Prof pr(p, p->sP, MXP_KCLASS_POTRF, (double)Nt * nb3 / 3.0, Nt);
+        if (p->debug_sync != 2) {
+            for (int64_t k = 0; k < Nt; ++k) launch_potrf_tile(a, k, p->sP);
+            p->launches += Nt;
+        }
+        CK(cudaGetLastError());
+    }
+    CK(cudaEventRecord(p->ev_done, p->sP));
+    CK(cudaStreamWaitEvent(p->sU, p->ev_done, 0));
 }
 
 int status_from_exception(const CudaError& e) {
@@ -410,7 +444,8 @@ int mxp_chol_plan_set(mxp_plan_t p, mxp_attr_t key, int64_t v) {
         p->hbm_cap = v;
         return MXP_OK;
     case MXP_ATTR_SPLITK_TILES:
-        if (v < 1) return -3;
+        if (v < 1 || v > 4096) return -3;
+        p->list_uploaded = false;
         if (p->ws && !p->ws_owned) return MXP_ESTATE;
         if (p->ws_owned) {
             cudaFree(p->ws);
@@ -420,10 +455,23 @@ int mxp_chol_plan_set(mxp_plan_t p, mxp_attr_t key, int64_t v) {
         p->splitk_tiles = v;
         return MXP_OK;
     case MXP_ATTR_LOOKAHEAD: p->lookahead = v ? 1 : 0; return MXP_OK;
-    case MXP_ATTR_DEBUG_SYNC: p->debug_sync = v ? 1 : 0; return MXP_OK;
+    case MXP_ATTR_DEBUG_SYNC:
+        if (v < 0 || v > 2) return -3;
+        if ((v == 2) != (p->debug_sync == 2)) p->list_uploaded = false;
+        p->debug_sync = (int)v;
+        return MXP_OK;
     case MXP_ATTR_PROFILE: p->profile = v ? 1 : 0; return MXP_OK;
     default: return -2;
     }
+}
+
+int mxp_chol_sched_diagnostics(mxp_plan_t p, uint64_t* out, int64_t count, int64_t* written) {
+    if (!p) return -1;
+    if (!out && count) return -2;
+    int64_t n = std::min<int64_t>(count, (int64_t)p->h_stats.size());
+    for (int64_t i = 0; i < n; ++i) out[i] = p->h_stats[i];
+    if (written) *written = (int64_t)p->h_stats.size();
+    return MXP_OK;
 }
 
 int mxp_chol_kernel_stats(mxp_plan_t p, int cls, int64_t* launches, double* ms, double* flops) {
@@ -458,16 +506,14 @@ int mxp_chol_plan_get(mxp_plan_t p, mxp_attr_t key, int64_t* v) {
 int mxp_chol_workspace_size(mxp_plan_t p, size_t* bytes) {
     if (!p) return -1;
     if (!bytes) return -2;
-    size_t a, b, c;
-    *bytes = workspace_need(p, &a, &b, &c);
+    *bytes = workspace_need(p);
     return MXP_OK;
 }
 
 int mxp_chol_set_workspace(mxp_plan_t p, void* dev, size_t bytes) {
     if (!p) return -1;
     if (!dev || ((uintptr_t)dev & 255)) return -2;
-    size_t a, b, c;
-    if (bytes < workspace_need(p, &a, &b, &c)) return -3;
+    if (bytes < workspace_need(p)) return -3;
     if (p->ws_owned && p->ws) {
         cudaSetDevice(p->device);
         cudaFree(p->ws);
@@ -475,6 +521,7 @@ int mxp_chol_set_workspace(mxp_plan_t p, void* dev, size_t bytes) {
     p->ws = (char*)dev;
     p->ws_bytes = bytes;
     p->ws_owned = false;
+    p->list_uploaded = false;
     return MXP_OK;
 }
 
@@ -504,11 +551,8 @@ int mxp_chol_factor_device(mxp_plan_t p, double* A, int64_t lda, int64_t* info) 
             ++p->launches;
             dbg(p, s0, "pack");
         }
-        CK(cudaEventRecord(p->ev_start, s0));
-        CK(cudaStreamWaitEvent(p->sU, p->ev_start, 0));
-        CK(cudaStreamWaitEvent(p->sP, p->ev_start, 0));
-        factor_incore_f64(p);
-        CK(cudaEventRecord(p->ev_done, p->sP));
+        factor_incore_f64(p, s0);
+        CK(cudaEventRecord(p->ev_done, p->sU));
         CK(cudaStreamWaitEvent(s0, p->ev_done, 0));
         {
             Prof pr(p, s0, MXP_KCLASS_OTHER, 0.0, 3);
@@ -519,10 +563,21 @@ int mxp_chol_factor_device(mxp_plan_t p, double* A, int64_t lda, int64_t* info) 
         }
         int64_t hinfo = 0;
         double ld = 0.0;
+        int herr = 0;
         CK(cudaMemcpyAsync(&hinfo, p->d_info, sizeof(int64_t), cudaMemcpyDeviceToHost, s0));
         CK(cudaMemcpyAsync(&ld, p->d_logdet, sizeof(double), cudaMemcpyDeviceToHost, s0));
+        CK(cudaMemcpyAsync(&herr, p->d_flags + 1, sizeof(int), cudaMemcpyDeviceToHost, s0));
         CK(cudaStreamSynchronize(s0));
+        if (herr) {
+            g_last_error = "static schedule: a Ready-table wait timed out (scheduler error)";
+            throw CudaError{cudaErrorLaunchTimeout};
+        }
         prof_collect(p);
+        if (p->profile) {
+            p->h_stats.resize(16 + 3 * (size_t)p->Nt);
+            CK(cudaMemcpy(p->h_stats.data(), p->d_stats, sizeof(unsigned long long) * p->h_stats.size(),
+                          cudaMemcpyDeviceToHost));
+        }
         *info = hinfo;
         p->have_result = (hinfo == 0);
         p->logdet = ld;

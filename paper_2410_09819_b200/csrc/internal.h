@@ -13,46 +13,40 @@ __host__ __device__ inline int64_t tile_index(int64_t Nt, int64_t i, int64_t j) 
     return j * Nt - j * (j - 1) / 2 + (i - j);
 }
 
-// ---- FP64 GEMM-chain update (Alg. 2, the hot loop P:265) -------
-// C(m,k)[bi,bj] -= sum_{n in [n0,n1)} A(m,n)[bi,:] * A(k,n)[bj,:]^T for the
-// rows m = m0 + y*mstride (y < mcount) of column k; 128x128 CTA blocks.
-// nchunks > 1 writes per-chunk partial sums to `partial` (deterministic
-// split-K), reduced in chunk order by launch_reduce_partials.
-struct ChainArgs {
+// ---- device-resident static schedule (sched_f64.cu) ----------------------
+// Task list entries (int4): {type, m, k, w}; GEMM: w = (block << 16) | chunk,
+// TRSM: w = 64-row block index.
+enum { ITEM_GEMM = 0, ITEM_TRSM = 1 };
+
+struct SchedArgs {
     double* pool;
     const int32_t* slot;
-    const int64_t* dinfo;   // abort flag: kernels exit when *dinfo != 0
-    double* partial;
+    int64_t* dinfo;            // LAPACK info (global row of the failed pivot), 0 = ok
+    int* err;                  // scheduler timeout flag
     int64_t Nt, nb;
-    int64_t k;              // output column
-    int64_t m0, mstride, mcount;
-    int64_t n0, n1;         // operand column range
-    int64_t nchunks, chunk_tiles;
+    int64_t KC;                // bulk chunk, in tiles
+    int64_t NB;                // 64x128 blocks per tile
+    const int4* items;
+    int nitems;
+    int* counter;              // next task ticket
+    int* ready;                // [T] Ready table: tile final
+    int* gemm_done;            // [T] completed GEMM tasks of the tile
+    const int* gemm_expected;  // [T]
+    int* trsm_done;            // [T] completed TRSM row tasks of the tile
+    int* blk_chunk;            // [T*NB] chunks applied to each output block
+    double* wbuf;              // [Nt][nb/128][128*128] inverses of L_kk's diagonal blocks
+    int reserved_sms;          // SMs (smid < this) left to the POTRF kernels
+    unsigned long long* stats; // optional diagnostics (MXP_ATTR_PROFILE): see STAT_*
 };
-void launch_chain_f64(const ChainArgs& a, cudaStream_t s);
-void launch_reduce_partials(const ChainArgs& a, cudaStream_t s);
-
-// ---- diagonal-tile POTRF (Alg. 2), right-looking on 128 blocks
-struct PotrfArgs {
-    double* pool;
-    const int32_t* slot;
-    int64_t* dinfo;
-    int64_t Nt, nb, k;
+// diagnostics layout (ns from %globaltimer, summed over CTAs)
+enum {
+    STAT_GEMM_BUSY = 0, STAT_GEMM_WAIT = 1, STAT_TRSM_BUSY = 2, STAT_TRSM_WAIT = 3,
+    STAT_GEMM_N = 4, STAT_TRSM_N = 5, STAT_T0 = 6, STAT_TEND = 7, STAT_CTAS = 8,
+    STAT_POTRF = 16  // + 3k: kernel start, wait done, end
 };
-// Runs the whole in-tile sequence (base POTRF, in-tile TRSM, trailing update
-// per 128-block); returns the number of kernels launched.
-int launch_potrf_tile_f64(const PotrfArgs& a, cudaStream_t s);
-
-// ---- TRSM of the tiles below the diagonal (Alg. 2, G3) --------
-// X L_kk^T = C for the rows m = m0 + y*mstride of column k, in place.
-struct TrsmArgs {
-    double* pool;
-    const int32_t* slot;
-    const int64_t* dinfo;
-    int64_t Nt, nb, k;
-    int64_t m0, mstride, mcount;
-};
-void launch_trsm_f64(const TrsmArgs& a, cudaStream_t s);
+int sched_ctas_per_sm();
+void launch_sched(const SchedArgs& a, int grid, cudaStream_t s);
+void launch_potrf_tile(const SchedArgs& a, int64_t k, cudaStream_t s);
 
 // ---- layout / utility kernels --------------------------------------------
 // lda matrix <-> pool tiles (padding: zeros, 1 on the padded diagonal)
@@ -67,7 +61,5 @@ void launch_logdet(const double* pool, const int32_t* slot, int64_t Nt, int64_t 
 void launch_tile_norms(const double* A, int64_t lda, int64_t n, int64_t nb, double* norms,
                        cudaStream_t s);
 
-// Shared-memory bytes the kernels request (for attribute setup).
-void configure_kernels();
 
 }  // namespace mxp

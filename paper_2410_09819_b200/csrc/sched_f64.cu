@@ -1,0 +1,456 @@
+// sched_f64.cu -- the FP64 left-looking tile Cholesky as a device-resident
+// static schedule (Alg. 1, Alg. 2).
+//
+// The paper's static scheduler gives every host thread a fixed, cyclic list of
+// tasks and resolves dependencies by busy-waiting on a write-once progress
+// table `Ready`.  On B200 the "threads" are persistent CTAs of
+// one kernel (k_sched): they walk ONE fixed task list in order (each CTA takes
+// the next task with an atomic ticket), and `Ready` lives in global memory
+// (acquire/release flags).  Tasks are the paper's GEMM/SYRK updates and TRSMs
+// at 64x128-block x K-chunk granularity; the POTRF of each diagonal tile runs
+// in its own kernel (k_potrf_tile) on a reserved SM on a high-priority
+// stream, spinning on the same table, so it never waits behind GEMM CTAs.
+//
+// Determinism: the accumulation order of every output block is fixed (chunks
+// are applied in chunk order, guarded by a per-block chunk counter; the
+// chunking is a function of (k, KC) only), so results are bitwise identical
+// run to run, whatever CTA executes what.
+//
+// Deadlock freedom: a task only waits on tasks that precede it in the list;
+// tasks are taken in list order by resident CTAs, so every awaited task is
+// done or running.  Every wait has a 20 s timeout (error flag, no hang).
+#include <math.h>
+
+#include "dmma_gemm.cuh"
+
+namespace mxp {
+
+namespace {
+
+constexpr uint64_t WAIT_TIMEOUT_NS = 20ull * 1000 * 1000 * 1000;
+
+// Thread 0 waits until *flag >= target.  Returns false to abort (failure in an
+// earlier column at or before `col`, or timeout).
+__device__ bool wait_flag(const int* flag, int target, const SchedArgs& a, int64_t col) {
+    if (ld_acquire(flag) >= target) return true;
+    uint64_t t0 = globaltimer();
+    unsigned ns = 32;
+    while (ld_acquire(flag) < target) {
+        int64_t info = *(volatile int64_t*)a.dinfo;
+        if (info != 0 && col >= (info - 1) / a.nb) return false;
+        if (*(volatile int*)a.err) return false;
+        if (globaltimer() - t0 > WAIT_TIMEOUT_NS) {
+            atomicExch(a.err, 1);
+            return false;
+        }
+        __nanosleep(ns);
+        if (ns < 1024) ns *= 2;
+    }
+    return true;
+}
+
+__device__ __forceinline__ bool skip_column(const SchedArgs& a, int64_t col) {
+    int64_t info = *(volatile int64_t*)a.dinfo;
+    return (info != 0 && col >= (info - 1) / a.nb) || *(volatile int*)a.err;
+}
+
+// chunk c of column k: fixed-size chunks over [0, k-1), then the singleton {k-1}
+__device__ __forceinline__ void chunk_range(int64_t k, int64_t c, int64_t KC, int64_t& n0, int64_t& n1) {
+    int64_t nfull = k >= 2 ? (k - 1 + KC - 1) / KC : 0;
+    if (c < nfull) {
+        n0 = c * KC;
+        n1 = n0 + KC < k - 1 ? n0 + KC : k - 1;
+    } else {
+        n0 = k - 1;
+        n1 = k;
+    }
+}
+
+template <class C>
+__device__ __forceinline__ void zero_acc(double (&acc)[C::MI][C::NI][2]) {
+#pragma unroll
+    for (int mi = 0; mi < C::MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < C::NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+}
+
+// ---------------------------------------------------------------- GEMM task
+// C(m,k)[block b] -= sum_{n in chunk c} A(m,n)[rows] A(k,n)[cols]^T
+__device__ bool task_gemm(const SchedArgs& a, int64_t m, int64_t k, int64_t b, int64_t c, double* smem,
+                          int* s_flag) {
+    const int64_t Nt = a.Nt, nb = a.nb;
+    const int64_t SR = nb / CC::BM;
+    const int64_t bi = b % SR, bj = b / SR;
+    const int64_t t = tile_index(Nt, m, k);
+    int64_t n0, n1;
+    chunk_range(k, c, a.KC, n0, n1);
+    int* chunk_flag = a.blk_chunk + t * a.NB + b;
+    uint64_t tw0 = 0;
+    if (threadIdx.x == 0) {
+        if (a.stats) tw0 = globaltimer();
+        bool ok = true;
+        for (int64_t n = n0; n < n1 && ok; ++n) {
+            ok = wait_flag(a.ready + tile_index(Nt, m, n), 1, a, k) &&
+                 wait_flag(a.ready + tile_index(Nt, k, n), 1, a, k);
+        }
+        if (ok) ok = wait_flag(chunk_flag, (int)c, a, k);
+        *s_flag = ok;
+        if (a.stats) {
+            uint64_t tw1 = globaltimer();
+            atomicAdd(a.stats + STAT_GEMM_WAIT, tw1 - tw0);
+            tw0 = tw1;
+        }
+    }
+    __syncthreads();
+    if (!*s_flag) return false;
+
+    const int64_t kper = nb / BK;
+    const int nk = (int)((n1 - n0) * kper);
+    const int64_t roff = bi * CC::BM, coff = bj * CC::BN;
+    double* pool = a.pool;
+    const int32_t* slot = a.slot;
+    // Stateful operand walk: the mainloop asks for K-chunks in increasing
+    // order, so tile pointers are looked up only when the walk enters the next
+    // tile n (once per nb/BK stages) -- no slot loads or divisions per stage.
+    int64_t cur_n = n0, kcol = 0;
+    const double* ta = tile_ptr(pool, slot, Nt, nb, m, n0) + roff;
+    const double* tb = tile_ptr(pool, slot, Nt, nb, k, n0) + coff;
+    auto src = [&](int, const double*& pa, const double*& pb) {
+        if (kcol == nb) {
+            kcol = 0;
+            ++cur_n;
+            ta = tile_ptr(pool, slot, Nt, nb, m, cur_n) + roff;
+            tb = tile_ptr(pool, slot, Nt, nb, k, cur_n) + coff;
+        }
+        pa = ta + kcol * nb;
+        pb = tb + kcol * nb;
+        kcol += BK;
+    };
+    double acc[CC::MI][CC::NI][2];
+    zero_acc<CC>(acc);
+    gemm_mainloop<CC>(acc, src, nb, nb, nk, smem);
+    double* Ct = tile_ptr(pool, slot, Nt, nb, m, k) + roff + coff * nb;
+#pragma unroll
+    for (int mi = 0; mi < CC::MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < CC::NI; ++ni)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                int r, cc;
+                frag_pos<CC>(mi, ni, i, r, cc);
+                double* p = Ct + r + (int64_t)cc * nb;
+                __stcg(p, __ldcg(p) - acc[mi][ni][i]);
+            }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        st_release(chunk_flag, (int)c + 1);
+        atom_add_release(a.gemm_done + t, 1);
+        if (a.stats) {
+            atomicAdd(a.stats + STAT_GEMM_BUSY, globaltimer() - tw0);
+            atomicAdd(a.stats + STAT_GEMM_N, 1ull);
+        }
+    }
+    return true;
+}
+
+// ---------------------------------------------------------------- TRSM task
+// X L_kk^T = C on rows [64r, 64r+64) of tile (m,k), in place (Alg. 2
+// P:269, G3).  Blocked by 128 columns J with the inverses W_J = L_JJ^-1 from
+// the POTRF kernel (MAGMA-style):  X[:,J] = (C[:,J] - X[:,<J] L[J,<J]^T) W_J^T.
+__device__ bool task_trsm(const SchedArgs& a, int64_t m, int64_t k, int64_t r, double* smem, int* s_flag) {
+    const int64_t Nt = a.Nt, nb = a.nb, S = nb / 128;
+    const int64_t t = tile_index(Nt, m, k);
+    uint64_t tw0 = 0;
+    if (threadIdx.x == 0) {
+        if (a.stats) tw0 = globaltimer();
+        bool ok = wait_flag(a.ready + tile_index(Nt, k, k), 1, a, k) &&
+                  wait_flag(a.gemm_done + t, a.gemm_expected[t], a, k);
+        *s_flag = ok;
+        if (a.stats) {
+            uint64_t tw1 = globaltimer();
+            atomicAdd(a.stats + STAT_TRSM_WAIT, tw1 - tw0);
+            tw0 = tw1;
+        }
+    }
+    __syncthreads();
+    if (!*s_flag) return false;
+    double* X = tile_ptr(a.pool, a.slot, Nt, nb, m, k) + r * 64;
+    const double* L = tile_ptr(a.pool, a.slot, Nt, nb, k, k);
+    const double* Wk = a.wbuf + k * S * (128 * 128);
+    for (int64_t J = 0; J < S; ++J) {
+        double acc[CC::MI][CC::NI][2];
+        zero_acc<CC>(acc);
+        if (J > 0) {
+            auto src = [&](int it, const double*& pa, const double*& pb) {
+                int64_t kcol = (int64_t)it * BK;
+                pa = X + kcol * nb;
+                pb = L + J * 128 + kcol * nb;
+            };
+            gemm_mainloop<CC>(acc, src, nb, nb, (int)(J * 128 / BK), smem);
+        }
+        double* XJ = X + J * 128 * nb;
+#pragma unroll
+        for (int mi = 0; mi < CC::MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < CC::NI; ++ni)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    int rr, cc;
+                    frag_pos<CC>(mi, ni, i, rr, cc);
+                    double* p = XJ + rr + (int64_t)cc * nb;
+                    __stcg(p, __ldcg(p) - acc[mi][ni][i]);
+                }
+        __threadfence_block();
+        __syncthreads();
+        zero_acc<CC>(acc);
+        const double* W = Wk + J * (128 * 128);
+        auto src2 = [&](int it, const double*& pa, const double*& pb) {
+            int64_t kcol = (int64_t)it * BK;
+            pa = XJ + kcol * nb;
+            pb = W + kcol * 128;
+        };
+        gemm_mainloop<CC>(acc, src2, nb, 128, 128 / BK, smem);
+#pragma unroll
+        for (int mi = 0; mi < CC::MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < CC::NI; ++ni)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    int rr, cc;
+                    frag_pos<CC>(mi, ni, i, rr, cc);
+                    __stcg(XJ + rr + (int64_t)cc * nb, acc[mi][ni][i]);
+                }
+        __threadfence_block();
+        __syncthreads();
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int old = atom_add_release(a.trsm_done + t, 1);
+        if (old + 1 == (int)(nb / 64)) st_release(a.ready + t, 1);
+        if (a.stats) {
+            atomicAdd(a.stats + STAT_TRSM_BUSY, globaltimer() - tw0);
+            atomicAdd(a.stats + STAT_TRSM_N, 1ull);
+        }
+    }
+    return true;
+}
+
+}  // namespace
+
+// ------------------------------------------------------ the static schedule
+__global__ void __launch_bounds__(CC::NT, 3) k_sched(SchedArgs a) {
+    if ((int)smid() < a.reserved_sms) return;  // leave these SMs to the POTRF kernels
+    extern __shared__ __align__(16) double smem[];
+    // The task ticket and wait verdict live in the padding columns of the A
+    // stage buffer (doubles BM..BM+PAD-1 of row 0 are never read or written by
+    // the pipeline): any static __shared__ byte would push 3 x (76.8 KB + 1 KB
+    // reserve) over the SM's 228 KB and drop occupancy from 3 CTAs/SM to 2.
+    static_assert(PAD * 8 >= 2 * sizeof(int), "scratch must fit in the padding");
+    int& s_idx = *reinterpret_cast<int*>(smem + CC::BM);
+    int& s_flag = *(reinterpret_cast<int*>(smem + CC::BM) + 1);
+    if (a.stats && threadIdx.x == 0) {
+        atomicMin(a.stats + STAT_T0, globaltimer());
+        atomicAdd(a.stats + STAT_CTAS, 1ull);
+    }
+    while (true) {
+        if (threadIdx.x == 0) {
+            int i = atomicAdd(a.counter, 1);
+            // -1: list exhausted; -2: task of a failed column (skip)
+            if (i >= a.nitems) i = -1;
+            else if (skip_column(a, a.items[i].z)) i = -2;
+            s_idx = i;
+        }
+        __syncthreads();
+        const int idx = s_idx;
+        __syncthreads();
+        if (idx == -1) break;
+        if (idx == -2) continue;
+        const int4 it = a.items[idx];
+        const int64_t m = it.y, k = it.z;
+        if (it.x == ITEM_GEMM) {
+            task_gemm(a, m, k, it.w >> 16, it.w & 0xFFFF, smem, &s_flag);
+        } else {
+            task_trsm(a, m, k, it.w, smem, &s_flag);
+        }
+        __syncthreads();
+    }
+    if (a.stats && threadIdx.x == 0) atomicMax(a.stats + STAT_TEND, globaltimer());
+}
+
+// ------------------------------------------------- POTRF of a diagonal tile
+// One CTA (256 threads) on a reserved SM: waits until every GEMM/SYRK task of
+// tile (k,k) is done, then factors it right-looking in 128 blocks:
+//   L_JJ = chol(D_JJ) (packed in smem, kij order) and W_J = L_JJ^-1,
+//   D[I,J] = D[I,J] W_J^T (I > J),  D[I,J'] -= D[I,J] D[J',J]^T (J < J' <= I).
+// Writes L_kk in place, W_J to wbuf (for the TRSM tasks), sets Ready(k,k).
+namespace {
+constexpr int PK = 128 * 129 / 2;  // packed lower-triangle length
+__device__ __forceinline__ int pidx_c(int i, int j) { return j * 128 - j * (j - 1) / 2 + (i - j); }  // col-major
+__device__ __forceinline__ int pidx_r(int i, int j) { return i * (i + 1) / 2 + j; }                  // row-major
+
+template <class C>
+__device__ void store_acc(double (&acc)[C::MI][C::NI][2], double* Ct, int64_t ld, bool subtract) {
+#pragma unroll
+    for (int mi = 0; mi < C::MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < C::NI; ++ni)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                int r, c;
+                frag_pos<C>(mi, ni, i, r, c);
+                double* p = Ct + r + (int64_t)c * ld;
+                __stcg(p, subtract ? __ldcg(p) - acc[mi][ni][i] : acc[mi][ni][i]);
+            }
+}
+}  // namespace
+
+__global__ void __launch_bounds__(256, 1) k_potrf_tile(SchedArgs a, int64_t k) {
+    extern __shared__ __align__(16) double smem[];
+    __shared__ int s_flag;
+    const int t = threadIdx.x;
+    const int64_t Nt = a.Nt, nb = a.nb;
+    const int S = (int)(nb / 128);
+    const int64_t tk = tile_index(Nt, k, k);
+    if (t == 0) {
+        if (a.stats) a.stats[STAT_POTRF + 3 * k] = globaltimer();
+        bool ok = !skip_column(a, k);
+        if (ok && k > 0) ok = wait_flag(a.gemm_done + tk, a.gemm_expected[tk], a, k);
+        s_flag = ok;
+        if (a.stats) a.stats[STAT_POTRF + 3 * k + 1] = globaltimer();
+    }
+    __syncthreads();
+    if (!s_flag) return;
+    double* D = tile_ptr(a.pool, a.slot, Nt, nb, k, k);
+    double* Wk = a.wbuf + k * S * (128 * 128);
+    double* P = smem;        // packed L_JJ, column-major lower
+    double* R = smem + PK;   // packed W_J, row-major lower
+
+    for (int J = 0; J < S; ++J) {
+        double* DJJ = D + (int64_t)J * 128 * (1 + nb);
+        // ---- load D_JJ (lower) into packed smem
+        for (int idx = t; idx < 128 * 128; idx += 256) {
+            int c = idx >> 7, r = idx & 127;
+            if (r >= c) P[pidx_c(r, c)] = __ldcg(DJJ + r + (int64_t)c * nb);
+        }
+        if (t == 0) s_flag = 0;
+        __syncthreads();
+        // ---- unblocked right-looking Cholesky; thread = (row i, column parity p)
+        const int i = t & 127, par = t >> 7;
+        for (int j = 0; j < 128; ++j) {
+            if (t == 0) {
+                double d = P[pidx_c(j, j)];
+                if (!(d > 0.0)) {
+                    s_flag = 1;
+                    *(volatile int64_t*)a.dinfo = k * nb + (int64_t)J * 128 + j + 1;
+                } else {
+                    P[pidx_c(j, j)] = sqrt(d);
+                }
+            }
+            __syncthreads();
+            if (s_flag) return;
+            if (t > j && t < 128) P[pidx_c(t, j)] = P[pidx_c(t, j)] / P[pidx_c(j, j)];
+            __syncthreads();
+            if (i > j) {
+                const double lij = P[pidx_c(i, j)];
+                int c0 = j + 1;
+                if ((c0 & 1) != par) ++c0;
+                for (int c = c0; c <= i; c += 2) P[pidx_c(i, c)] -= lij * P[pidx_c(c, j)];
+            }
+            __syncthreads();
+        }
+        // ---- W = L^-1 by forward substitution, one column per thread (t < 128)
+        if (t < 128) {
+            const int c = t;
+            for (int r = 0; r < 128; ++r) {
+                double s0 = (r == c) ? 1.0 : 0.0, s1 = 0.0;
+                int q = 0;
+                for (; q + 1 < r; q += 2) {
+                    double w0 = (q >= c) ? R[pidx_r(q, c)] : 0.0;
+                    double w1 = (q + 1 >= c) ? R[pidx_r(q + 1, c)] : 0.0;
+                    s0 -= P[pidx_c(r, q)] * w0;
+                    s1 -= P[pidx_c(r, q + 1)] * w1;
+                }
+                if (q < r) s0 -= P[pidx_c(r, q)] * ((q >= c) ? R[pidx_r(q, c)] : 0.0);
+                if (r >= c) R[pidx_r(r, c)] = (s0 + s1) / P[pidx_c(r, r)];
+            }
+        }
+        __syncthreads();
+        // ---- write L_JJ (zero upper) and W_J (col-major, zero upper)
+        double* W = Wk + J * (128 * 128);
+        for (int idx = t; idx < 128 * 128; idx += 256) {
+            int c = idx >> 7, r = idx & 127;
+            __stcg(DJJ + r + (int64_t)c * nb, r >= c ? P[pidx_c(r, c)] : 0.0);
+            __stcg(W + r + c * 128, r >= c ? R[pidx_r(r, c)] : 0.0);
+        }
+        __threadfence_block();
+        __syncthreads();
+        // ---- TRSM of the blocks below: D[I,J] = D[I,J] W^T (mainloop consumes
+        //      all of D[I,J] before the epilogue overwrites it)
+        for (int I = J + 1; I < S; ++I) {
+            double acc[PC::MI][PC::NI][2];
+            zero_acc<PC>(acc);
+            double* DIJ = D + (int64_t)I * 128 + (int64_t)J * 128 * nb;
+            auto src = [&](int it, const double*& pa, const double*& pb) {
+                pa = DIJ + (int64_t)it * BK * nb;
+                pb = W + it * BK * 128;
+            };
+            gemm_mainloop<PC>(acc, src, nb, 128, 128 / BK, smem);
+            store_acc<PC>(acc, DIJ, nb, false);
+            __threadfence_block();
+            __syncthreads();
+        }
+        // ---- trailing update inside the tile
+        for (int Jp = J + 1; Jp < S; ++Jp)
+            for (int I = Jp; I < S; ++I) {
+                double acc[PC::MI][PC::NI][2];
+                zero_acc<PC>(acc);
+                const double* Ab = D + (int64_t)I * 128 + (int64_t)J * 128 * nb;
+                const double* Bb = D + (int64_t)Jp * 128 + (int64_t)J * 128 * nb;
+                auto src = [&](int it, const double*& pa, const double*& pb) {
+                    pa = Ab + (int64_t)it * BK * nb;
+                    pb = Bb + (int64_t)it * BK * nb;
+                };
+                gemm_mainloop<PC>(acc, src, nb, nb, 128 / BK, smem);
+                store_acc<PC>(acc, D + (int64_t)I * 128 + (int64_t)Jp * 128 * nb, nb, true);
+                __threadfence_block();
+                __syncthreads();
+            }
+    }
+    __threadfence();
+    __syncthreads();
+    if (t == 0) {
+        st_release(a.ready + tk, 1);
+        if (a.stats) a.stats[STAT_POTRF + 3 * k + 2] = globaltimer();
+    }
+}
+
+constexpr int POTRF_SMEM = (2 * PK * 8 > PC::SMEM_BYTES) ? 2 * PK * 8 : PC::SMEM_BYTES;
+
+void configure_sched() {
+    static bool done = false;
+    if (done) return;
+    cudaFuncSetAttribute(k_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM_BYTES);
+    cudaFuncSetAttribute(k_potrf_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF_SMEM);
+    done = true;
+}
+
+int sched_ctas_per_sm() {
+    int occ = 0;
+    configure_sched();
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sched, CC::NT, CC::SMEM_BYTES);
+    return occ;
+}
+
+void launch_sched(const SchedArgs& a, int grid, cudaStream_t s) {
+    configure_sched();
+    k_sched<<<grid, CC::NT, CC::SMEM_BYTES, s>>>(a);
+}
+
+void launch_potrf_tile(const SchedArgs& a, int64_t k, cudaStream_t s) {
+    configure_sched();
+    k_potrf_tile<<<1, 256, POTRF_SMEM, s>>>(a, k);
+}
+
+}  // namespace mxp

@@ -9,7 +9,12 @@ for spec in sys.argv[1:]:
     A = torch.empty((n, n), dtype=torch.float64, device="cuda").T
     m.generate_plgsy_device(A, 42)
     plan = m.Plan(n, nb)
+    if os.environ.get("KC"):
+        plan.set("splitk_tiles", int(os.environ["KC"]))
+    if os.environ.get("PROBE"):
+        plan.set("debug_sync", 2)
     plan.use_torch_workspace()
+    plan.set("profile", 1)
     B = torch.empty_like(A.T).T
     ts = []
     for r in range(3):
@@ -26,7 +31,21 @@ for spec in sys.argv[1:]:
     x = torch.randn(n, 1, dtype=torch.float64, device="cuda")
     r = (A @ x - L @ (L.T @ x)).norm() / (torch.linalg.matrix_norm(A, 2 if n <= 4096 else 'fro') * x.norm())
     print(f"n={n} nb={nb} info={info} t={t:.3f}s {n**3/3/t/1e12:.2f} TF/s probe={r.item():.2e} launches={plan.get('gpu_launches')}", flush=True)
+    for k, (nl, ms, fl) in plan.kernel_stats().items():
+        print(f"    {k:6s} launches={nl:5d} ms={ms:9.2f} TF/s={(fl/(ms/1e3)/1e12 if ms and fl else 0):6.2f}", flush=True)
+    d = plan.sched_diagnostics()
+    if d:
+        pot = d.pop("potrf_timeline_ms")
+        print("    sched", {k: (round(v, 2) if isinstance(v, float) else v) for k, v in d.items()}, flush=True)
+        durs = [e - w for (s0, w, e) in pot]
+        gaps = [pot[i][1] - pot[i - 1][2] for i in range(1, len(pot))]
+        print(f"    KC={plan.get('splitk_tiles')} busy/CTA gemm {d['gemm_busy_ms']/d['ctas']:.1f} ms wait {d['gemm_wait_ms']/d['ctas']:.1f} trsm {d['trsm_busy_ms']/d['ctas']:.1f} ms", flush=True)
+        print(f"    potrf: mean dur {sum(durs)/len(durs):.3f} ms, max {max(durs):.3f}; last 6 (start,ready,end): "
+              + str([tuple(round(x, 2) for x in t) for t in pot[-6:]]), flush=True)
+        print(f"    potrf ready-wait gaps (ms) first 8: {[round(g,3) for g in gaps[:8]]} last 8: {[round(g,3) for g in gaps[-8:]]}", flush=True)
     del B, L
+    if os.environ.get("NO_CUSOLVER"):
+        continue
     S = A.T.contiguous()
     ts = []
     for r in range(2):
