@@ -54,9 +54,16 @@ using PC = GemmCfg<128, 128, 2, 4, 3>;  // single-CTA POTRF kernel: 256 threads
 // Operand source: for K-chunk `it` (BK columns), the address of element
 // (row0, kcol) of the A and B panels; both column-major with ld.
 // `src` is a functor: src(it, &pa, &pb).
-template <class C, class Src>
+struct NoPost {
+    static constexpr bool active = false;
+    __device__ void operator()(int, double*, double*) const {}
+};
+
+// `post(it, sA, sB)` (if Post::active) transforms stage `it` in shared memory
+// after it has landed and before it is consumed (used for on-the-fly casts).
+template <class C, class Src, class Post = NoPost>
 __device__ __forceinline__ void gemm_mainloop(double (&acc)[C::MI][C::NI][2], const Src& src, int64_t lda,
-                                              int64_t ldb, int nk, double* smem) {
+                                              int64_t ldb, int nk, double* smem, const Post& post = Post()) {
     constexpr int BM = C::BM, BN = C::BN, STAGES = C::STAGES, NT = C::NT;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
@@ -93,6 +100,11 @@ __device__ __forceinline__ void gemm_mainloop(double (&acc)[C::MI][C::NI][2], co
         int nxt = it + STAGES - 1;
         if (nxt < nk) load_stage(nxt % STAGES, nxt);
         cp_async_commit();
+        if constexpr (Post::active) {
+            double* wA = smem + (it % STAGES) * C::STAGE_DOUBLES;
+            post(it, wA, wA + BK * C::LDA_S);
+            __syncthreads();
+        }
         const double* sA = smem + (it % STAGES) * C::STAGE_DOUBLES;
         const double* sB = sA + BK * C::LDA_S;
 #pragma unroll

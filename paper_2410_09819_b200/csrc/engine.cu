@@ -68,6 +68,10 @@ struct mxp_plan_s {
     std::vector<int> expected;
     bool list_uploaded = false;
     int reserved_sms = 1;
+    bool mxp = false;              // any tile below FP64
+    uint8_t* d_prec = nullptr;
+    unsigned long long* d_amax_x = nullptr;
+    double* d_amax_s = nullptr;
 
     bool streams_ready = false;
     cudaStream_t sU = 0, sP = 0;
@@ -157,6 +161,10 @@ void build_task_list(mxp_plan_s* p) {
         if (p->debug_sync == 2) continue;  // GEMM-throughput probe: no TRSM tasks
         for (int64_t m = k + 1; m < Nt; ++m)
             for (int64_t r = 0; r < nb / 64; ++r) p->items.push_back(make_int4(ITEM_TRSM, (int)m, (int)k, (int)r));
+        for (int64_t m = k + 1; m < Nt; ++m)
+            if (p->map[tile_index(Nt, m, k)] != MXP_FP64)
+                for (int64_t r = 0; r < nb / 64; ++r)
+                    p->items.push_back(make_int4(ITEM_QUANT, (int)m, (int)k, (int)r));
     }
 }
 
@@ -168,11 +176,13 @@ size_t list_bytes(const mxp_plan_s* p) {
     int64_t cnt = 0;
     for (int64_t k = 1; k < Nt; ++k) cnt += nchunks(k, p->splitk_tiles) * ((Nt - k - 1) * NB + diag_blocks);
     cnt += (Nt * (Nt - 1) / 2) * (nb / 64);
+    for (int64_t k = 0; k < Nt; ++k)
+        for (int64_t m = k + 1; m < Nt; ++m) cnt += (p->map[tile_index(Nt, m, k)] != MXP_FP64) * (nb / 64);
     return sizeof(int4) * (size_t)cnt;
 }
 
 struct Layout {
-    size_t slot, flags, flags_bytes, expected, items, wbuf, stats, pool, total;
+    size_t slot, flags, flags_bytes, expected, items, wbuf, stats, prec, amax_x, amax_s, pool, total;
 };
 
 Layout layout(const mxp_plan_s* p) {
@@ -181,7 +191,9 @@ Layout layout(const mxp_plan_s* p) {
     L.slot = off;
     off += align_up(sizeof(int32_t) * p->T, 256);
     L.flags = off;
-    L.flags_bytes = sizeof(int) * (size_t)(2 + 3 * p->T + p->T * blocks_per_tile(p->nb));
+    // counter, err, ready, gemm_done, trsm_done, quant_done, blk_chunk; then amax_x (u64, zeroed too)
+    L.flags_bytes = align_up(sizeof(int) * (size_t)(2 + 4 * p->T + p->T * blocks_per_tile(p->nb)), 8) +
+                    sizeof(unsigned long long) * (size_t)p->T;
     off += align_up(L.flags_bytes, 256);
     L.expected = off;
     off += align_up(sizeof(int) * p->T, 256);
@@ -191,6 +203,10 @@ Layout layout(const mxp_plan_s* p) {
     off += align_up(sizeof(double) * (size_t)p->Nt * p->nb * 128, 256);
     L.stats = off;
     off += align_up(sizeof(unsigned long long) * (size_t)(16 + 3 * p->Nt), 256);
+    L.prec = off;
+    off += align_up((size_t)p->T, 256);
+    L.amax_s = off;
+    off += align_up(sizeof(double) * (size_t)p->T, 256);
     L.pool = off;
     off += sizeof(double) * (size_t)p->T * p->nb * p->nb;
     L.total = off;
@@ -224,6 +240,10 @@ void bind_workspace(mxp_plan_s* p) {
     p->d_items = (int4*)(p->ws + L.items);
     p->d_wbuf = (double*)(p->ws + L.wbuf);
     p->d_stats = (unsigned long long*)(p->ws + L.stats);
+    p->d_prec = (uint8_t*)(p->ws + L.prec);
+    p->d_amax_s = (double*)(p->ws + L.amax_s);
+    p->d_amax_x = (unsigned long long*)(p->ws + L.flags +
+                                        align_up(sizeof(int) * (size_t)(2 + 4 * p->T + p->T * blocks_per_tile(p->nb)), 8));
     p->pool = (double*)(p->ws + L.pool);
 }
 
@@ -310,10 +330,18 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0) {
         build_task_list(p);
         CK(cudaMemcpyAsync(p->d_items, p->items.data(), sizeof(int4) * p->items.size(), cudaMemcpyHostToDevice, s0));
         CK(cudaMemcpyAsync(p->d_expected, p->expected.data(), sizeof(int) * T, cudaMemcpyHostToDevice, s0));
+        CK(cudaMemcpyAsync(p->d_prec, p->map.data(), (size_t)T, cudaMemcpyHostToDevice, s0));
         CK(cudaStreamSynchronize(s0));
         p->list_uploaded = true;
     }
     CK(cudaMemsetAsync(p->d_flags, 0, p->flags_bytes, s0));
+    if (p->mxp) {
+        // O3: stored input A^ = deq(q_p(A)) per tile; amax_x is then reset for the TRSM outputs
+        Prof pr(p, s0, MXP_KCLASS_OTHER, 0.0, 2);
+        launch_input_quantize(p->pool, p->d_slot, p->d_prec, Nt, p->nb, p->d_amax_x, p->d_amax_s, s0);
+        p->launches += 2;
+        CK(cudaMemsetAsync(p->d_amax_x, 0, sizeof(unsigned long long) * T, s0));
+    }
     if (p->debug_sync == 2)  // GEMM-throughput probe: every tile "ready", no POTRF (values are garbage)
         CK(cudaMemsetAsync(p->d_flags + 2, 1, sizeof(int) * T, s0));
     CK(cudaEventRecord(p->ev_start, s0));
@@ -329,7 +357,11 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0) {
     a.ready = p->d_flags + 2;
     a.gemm_done = a.ready + T;
     a.trsm_done = a.gemm_done + T;
-    a.blk_chunk = a.trsm_done + T;
+    a.quant_done = a.trsm_done + T;
+    a.blk_chunk = a.quant_done + T;
+    a.prec = p->mxp ? p->d_prec : nullptr;
+    a.amax_x = p->d_amax_x;
+    a.amax_s = p->d_amax_s;
     a.gemm_expected = p->d_expected;
     a.Nt = Nt;
     a.nb = p->nb;
@@ -417,8 +449,6 @@ int mxp_chol_plan(int64_t n, int64_t nb, const uint8_t* precision_map, int ngpus
                 if (i == j && c != MXP_FP64) return -3;
                 map[tile_index(Nt, i, j)] = c;
             }
-        for (auto c : map)
-            if (c != MXP_FP64) return MXP_ENOTSUP;  // MxP kernels: not in this build yet
     }
     auto* p = new mxp_plan_s();
     p->n = n;
@@ -426,6 +456,7 @@ int mxp_chol_plan(int64_t n, int64_t nb, const uint8_t* precision_map, int ngpus
     p->Nt = Nt;
     p->T = T;
     p->map = std::move(map);
+    for (auto c : p->map) p->mxp |= (c != MXP_FP64);
     cudaGetDevice(&p->device);
     *out = p;
     return MXP_OK;

@@ -16,7 +16,7 @@ __host__ __device__ inline int64_t tile_index(int64_t Nt, int64_t i, int64_t j) 
 // ---- device-resident static schedule (sched_f64.cu) ----------------------
 // Task list entries (int4): {type, m, k, w}; GEMM: w = (block << 16) | chunk,
 // TRSM: w = 64-row block index.
-enum { ITEM_GEMM = 0, ITEM_TRSM = 1 };
+enum { ITEM_GEMM = 0, ITEM_TRSM = 1, ITEM_QUANT = 2 };
 
 struct SchedArgs {
     double* pool;
@@ -35,6 +35,10 @@ struct SchedArgs {
     int* trsm_done;            // [T] completed TRSM row tasks of the tile
     int* blk_chunk;            // [T*NB] chunks applied to each output block
     double* wbuf;              // [Nt][nb/128][128*128] inverses of L_kk's diagonal blocks
+    const uint8_t* prec;       // [T] storage / compute precision of each tile; NULL = all FP64
+    unsigned long long* amax_x;  // [T] max |X| of the tile before quantization (atomicMax on bits)
+    double* amax_s;            // [T] max |stored value| (drives down-casts of the tile as an operand)
+    int* quant_done;           // [T] completed QUANT row tasks
     int reserved_sms;          // SMs (smid < this) left to the POTRF kernels
     unsigned long long* stats; // optional diagnostics (MXP_ATTR_PROFILE): see STAT_*
 };
@@ -45,6 +49,9 @@ enum {
     STAT_POTRF = 16  // + 3k: kernel start, wait done, end
 };
 int sched_ctas_per_sm();
+// input stage of MxP (a3, O3): per-tile amax, then A^ = deq(q_p(A)) in place
+void launch_input_quantize(double* pool, const int32_t* slot, const uint8_t* prec, int64_t Nt, int64_t nb,
+                           unsigned long long* amax_x, double* amax_s, cudaStream_t s);
 void launch_sched(const SchedArgs& a, int grid, cudaStream_t s);
 void launch_potrf_tile(const SchedArgs& a, int64_t k, cudaStream_t s);
 

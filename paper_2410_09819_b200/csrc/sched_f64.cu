@@ -22,6 +22,7 @@
 #include <math.h>
 
 #include "dmma_gemm.cuh"
+#include "quant.cuh"
 
 namespace mxp {
 
@@ -73,6 +74,31 @@ __device__ __forceinline__ void zero_acc(double (&acc)[C::MI][C::NI][2]) {
 #pragma unroll
         for (int ni = 0; ni < C::NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 }
+
+// Stage transform of the non-FP64 GEMM path: cast_c(L) = deq(q_c(L)) of the
+// operands stored finer than the compute precision c (P:42 down-casting).
+struct CastPost {
+    static constexpr bool active = true;
+    const SchedArgs* a;
+    int64_t m, k, n0, kper;
+    int c;
+    __device__ void operator()(int it, double* sA, double* sB) const {
+        const int64_t n = n0 + it / kper;
+        const int64_t ta = tile_index(a->Nt, m, n), tb = tile_index(a->Nt, k, n);
+        const Cast ca = make_cast(a->prec[ta], c, a->amax_s[ta]);
+        const Cast cb = make_cast(a->prec[tb], c, a->amax_s[tb]);
+        if (ca.mode != P_FP64)
+            for (int idx = threadIdx.x; idx < BK * CC::BM; idx += CC::NT) {
+                double* p = sA + (idx / CC::BM) * CC::LDA_S + idx % CC::BM;
+                *p = apply_cast(ca, *p);
+            }
+        if (cb.mode != P_FP64)
+            for (int idx = threadIdx.x; idx < BK * CC::BN; idx += CC::NT) {
+                double* p = sB + (idx / CC::BN) * CC::LDB_S + idx % CC::BN;
+                *p = apply_cast(cb, *p);
+            }
+    }
+};
 
 // ---------------------------------------------------------------- GEMM task
 // C(m,k)[block b] -= sum_{n in chunk c} A(m,n)[rows] A(k,n)[cols]^T
@@ -128,7 +154,16 @@ __device__ bool task_gemm(const SchedArgs& a, int64_t m, int64_t k, int64_t b, i
     };
     double acc[CC::MI][CC::NI][2];
     zero_acc<CC>(acc);
-    gemm_mainloop<CC>(acc, src, nb, nb, nk, smem);
+    const int cprec = a.prec ? a.prec[t] : P_FP64;  // compute precision = the output tile's (G12)
+    if (cprec == P_FP64) {
+        // FP64 compute: every stored operand is exactly representable (up-casts
+        // are the identity), so the raw cp.async pipeline is already exact.
+        gemm_mainloop<CC>(acc, src, nb, nb, nk, smem);
+    } else {
+        // operands stored finer than c are cast in shared memory, stage by stage
+        CastPost post{&a, m, k, n0, kper, cprec};
+        gemm_mainloop<CC>(acc, src, nb, nb, nk, smem, post);
+    }
     double* Ct = tile_ptr(pool, slot, Nt, nb, m, k) + roff + coff * nb;
 #pragma unroll
     for (int mi = 0; mi < CC::MI; ++mi)
@@ -178,6 +213,7 @@ __device__ bool task_trsm(const SchedArgs& a, int64_t m, int64_t k, int64_t r, d
     double* X = tile_ptr(a.pool, a.slot, Nt, nb, m, k) + r * 64;
     const double* L = tile_ptr(a.pool, a.slot, Nt, nb, k, k);
     const double* Wk = a.wbuf + k * S * (128 * 128);
+    double xmax = 0.0;  // max |X| over this task's rows (tile amax for quantization, G11)
     for (int64_t J = 0; J < S; ++J) {
         double acc[CC::MI][CC::NI][2];
         zero_acc<CC>(acc);
@@ -220,19 +256,56 @@ __device__ bool task_trsm(const SchedArgs& a, int64_t m, int64_t k, int64_t r, d
                     int rr, cc;
                     frag_pos<CC>(mi, ni, i, rr, cc);
                     __stcg(XJ + rr + (int64_t)cc * nb, acc[mi][ni][i]);
+                    xmax = fmax(xmax, fabs(acc[mi][ni][i]));
                 }
         __threadfence_block();
         __syncthreads();
     }
+    for (int o = 16; o > 0; o >>= 1) xmax = fmax(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
+    if ((threadIdx.x & 31) == 0) atomic_max_abs(a.amax_x + t, xmax);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
         int old = atom_add_release(a.trsm_done + t, 1);
-        if (old + 1 == (int)(nb / 64)) st_release(a.ready + t, 1);
+        const bool fp64 = !a.prec || a.prec[t] == P_FP64;
+        if (old + 1 == (int)(nb / 64) && fp64) {
+            // FP64 tile: stored values are the TRSM result; amax_s drives later down-casts
+            a.amax_s[t] = amax_of(a.amax_x + t);
+            __threadfence();
+            st_release(a.ready + t, 1);
+        }
         if (a.stats) {
             atomicAdd(a.stats + STAT_TRSM_BUSY, globaltimer() - tw0);
             atomicAdd(a.stats + STAT_TRSM_N, 1ull);
         }
+    }
+    return true;
+}
+
+// --------------------------------------------------------------- QUANT task
+// L_mk = deq(q_p(X)) on rows [64r, 64r+64) once every TRSM row task of the
+// tile has contributed to its amax (quantize once per task, after TRSM; O4).
+__device__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k, int64_t r, int* s_flag) {
+    const int64_t Nt = a.Nt, nb = a.nb;
+    const int64_t t = tile_index(Nt, m, k);
+    if (threadIdx.x == 0) *s_flag = wait_flag(a.trsm_done + t, (int)(nb / 64), a, k);
+    __syncthreads();
+    if (!*s_flag) return false;
+    const int p = a.prec[t];
+    const double amax = amax_of(a.amax_x + t);
+    const double sc = tile_scale(p, amax);
+    double* X = tile_ptr(a.pool, a.slot, Nt, nb, m, k) + r * 64;
+    for (int64_t idx = threadIdx.x; idx < 64 * nb; idx += blockDim.x) {
+        double* q = X + (idx & 63) + (idx >> 6) * nb;
+        __stcg(q, quantize_value(p, __ldcg(q), sc));
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        a.amax_s[t] = quantize_value(p, amax, sc);  // q is monotone: max|q(x)| = q(max|x|)
+        __threadfence();
+        int old = atom_add_release(a.quant_done + t, 1);
+        if (old + 1 == (int)(nb / 64)) st_release(a.ready + t, 1);
     }
     return true;
 }
@@ -271,8 +344,10 @@ __global__ void __launch_bounds__(CC::NT, 3) k_sched(SchedArgs a) {
         const int64_t m = it.y, k = it.z;
         if (it.x == ITEM_GEMM) {
             task_gemm(a, m, k, it.w >> 16, it.w & 0xFFFF, smem, &s_flag);
-        } else {
+        } else if (it.x == ITEM_TRSM) {
             task_trsm(a, m, k, it.w, smem, &s_flag);
+        } else {
+            task_quant(a, m, k, it.w, &s_flag);
         }
         __syncthreads();
     }
@@ -424,6 +499,41 @@ __global__ void __launch_bounds__(256, 1) k_potrf_tile(SchedArgs a, int64_t k) {
         st_release(a.ready + tk, 1);
         if (a.stats) a.stats[STAT_POTRF + 3 * k + 2] = globaltimer();
     }
+}
+
+// ------------------------------------------------------ input quantization
+// (O3, G14): the accumulator of every task starts from A^ = deq(q_p(A)).
+__global__ void k_tile_amax(const double* pool, const int32_t* slot, int64_t Nt, int64_t nb,
+                            unsigned long long* amax_x) {
+    const int64_t j = blockIdx.y, i = j + blockIdx.x;
+    if (i >= Nt) return;
+    const int64_t t = tile_index(Nt, i, j);
+    const double* T = pool + (int64_t)slot[t] * nb * nb;
+    double v = 0.0;
+    for (int64_t e = (int64_t)blockIdx.z * blockDim.x + threadIdx.x; e < nb * nb; e += (int64_t)gridDim.z * blockDim.x)
+        v = fmax(v, fabs(T[e]));
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) atomic_max_abs(amax_x + t, v);
+}
+__global__ void k_tile_quantize(double* pool, const int32_t* slot, const uint8_t* prec, int64_t Nt, int64_t nb,
+                                const unsigned long long* amax_x, double* amax_s) {
+    const int64_t j = blockIdx.y, i = j + blockIdx.x;
+    if (i >= Nt) return;
+    const int64_t t = tile_index(Nt, i, j);
+    const int p = prec[t];
+    const double amax = amax_of(amax_x + t);
+    const double sc = tile_scale(p, amax);
+    if (blockIdx.z == 0 && threadIdx.x == 0) amax_s[t] = quantize_value(p, amax, sc);
+    if (p == P_FP64) return;
+    double* T = pool + (int64_t)slot[t] * nb * nb;
+    for (int64_t e = (int64_t)blockIdx.z * blockDim.x + threadIdx.x; e < nb * nb; e += (int64_t)gridDim.z * blockDim.x)
+        T[e] = quantize_value(p, T[e], sc);
+}
+void launch_input_quantize(double* pool, const int32_t* slot, const uint8_t* prec, int64_t Nt, int64_t nb,
+                           unsigned long long* amax_x, double* amax_s, cudaStream_t s) {
+    dim3 grid((unsigned)Nt, (unsigned)Nt, 8);
+    k_tile_amax<<<grid, 256, 0, s>>>(pool, slot, Nt, nb, amax_x);
+    k_tile_quantize<<<grid, 256, 0, s>>>(pool, slot, prec, Nt, nb, amax_x, amax_s);
 }
 
 constexpr int POTRF_SMEM = (2 * PK * 8 > PC::SMEM_BYTES) ? 2 * PK * 8 : PC::SMEM_BYTES;
