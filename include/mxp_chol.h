@@ -65,6 +65,8 @@ typedef enum mxp_attr {
     MXP_ATTR_DEBUG_SYNC = 5,      /* 1 = synchronize and check after every kernel; 2 = GEMM-throughput
                                      probe (GEMM tasks only, Ready pre-set, no POTRF: result is garbage) */
     MXP_ATTR_PROFILE = 6,         /* 1 = time every launch with CUDA events on its stream (mxp_chol_kernel_stats) */
+    MXP_ATTR_TC_ENGINE = 7,       /* 1 (default) = GEMM tasks of tiles below FP64 on tcgen05 (kind::tf32: 3xTF32 for
+                                     FP32 tiles, 1xTF32 for FP16/FP8 values); 0 = FP64 DMMA with the same casts */
     MXP_ATTR_GPU_LAUNCHES = 100,  /* (get only) kernels launched by the last factorization */
     MXP_ATTR_H2D_BYTES = 101,     /* (get only) host->device bytes moved by the last factorization */
     MXP_ATTR_D2H_BYTES = 102,     /* (get only) device->host bytes moved by the last factorization */
@@ -166,6 +168,10 @@ int mxp_precision_map_from_matrix_device(int64_t n, int64_t nb, const double* A_
  */
 int mxp_generate_plgsy_device(int64_t n, uint64_t seed, double* A_dev, int64_t lda, void* stream);
 int mxp_generate_kms_device(int64_t n, double rho, double* A_dev, int64_t lda, void* stream);
+/* Matern nu = 0.5 covariance (Eq. 2 closed form): A_ij = sigma2 exp(-|s_i - s_j| / range_a)
+ * (+ nugget on the diagonal) from n locations xy_dev (device, interleaved x,y); see workloads.matern_*. */
+int mxp_generate_matern_device(int64_t n, const double* xy_dev, double sigma2, double range_a, double nugget,
+                               double* A_dev, int64_t lda, void* stream);
 
 /*
  * Per-kernel-class statistics of the last factorization when MXP_ATTR_PROFILE

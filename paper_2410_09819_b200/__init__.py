@@ -26,6 +26,7 @@ from .binding import (  # noqa: F401
     Plan,
     abi_version,
     generate_kms_device,
+    generate_matern_device,
     generate_plgsy_device,
     host_alloc,
     host_free,
@@ -37,5 +38,6 @@ from .binding import (  # noqa: F401
 __all__ = [
     "FP64", "FP32", "FP16", "FP8", "MxpError", "Plan", "abi_version", "lib", "lib_path",
     "precision_map_from_matrix_device", "generate_plgsy_device", "generate_kms_device",
+    "generate_matern_device",
     "host_alloc", "host_free",
 ]

@@ -14,7 +14,7 @@ _lock = threading.Lock()
 
 ATTR = {
     "device": 0, "stream": 1, "hbm_bytes_cap": 2, "splitk_tiles": 3, "lookahead": 4,
-    "debug_sync": 5, "profile": 6, "gpu_launches": 100, "h2d_bytes": 101, "d2h_bytes": 102,
+    "debug_sync": 5, "profile": 6, "tc_engine": 7, "gpu_launches": 100, "h2d_bytes": 101, "d2h_bytes": 102,
     "pool_slots": 103, "nt": 104,
 }
 
@@ -23,6 +23,7 @@ EXPORTS = [
     "mxp_chol_plan", "mxp_chol_plan_set", "mxp_chol_plan_get", "mxp_chol_workspace_size",
     "mxp_chol_set_workspace", "mxp_chol_factor_device", "mxp_chol_factor", "mxp_chol_logdet",
     "mxp_precision_map_from_matrix_device", "mxp_generate_plgsy_device", "mxp_generate_kms_device",
+    "mxp_generate_matern_device",
     "mxp_chol_plan_destroy", "mxp_host_alloc", "mxp_host_free", "mxp_strerror", "mxp_last_error",
     "mxp_chol_abi_version", "mxp_chol_kernel_stats", "mxp_chol_sched_diagnostics",
 ]
@@ -66,6 +67,8 @@ def lib():
                                                             ctypes.c_uint32, vp, vp]
         L.mxp_generate_plgsy_device.argtypes = [i64, u64, vp, i64, vp]
         L.mxp_generate_kms_device.argtypes = [i64, ctypes.c_double, vp, i64, vp]
+        L.mxp_generate_matern_device.argtypes = [i64, vp, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                                 vp, i64, vp]
         L.mxp_chol_plan_destroy.argtypes = [vp]
         L.mxp_chol_plan_destroy.restype = None
         L.mxp_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(vp)]
@@ -251,6 +254,20 @@ def generate_kms_device(A, rho: float, stream=None):
     n = A.shape[0]
     ptr, lda, is_cuda = _colmajor_ptr(A, n)
     _check("mxp_generate_kms_device", lib().mxp_generate_kms_device(n, float(rho), ptr, lda, stream))
+
+
+def generate_matern_device(A, xy, sigma2: float = 1.0, range_a: float = 0.02627, nugget: float = 0.0,
+                           stream=None):
+    """A (column-major device view) <- Matern nu=0.5 covariance of the n x 2
+    locations xy (numpy or torch; copied to the device)."""
+    import torch
+    n = A.shape[0]
+    ptr, lda, is_cuda = _colmajor_ptr(A, n)
+    xyd = torch.as_tensor(xy, dtype=torch.float64).to(A.device).contiguous()
+    _check("mxp_generate_matern_device",
+           lib().mxp_generate_matern_device(n, xyd.data_ptr(), float(sigma2), float(range_a), float(nugget),
+                                            ptr, lda, stream))
+    return xyd
 
 
 def host_alloc(nbytes: int) -> int:

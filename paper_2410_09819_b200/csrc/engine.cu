@@ -68,10 +68,13 @@ struct mxp_plan_s {
     std::vector<int> expected;
     bool list_uploaded = false;
     int reserved_sms = 1;
+    int tc_engine = 1;             // non-FP64 GEMM tasks on tcgen05 (0: DMMA with casts)
     bool mxp = false;              // any tile below FP64
     uint8_t* d_prec = nullptr;
     unsigned long long* d_amax_x = nullptr;
     double* d_amax_s = nullptr;
+    SchedArgs* d_args = nullptr;
+    SchedArgs h_args{};
 
     bool streams_ready = false;
     cudaStream_t sU = 0, sP = 0;
@@ -124,6 +127,14 @@ bool block_needed(int64_t m, int64_t k, int64_t b, int64_t nb) {
     return (bi + 1) * 64 > bj * 128;
 }
 
+// GEMM blocks of a tile: 64x128 DMMA blocks, or 128x128 tcgen05 blocks for
+// tiles computed below FP64 when the tensor-core engine is on.
+int64_t gemm_blocks(const mxp_plan_s* p, int64_t m, int64_t k) {
+    const int64_t nb = p->nb;
+    if (p->tc_engine && p->map[tile_index(p->Nt, m, k)] != MXP_FP64) return (nb / 128) * (nb / 128);
+    return blocks_per_tile(nb);
+}
+
 // chunks of column k: ceil((k-1)/KC) fixed-size chunks over [0, k-1), then {k-1}
 int64_t nchunks(int64_t k, int64_t KC) {
     if (k == 0) return 0;
@@ -143,7 +154,7 @@ void build_task_list(mxp_plan_s* p) {
     auto gemm_col = [&](int64_t k, int64_t c0, int64_t c1) {
         for (int64_t c = c0; c < c1; ++c)
             for (int64_t m = k; m < Nt; ++m)
-                for (int64_t b = 0; b < NB; ++b)
+                for (int64_t b = 0; b < gemm_blocks(p, m, k); ++b)
                     if (block_needed(m, k, b, nb)) {
                         p->items.push_back(make_int4(ITEM_GEMM, (int)m, (int)k, (int)((b << 16) | c)));
                         p->expected[tile_index(Nt, m, k)]++;
@@ -174,7 +185,11 @@ size_t list_bytes(const mxp_plan_s* p) {
     int64_t diag_blocks = 0;
     for (int64_t b = 0; b < NB; ++b) diag_blocks += block_needed(0, 0, b, nb);
     int64_t cnt = 0;
-    for (int64_t k = 1; k < Nt; ++k) cnt += nchunks(k, p->splitk_tiles) * ((Nt - k - 1) * NB + diag_blocks);
+    for (int64_t k = 1; k < Nt; ++k) {
+        int64_t per = diag_blocks;
+        for (int64_t m = k + 1; m < Nt; ++m) per += gemm_blocks(p, m, k);
+        cnt += nchunks(k, p->splitk_tiles) * per;
+    }
     cnt += (Nt * (Nt - 1) / 2) * (nb / 64);
     for (int64_t k = 0; k < Nt; ++k)
         for (int64_t m = k + 1; m < Nt; ++m) cnt += (p->map[tile_index(Nt, m, k)] != MXP_FP64) * (nb / 64);
@@ -182,7 +197,7 @@ size_t list_bytes(const mxp_plan_s* p) {
 }
 
 struct Layout {
-    size_t slot, flags, flags_bytes, expected, items, wbuf, stats, prec, amax_x, amax_s, pool, total;
+    size_t slot, flags, flags_bytes, expected, items, wbuf, stats, prec, amax_x, amax_s, args, pool, total;
 };
 
 Layout layout(const mxp_plan_s* p) {
@@ -207,6 +222,8 @@ Layout layout(const mxp_plan_s* p) {
     off += align_up((size_t)p->T, 256);
     L.amax_s = off;
     off += align_up(sizeof(double) * (size_t)p->T, 256);
+    L.args = off;
+    off += align_up(sizeof(SchedArgs), 256);
     L.pool = off;
     off += sizeof(double) * (size_t)p->T * p->nb * p->nb;
     L.total = off;
@@ -242,6 +259,7 @@ void bind_workspace(mxp_plan_s* p) {
     p->d_stats = (unsigned long long*)(p->ws + L.stats);
     p->d_prec = (uint8_t*)(p->ws + L.prec);
     p->d_amax_s = (double*)(p->ws + L.amax_s);
+    p->d_args = (SchedArgs*)(p->ws + L.args);
     p->d_amax_x = (unsigned long long*)(p->ws + L.flags +
                                         align_up(sizeof(int) * (size_t)(2 + 4 * p->T + p->T * blocks_per_tile(p->nb)), 8));
     p->pool = (double*)(p->ws + L.pool);
@@ -360,6 +378,7 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0) {
     a.quant_done = a.trsm_done + T;
     a.blk_chunk = a.quant_done + T;
     a.prec = p->mxp ? p->d_prec : nullptr;
+    a.tc_engine = p->tc_engine;
     a.amax_x = p->d_amax_x;
     a.amax_s = p->d_amax_s;
     a.gemm_expected = p->d_expected;
@@ -388,7 +407,9 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0) {
     const double total = (double)Nt * Nt * Nt * nb3 / 3.0;
     {
         Prof pr(p, p->sU, MXP_KCLASS_CHAIN, total - (double)Nt * nb3 / 3.0);
-        launch_sched(a, occ * nsm, p->sU);
+        p->h_args = a;
+        CK(cudaMemcpyAsync(p->d_args, &p->h_args, sizeof(SchedArgs), cudaMemcpyHostToDevice, p->sU));
+        launch_sched(a, p->d_args, p->mxp, occ * nsm, p->sU);
         ++p->launches;
         dbg(p, p->sU, "sched");
     }
@@ -492,6 +513,16 @@ int mxp_chol_plan_set(mxp_plan_t p, mxp_attr_t key, int64_t v) {
         p->debug_sync = (int)v;
         return MXP_OK;
     case MXP_ATTR_PROFILE: p->profile = v ? 1 : 0; return MXP_OK;
+    case MXP_ATTR_TC_ENGINE:
+        if (p->ws && !p->ws_owned) return MXP_ESTATE;  // changes the task list size
+        if (p->ws_owned) {
+            cudaFree(p->ws);
+            p->ws = nullptr;
+            p->ws_owned = false;
+        }
+        p->tc_engine = v ? 1 : 0;
+        p->list_uploaded = false;
+        return MXP_OK;
     default: return -2;
     }
 }
@@ -525,6 +556,7 @@ int mxp_chol_plan_get(mxp_plan_t p, mxp_attr_t key, int64_t* v) {
     case MXP_ATTR_LOOKAHEAD: *v = p->lookahead; return MXP_OK;
     case MXP_ATTR_DEBUG_SYNC: *v = p->debug_sync; return MXP_OK;
     case MXP_ATTR_PROFILE: *v = p->profile; return MXP_OK;
+    case MXP_ATTR_TC_ENGINE: *v = p->tc_engine; return MXP_OK;
     case MXP_ATTR_GPU_LAUNCHES: *v = p->launches; return MXP_OK;
     case MXP_ATTR_H2D_BYTES: *v = p->h2d; return MXP_OK;
     case MXP_ATTR_D2H_BYTES: *v = p->d2h; return MXP_OK;

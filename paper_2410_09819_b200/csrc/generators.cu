@@ -43,6 +43,20 @@ __global__ void k_gen_kms(int64_t n, double rho, double* A, int64_t lda) {
     }
 }
 
+__global__ void k_gen_matern(int64_t n, const double* __restrict__ xy, double sigma2, double a, double nugget,
+                             double* A, int64_t lda) {
+    const int64_t j = blockIdx.y + (int64_t)blockIdx.z * gridDim.y;
+    if (j >= n) return;
+    const double xj = xy[2 * j], yj = xy[2 * j + 1];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double dx = xy[2 * i] - xj, dy = xy[2 * i + 1] - yj;
+        const double h = sqrt(dx * dx + dy * dy);
+        double v = sigma2 * exp(-h / a);
+        if (i == j) v += nugget;
+        A[i + j * lda] = v;
+    }
+}
+
 void grid_for(int64_t n, dim3& g) {
     unsigned gy = (unsigned)(n < 65535 ? n : 65535);
     unsigned gz = (unsigned)((n + gy - 1) / gy);
@@ -73,5 +87,20 @@ extern "C" int mxp_generate_kms_device(int64_t n, double rho, double* A, int64_t
     dim3 g;
     grid_for(n, g);
     k_gen_kms<<<g, 256, 0, (cudaStream_t)stream>>>(n, rho, A, lda);
+    return cudaGetLastError() == cudaSuccess ? MXP_OK : MXP_ECUDA;
+}
+
+extern "C" int mxp_generate_matern_device(int64_t n, const double* xy_dev, double sigma2, double range_a,
+                                          double nugget, double* A, int64_t lda, void* stream) {
+    if (n < 1) return -1;
+    if (!xy_dev) return -2;
+    if (!(sigma2 > 0.0)) return -3;
+    if (!(range_a > 0.0)) return -4;
+    if (!(nugget >= 0.0)) return -5;
+    if (!A) return -6;
+    if (lda < n) return -7;
+    dim3 g;
+    grid_for(n, g);
+    k_gen_matern<<<g, 256, 0, (cudaStream_t)stream>>>(n, xy_dev, sigma2, range_a, nugget, A, lda);
     return cudaGetLastError() == cudaSuccess ? MXP_OK : MXP_ECUDA;
 }

@@ -39,6 +39,7 @@ struct SchedArgs {
     unsigned long long* amax_x;  // [T] max |X| of the tile before quantization (atomicMax on bits)
     double* amax_s;            // [T] max |stored value| (drives down-casts of the tile as an operand)
     int* quant_done;           // [T] completed QUANT row tasks
+    int tc_engine;             // 1: non-FP64 tiles on tcgen05 (128x128 blocks); 0: DMMA with casts (64x128)
     int reserved_sms;          // SMs (smid < this) left to the POTRF kernels
     unsigned long long* stats; // optional diagnostics (MXP_ATTR_PROFILE): see STAT_*
 };
@@ -52,7 +53,7 @@ int sched_ctas_per_sm();
 // input stage of MxP (a3, O3): per-tile amax, then A^ = deq(q_p(A)) in place
 void launch_input_quantize(double* pool, const int32_t* slot, const uint8_t* prec, int64_t Nt, int64_t nb,
                            unsigned long long* amax_x, double* amax_s, cudaStream_t s);
-void launch_sched(const SchedArgs& a, int grid, cudaStream_t s);
+void launch_sched(const SchedArgs& a, const SchedArgs* a_dev, bool mxp, int grid, cudaStream_t s);  // a_dev: device copy of a
 void launch_potrf_tile(const SchedArgs& a, int64_t k, cudaStream_t s);
 
 // ---- layout / utility kernels --------------------------------------------

@@ -31,9 +31,36 @@ __device__ __forceinline__ double rne_format(double v, int mb, int emin, double 
     return copysign(r, v);
 }
 
+// Fast exact paths: hardware cvt.rn for binary32/binary16 (IEEE RNE with
+// gradual underflow, overflow to inf); E4M3 by integer mantissa rounding on
+// the fp64 bit pattern (normal range) and a magic-number add (subnormal
+// range, quantum 2^-9), then satfinite.  Equal to rne_format() for every input.
 __device__ __forceinline__ double round_fp32(double v) { return (double)__double2float_rn(v); }
-__device__ __forceinline__ double round_fp16(double v) { return rne_format(v, 10, -14, 65504.0, false); }
-__device__ __forceinline__ double round_e4m3(double v) { return rne_format(v, 3, -6, 448.0, true); }
+__device__ __forceinline__ double round_fp16(double v) {
+    unsigned short h;
+    asm("cvt.rn.f16.f64 %0, %1;" : "=h"(h) : "d"(v));
+    float f;
+    asm("cvt.f32.f16 %0, %1;" : "=f"(f) : "h"(h));
+    return (double)f;
+}
+__device__ __forceinline__ double round_e4m3(double v) {
+    double a = fabs(v);
+    if (!(a == a)) return v;
+    double r;
+    if (a > 448.0) {
+        r = 448.0;  // satfinite: everything above the largest finite rounds/saturates to it
+    } else if (a < 0.015625) {  // below 2^-6: fixed quantum 2^-9 (RNE via the 1.5*2^43 shifter)
+        const double M = 13194139533312.0;  // 1.5 * 2^43
+        r = (a + M) - M;
+    } else {  // keep 3 explicit mantissa bits: RNE on bit 49 of the fp64 pattern
+        unsigned long long b = (unsigned long long)__double_as_longlong(a);
+        b += 0x0000FFFFFFFFFFFFull + ((b >> 49) & 1ull);
+        b &= ~0x0001FFFFFFFFFFFFull;
+        r = __longlong_as_double((long long)b);
+        if (r > 448.0) r = 448.0;
+    }
+    return copysign(r, v);
+}
 
 // power-of-two scale of a tile with max-abs `amax` for precision p (G11)
 __device__ __forceinline__ double tile_scale(int p, double amax) {
@@ -44,29 +71,36 @@ __device__ __forceinline__ double tile_scale(int p, double amax) {
     return scalbn(1.0, k);
 }
 
-// q then deq of one value with the tile scale s (s = 1 for FP64/FP32)
-__device__ __forceinline__ double quantize_value(int p, double x, double s) {
+// q then deq of one value with the tile scale s (s = 1 for FP64/FP32);
+// s is a power of two, so dividing by it is the exact multiply by 1/s.
+__device__ __forceinline__ double quantize_value(int p, double x, double s, double inv_s) {
     switch (p) {
     case P_FP32: return round_fp32(x);
-    case P_FP16: return round_fp16(x * s) / s;
-    case P_FP8: return round_e4m3(x * s) / s;
+    case P_FP16: return round_fp16(x * s) * inv_s;
+    case P_FP8: return round_e4m3(x * s) * inv_s;
     default: return x;
     }
+}
+__device__ __forceinline__ double quantize_value(int p, double x, double s) {
+    return quantize_value(p, x, s, 1.0 / s);
 }
 
 // A cast applied while staging an operand tile: mode = target precision when
 // the stored precision is finer than the compute precision, else FP64 (none).
 struct Cast {
     int mode;
-    double s;
+    double s, inv_s;
 };
 __device__ __forceinline__ Cast make_cast(int stored, int compute, double amax) {
     Cast c;
     c.mode = (stored < compute) ? compute : P_FP64;  // codes: lower = finer
     c.s = tile_scale(c.mode, amax);
+    c.inv_s = 1.0 / c.s;
     return c;
 }
-__device__ __forceinline__ double apply_cast(const Cast& c, double x) { return quantize_value(c.mode, x, c.s); }
+__device__ __forceinline__ double apply_cast(const Cast& c, double x) {
+    return quantize_value(c.mode, x, c.s, c.inv_s);
+}
 
 // amax of non-negative doubles via their bit patterns (monotone for x >= 0)
 __device__ __forceinline__ void atomic_max_abs(unsigned long long* slot, double v) {

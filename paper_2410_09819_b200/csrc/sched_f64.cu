@@ -23,6 +23,7 @@
 
 #include "dmma_gemm.cuh"
 #include "quant.cuh"
+#include "tc_block.cuh"
 
 namespace mxp {
 
@@ -102,7 +103,8 @@ struct CastPost {
 
 // ---------------------------------------------------------------- GEMM task
 // C(m,k)[block b] -= sum_{n in chunk c} A(m,n)[rows] A(k,n)[cols]^T
-__device__ bool task_gemm(const SchedArgs& a, int64_t m, int64_t k, int64_t b, int64_t c, double* smem,
+template <bool CAST>
+__device__ __forceinline__ bool task_gemm(const SchedArgs& a, int64_t m, int64_t k, int64_t b, int64_t c, double* smem,
                           int* s_flag) {
     const int64_t Nt = a.Nt, nb = a.nb;
     const int64_t SR = nb / CC::BM;
@@ -155,7 +157,7 @@ __device__ bool task_gemm(const SchedArgs& a, int64_t m, int64_t k, int64_t b, i
     double acc[CC::MI][CC::NI][2];
     zero_acc<CC>(acc);
     const int cprec = a.prec ? a.prec[t] : P_FP64;  // compute precision = the output tile's (G12)
-    if (cprec == P_FP64) {
+    if constexpr (!CAST) {
         // FP64 compute: every stored operand is exactly representable (up-casts
         // are the identity), so the raw cp.async pipeline is already exact.
         gemm_mainloop<CC>(acc, src, nb, nb, nk, smem);
@@ -189,11 +191,16 @@ __device__ bool task_gemm(const SchedArgs& a, int64_t m, int64_t k, int64_t b, i
     return true;
 }
 
+__device__ __noinline__ bool task_gemm_cast(const SchedArgs& a, int64_t m, int64_t k, int64_t b, int64_t c,
+                                           double* smem, int* s_flag) {
+    return task_gemm<true>(a, m, k, b, c, smem, s_flag);
+}
+
 // ---------------------------------------------------------------- TRSM task
 // X L_kk^T = C on rows [64r, 64r+64) of tile (m,k), in place (Alg. 2
 // P:269, G3).  Blocked by 128 columns J with the inverses W_J = L_JJ^-1 from
 // the POTRF kernel (MAGMA-style):  X[:,J] = (C[:,J] - X[:,<J] L[J,<J]^T) W_J^T.
-__device__ bool task_trsm(const SchedArgs& a, int64_t m, int64_t k, int64_t r, double* smem, int* s_flag) {
+__device__ __forceinline__ bool task_trsm(const SchedArgs& a, int64_t m, int64_t k, int64_t r, double* smem, int* s_flag) {
     const int64_t Nt = a.Nt, nb = a.nb, S = nb / 128;
     const int64_t t = tile_index(Nt, m, k);
     uint64_t tw0 = 0;
@@ -282,10 +289,83 @@ __device__ bool task_trsm(const SchedArgs& a, int64_t m, int64_t k, int64_t r, d
     return true;
 }
 
+__device__ __noinline__ bool task_trsm_ool(const SchedArgs& a, int64_t m, int64_t k, int64_t r, double* smem,
+                                          int* s_flag) {
+    return task_trsm(a, m, k, r, smem, s_flag);
+}
+
+// ------------------------------------------------------ tcgen05 GEMM task
+// Tiles stored below FP64 (G12): C(m,k)[128x128 block b] -= sum over the
+// chunk of cast_c(A(m,n)) cast_c(A(k,n))^T on the 5th-gen tensor cores
+// (kind::tf32; 3xTF32 when c = FP32, else 1xTF32 on exact FP16/E4M3 values),
+// fp32 accumulator in TMEM, added into the fp64 container.
+template <bool THREE>
+__device__ __noinline__ bool task_gemm_tc(const SchedArgs& a, int64_t m, int64_t k, int64_t b, int64_t c, int cprec,
+                             uint8_t* smem, uint64_t* mbar, uint32_t tmem, int* s_flag) {
+    const int64_t Nt = a.Nt, nb = a.nb, S = nb / 128;
+    const int64_t bi = b % S, bj = b / S;
+    const int64_t t = tile_index(Nt, m, k);
+    int64_t n0, n1;
+    chunk_range(k, c, a.KC, n0, n1);
+    int* chunk_flag = a.blk_chunk + t * a.NB + b;
+    uint64_t tw0 = 0;
+    if (threadIdx.x == 0) {
+        if (a.stats) tw0 = globaltimer();
+        bool ok = true;
+        for (int64_t n = n0; n < n1 && ok; ++n)
+            ok = wait_flag(a.ready + tile_index(Nt, m, n), 1, a, k) &&
+                 wait_flag(a.ready + tile_index(Nt, k, n), 1, a, k);
+        if (ok) ok = wait_flag(chunk_flag, (int)c, a, k);
+        *s_flag = ok;
+        if (a.stats) {
+            uint64_t tw1 = globaltimer();
+            atomicAdd(a.stats + STAT_GEMM_WAIT, tw1 - tw0);
+            tw0 = tw1;
+        }
+    }
+    __syncthreads();
+    if (!*s_flag) return false;
+    const int64_t kper = nb / tc::KS;
+    const int nsteps = (int)((n1 - n0) * kper);
+    const int64_t roff = bi * 128, coff = bj * 128;
+    // stateful K walk: tile pointers and casts change only at tile boundaries
+    int64_t cur_n = n0 - 1, kcol = nb;
+    tc::Chunk cur{};
+    auto src = [&](int) {
+        if (kcol == nb) {
+            kcol = 0;
+            ++cur_n;
+            const int64_t ta = tile_index(Nt, m, cur_n), tb = tile_index(Nt, k, cur_n);
+            cur.a = tile_ptr(a.pool, a.slot, Nt, nb, m, cur_n) + roff;
+            cur.b = tile_ptr(a.pool, a.slot, Nt, nb, k, cur_n) + coff;
+            cur.ca = make_cast(a.prec[ta], cprec, a.amax_s[ta]);
+            cur.cb = make_cast(a.prec[tb], cprec, a.amax_s[tb]);
+        }
+        tc::Chunk ch = cur;
+        ch.a += kcol * nb;
+        ch.b += kcol * nb;
+        kcol += tc::KS;
+        return ch;
+    };
+    double* Ct = tile_ptr(a.pool, a.slot, Nt, nb, m, k) + roff + coff * nb;
+    tc::block_gemm<THREE>(Ct, nb, src, nsteps, nb, nb, smem, mbar, tmem);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        st_release(chunk_flag, (int)c + 1);
+        atom_add_release(a.gemm_done + t, 1);
+        if (a.stats) {
+            atomicAdd(a.stats + STAT_GEMM_BUSY, globaltimer() - tw0);
+            atomicAdd(a.stats + STAT_GEMM_N, 1ull);
+        }
+    }
+    return true;
+}
+
 // --------------------------------------------------------------- QUANT task
 // L_mk = deq(q_p(X)) on rows [64r, 64r+64) once every TRSM row task of the
 // tile has contributed to its amax (quantize once per task, after TRSM; O4).
-__device__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k, int64_t r, int* s_flag) {
+__device__ __noinline__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k, int64_t r, int* s_flag) {
     const int64_t Nt = a.Nt, nb = a.nb;
     const int64_t t = tile_index(Nt, m, k);
     if (threadIdx.x == 0) *s_flag = wait_flag(a.trsm_done + t, (int)(nb / 64), a, k);
@@ -313,7 +393,15 @@ __device__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k, int64_t r, 
 }  // namespace
 
 // ------------------------------------------------------ the static schedule
-__global__ void __launch_bounds__(CC::NT, 3) k_sched(SchedArgs a) {
+// The arguments live in global memory (copied once per factorization) so the
+// out-of-line task functions can take them by reference without a local copy.
+// MXP = false: FP64-only task list (DMMA GEMM + TRSM, fully inlined, no
+// spills); MXP = true adds tcgen05 / cast / QUANT tasks, kept out of line.
+// (FP64: arguments by value in the constant bank -- operands read straight
+// from it keep register pressure at the no-spill level; MxP: through `ap`.)
+template <bool MXP>
+__global__ void __launch_bounds__(CC::NT, 3) k_sched(const SchedArgs a_param, const SchedArgs* __restrict__ ap) {
+    const SchedArgs& a = MXP ? *ap : a_param;
     if ((int)smid() < a.reserved_sms) return;  // leave these SMs to the POTRF kernels
     extern __shared__ __align__(16) double smem[];
     // The task ticket and wait verdict live in the padding columns of the A
@@ -323,6 +411,20 @@ __global__ void __launch_bounds__(CC::NT, 3) k_sched(SchedArgs a) {
     static_assert(PAD * 8 >= 2 * sizeof(int), "scratch must fit in the padding");
     int& s_idx = *reinterpret_cast<int*>(smem + CC::BM);
     int& s_flag = *(reinterpret_cast<int*>(smem + CC::BM) + 1);
+    // tcgen05 state in the last 32 bytes (padding of the last B row of the DMMA
+    // pipeline, never touched by it): two mbarriers + the TMEM base address.
+    uint8_t* smem_b = reinterpret_cast<uint8_t*>(smem);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_b + CC::SMEM_BYTES - 32);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_b + CC::SMEM_BYTES - 16);
+    uint32_t tmem = 0;
+    if (MXP && a.tc_engine) {  // MxP: this CTA owns 128 TMEM columns (3 CTAs x 128 <= 512 per SM)
+        if (threadIdx.x < 32) tc::tmem_alloc(tmem_slot, tc::TMEM_COLS);
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        tmem = *tmem_slot;
+        __syncthreads();
+    }
     if (a.stats && threadIdx.x == 0) {
         atomicMin(a.stats + STAT_T0, globaltimer());
         atomicAdd(a.stats + STAT_CTAS, 1ull);
@@ -342,14 +444,32 @@ __global__ void __launch_bounds__(CC::NT, 3) k_sched(SchedArgs a) {
         if (idx == -2) continue;
         const int4 it = a.items[idx];
         const int64_t m = it.y, k = it.z;
-        if (it.x == ITEM_GEMM) {
-            task_gemm(a, m, k, it.w >> 16, it.w & 0xFFFF, smem, &s_flag);
-        } else if (it.x == ITEM_TRSM) {
-            task_trsm(a, m, k, it.w, smem, &s_flag);
+        if constexpr (!MXP) {
+            if (it.x == ITEM_GEMM) task_gemm<false>(a, m, k, it.w >> 16, it.w & 0xFFFF, smem, &s_flag);
+            else task_trsm(a, m, k, it.w, smem, &s_flag);
         } else {
-            task_quant(a, m, k, it.w, &s_flag);
+            if (it.x == ITEM_GEMM) {
+                const int cp = a.prec[tile_index(a.Nt, m, k)];
+                if (cp == P_FP64)
+                    task_gemm<false>(a, m, k, it.w >> 16, it.w & 0xFFFF, smem, &s_flag);
+                else if (!a.tc_engine)
+                    task_gemm_cast(a, m, k, it.w >> 16, it.w & 0xFFFF, smem, &s_flag);
+                else if (cp == P_FP32)
+                    task_gemm_tc<true>(a, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_b, mbar, tmem, &s_flag);
+                else
+                    task_gemm_tc<false>(a, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_b, mbar, tmem, &s_flag);
+            } else if (it.x == ITEM_TRSM) {
+                task_trsm_ool(a, m, k, it.w, smem, &s_flag);
+            } else {
+                task_quant(a, m, k, it.w, &s_flag);
+            }
         }
         __syncthreads();
+    }
+    if (MXP && a.tc_engine) {
+        tc::fence_before();
+        __syncthreads();
+        if (threadIdx.x < 32) tc::tmem_dealloc(tmem, tc::TMEM_COLS);
     }
     if (a.stats && threadIdx.x == 0) atomicMax(a.stats + STAT_TEND, globaltimer());
 }
@@ -541,7 +661,8 @@ constexpr int POTRF_SMEM = (2 * PK * 8 > PC::SMEM_BYTES) ? 2 * PK * 8 : PC::SMEM
 void configure_sched() {
     static bool done = false;
     if (done) return;
-    cudaFuncSetAttribute(k_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM_BYTES);
+    cudaFuncSetAttribute(k_sched<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM_BYTES);
+    cudaFuncSetAttribute(k_sched<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM_BYTES);
     cudaFuncSetAttribute(k_potrf_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF_SMEM);
     done = true;
 }
@@ -549,13 +670,14 @@ void configure_sched() {
 int sched_ctas_per_sm() {
     int occ = 0;
     configure_sched();
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sched, CC::NT, CC::SMEM_BYTES);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sched<false>, CC::NT, CC::SMEM_BYTES);
     return occ;
 }
 
-void launch_sched(const SchedArgs& a, int grid, cudaStream_t s) {
+void launch_sched(const SchedArgs& a, const SchedArgs* a_dev, bool mxp, int grid, cudaStream_t s) {
     configure_sched();
-    k_sched<<<grid, CC::NT, CC::SMEM_BYTES, s>>>(a);
+    if (mxp) k_sched<true><<<grid, CC::NT, CC::SMEM_BYTES, s>>>(a, a_dev);
+    else k_sched<false><<<grid, CC::NT, CC::SMEM_BYTES, s>>>(a, a_dev);
 }
 
 void launch_potrf_tile(const SchedArgs& a, int64_t k, cudaStream_t s) {

@@ -21,19 +21,24 @@ def _matern(n, a=0.02627):
     return w.matern_cov(xy, 1.0, a)
 
 
+@pytest.mark.parametrize("tc", [1, 0])
 @pytest.mark.parametrize("eps", [1e-5, 1e-8])
 @pytest.mark.parametrize("n,nb", [(2048, 128), (4096, 256), (1900, 256)])
-def test_mxp_matern_against_oracle(n, nb, eps):
+def test_mxp_matern_against_oracle(n, nb, eps, tc):
+    """tc=1: tiles below FP64 on tcgen05 (3xTF32 / 1xTF32, fp32 accumulation);
+    tc=0: the same casts on FP64 DMMA (fp64 accumulation, like the oracle)."""
     S = _matern(n)
     pmap = oracle.plan(S, nb, eps)
     assert np.any(pmap != oracle.FP64)
-    L, info, ld, _ = gpu_factor(S, nb, pmap)
+    L, info, ld, _ = gpu_factor(S, nb, pmap, attrs={"tc_engine": tc})
     Lo, oinfo = oracle.factor(S, nb, pmap)
     assert info == oinfo == 0
     err = np.max(np.abs(L - Lo))
     assert err <= 5e-3 * np.max(np.abs(Lo)), err
-    # much tighter in practice: both accumulate in fp64 here
-    assert err <= 1e-6 * np.max(np.abs(Lo)), err
+    if tc == 0:  # same casts, fp64 accumulation: far inside the tolerance
+        assert err <= 1e-6 * np.max(np.abs(Lo)), err
+    else:        # fp32 accumulation of the non-FP64 tiles (G12)
+        assert err <= 1e-4 * np.max(np.abs(Lo)), err
     assert abs(ld - oracle.logdet(Lo)) <= 1e-6 * abs(oracle.logdet(Lo))
 
 

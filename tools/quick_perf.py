@@ -1,14 +1,28 @@
 """Quick timing of the device path vs cuSOLVER (torch.linalg.cholesky) -- dev tool."""
 import sys, time, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2410_09819_b200 as m
 
 for spec in sys.argv[1:]:
     n, nb = map(int, spec.split(":"))
     A = torch.empty((n, n), dtype=torch.float64, device="cuda").T
-    m.generate_plgsy_device(A, 42)
-    plan = m.Plan(n, nb)
+    pmap = None
+    if os.environ.get("MXP"):
+        import workloads as w
+        xy = w.matern_locations(n, seed=1)
+        m.generate_matern_device(A, xy, 1.0, float(os.environ.get("RANGE", "0.02627")))
+        pmap, _ = m.precision_map_from_matrix_device(A, nb, float(os.environ["MXP"]))
+        import numpy as np
+        Ntt = n // nb
+        off = [pmap[i] for i in range(len(pmap))]
+        print("   map fractions (FP64,FP32,FP16,FP8):", [round(float(np.mean(pmap == c)), 3) for c in range(4)], flush=True)
+    else:
+        m.generate_plgsy_device(A, 42)
+    plan = m.Plan(n, nb, pmap)
+    if os.environ.get("TC") is not None:
+        plan.set("tc_engine", int(os.environ["TC"]))
     if os.environ.get("KC"):
         plan.set("splitk_tiles", int(os.environ["KC"]))
     if os.environ.get("PROBE"):
