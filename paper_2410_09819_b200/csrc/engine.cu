@@ -5,6 +5,7 @@
 // uploads it; the device executes it with persistent CTAs that busy-wait on a
 // device-resident Ready table (sched_f64.cu).  The diagonal POTRFs run as one
 // small kernel per column on a high-priority stream on reserved SMs.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -12,6 +13,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/mxp_chol.h"
@@ -36,6 +38,25 @@ struct CudaError {
     } while (0)
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Stream memory operations (executed by the GPU front-end, no SM needed):
+// the copy streams publish "tile landed" and wait for "tile final" flags.
+typedef CUresult (*PFN_streamValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_streamValue32 g_write32 = nullptr, g_wait32 = nullptr;
+bool stream_memops() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", (void**)&g_write32, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            g_write32 = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", (void**)&g_wait32, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            g_wait32 = nullptr;
+        cudaGetLastError();
+    });
+    return g_write32 && g_wait32;
+}
 }  // namespace
 
 struct mxp_plan_s {
@@ -75,6 +96,10 @@ struct mxp_plan_s {
     double* d_amax_s = nullptr;
     SchedArgs* d_args = nullptr;
     SchedArgs h_args{};
+    bool host_mode = false;        // task list built for the host-streaming path (PREP tasks)
+    cudaStream_t sH2D = 0, sD2H = 0, sAux = 0;
+    double* h_stage = nullptr;     // pinned staging for the diagonal tiles (upper triangle untouched)
+    size_t h_stage_bytes = 0;
 
     bool streams_ready = false;
     cudaStream_t sU = 0, sP = 0;
@@ -112,6 +137,10 @@ mxp_plan_s::~mxp_plan_s() {
     if (ev_done) cudaEventDestroy(ev_done);
     if (sU) cudaStreamDestroy(sU);
     if (sP) cudaStreamDestroy(sP);
+    if (sH2D) cudaStreamDestroy(sH2D);
+    if (sD2H) cudaStreamDestroy(sD2H);
+    if (sAux) cudaStreamDestroy(sAux);
+    if (h_stage) cudaFreeHost(h_stage);
     cudaSetDevice(cur);
 }
 
@@ -160,7 +189,12 @@ void build_task_list(mxp_plan_s* p) {
                         p->expected[tile_index(Nt, m, k)]++;
                     }
     };
+    auto prep_col = [&](int64_t k) {
+        for (int64_t m = k; m < Nt; ++m) p->items.push_back(make_int4(ITEM_PREP, (int)m, (int)k, 0));
+    };
+    if (p->host_mode) prep_col(0);
     for (int64_t k = 0; k < Nt; ++k) {
+        if (p->host_mode && k + 1 < Nt) prep_col(k + 1);  // before any GEMM on column k+1
         if (k >= 1) {
             int64_t last = nchunks(k, KC) - 1;
             gemm_col(k, last, last + 1);
@@ -193,6 +227,7 @@ size_t list_bytes(const mxp_plan_s* p) {
     cnt += (Nt * (Nt - 1) / 2) * (nb / 64);
     for (int64_t k = 0; k < Nt; ++k)
         for (int64_t m = k + 1; m < Nt; ++m) cnt += (p->map[tile_index(Nt, m, k)] != MXP_FP64) * (nb / 64);
+    cnt += p->T;  // PREP tasks (host-streaming mode)
     return sizeof(int4) * (size_t)cnt;
 }
 
@@ -206,8 +241,8 @@ Layout layout(const mxp_plan_s* p) {
     L.slot = off;
     off += align_up(sizeof(int32_t) * p->T, 256);
     L.flags = off;
-    // counter, err, ready, gemm_done, trsm_done, quant_done, blk_chunk; then amax_x (u64, zeroed too)
-    L.flags_bytes = align_up(sizeof(int) * (size_t)(2 + 4 * p->T + p->T * blocks_per_tile(p->nb)), 8) +
+    // counter, err, ready, gemm_done, trsm_done, quant_done, loaded, prep_done, blk_chunk; then amax_x
+    L.flags_bytes = align_up(sizeof(int) * (size_t)(2 + 6 * p->T + p->T * blocks_per_tile(p->nb)), 8) +
                     sizeof(unsigned long long) * (size_t)p->T;
     off += align_up(L.flags_bytes, 256);
     L.expected = off;
@@ -261,7 +296,7 @@ void bind_workspace(mxp_plan_s* p) {
     p->d_amax_s = (double*)(p->ws + L.amax_s);
     p->d_args = (SchedArgs*)(p->ws + L.args);
     p->d_amax_x = (unsigned long long*)(p->ws + L.flags +
-                                        align_up(sizeof(int) * (size_t)(2 + 4 * p->T + p->T * blocks_per_tile(p->nb)), 8));
+                                        align_up(sizeof(int) * (size_t)(2 + 6 * p->T + p->T * blocks_per_tile(p->nb)), 8));
     p->pool = (double*)(p->ws + L.pool);
 }
 
@@ -271,6 +306,9 @@ void ensure_streams(mxp_plan_s* p) {
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(cudaStreamCreateWithPriority(&p->sU, cudaStreamNonBlocking, lo));
     CK(cudaStreamCreateWithPriority(&p->sP, cudaStreamNonBlocking, hi));
+    CK(cudaStreamCreateWithFlags(&p->sH2D, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&p->sD2H, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&p->sAux, cudaStreamNonBlocking));
     p->ev_panel.resize(p->Nt);
     p->ev_bulk.resize(p->Nt);
     for (int64_t k = 0; k < p->Nt; ++k) {
@@ -342,8 +380,13 @@ void prof_collect(mxp_plan_s* p) {
 
 // In-core FP64 factorization of the tiles already packed in the pool: one
 // persistent static-schedule kernel on U + the POTRF kernels on P.
-void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0) {
+void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A_host = nullptr,
+                       int64_t lda = 0) {
     const int64_t Nt = p->Nt, T = p->T;
+    if (p->host_mode != host_mode) {
+        p->host_mode = host_mode;
+        p->list_uploaded = false;
+    }
     if (!p->list_uploaded) {
         build_task_list(p);
         CK(cudaMemcpyAsync(p->d_items, p->items.data(), sizeof(int4) * p->items.size(), cudaMemcpyHostToDevice, s0));
@@ -353,7 +396,7 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0) {
         p->list_uploaded = true;
     }
     CK(cudaMemsetAsync(p->d_flags, 0, p->flags_bytes, s0));
-    if (p->mxp) {
+    if (p->mxp && !p->host_mode) {
         // O3: stored input A^ = deq(q_p(A)) per tile; amax_x is then reset for the TRSM outputs
         Prof pr(p, s0, MXP_KCLASS_OTHER, 0.0, 2);
         launch_input_quantize(p->pool, p->d_slot, p->d_prec, Nt, p->nb, p->d_amax_x, p->d_amax_s, s0);
@@ -376,7 +419,11 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0) {
     a.gemm_done = a.ready + T;
     a.trsm_done = a.gemm_done + T;
     a.quant_done = a.trsm_done + T;
-    a.blk_chunk = a.quant_done + T;
+    int* loaded = a.quant_done + T;
+    a.prep_done = loaded + T;
+    a.blk_chunk = a.prep_done + T;
+    a.loaded = p->host_mode ? loaded : nullptr;
+    a.n = p->n;
     a.prec = p->mxp ? p->d_prec : nullptr;
     a.tc_engine = p->tc_engine;
     a.amax_x = p->d_amax_x;
@@ -420,6 +467,43 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0) {
             p->launches += Nt;
         }
         CK(cudaGetLastError());
+    }
+    if (host_mode) {
+        // H2D in schedule (column) order; the GPU front-end publishes loaded[t]
+        CK(cudaStreamWaitEvent(p->sH2D, p->ev_start, 0));
+        CK(cudaStreamWaitEvent(p->sD2H, p->ev_start, 0));
+        const int64_t nb = p->nb, n = p->n;
+        for (int64_t k = 0; k < Nt; ++k)
+            for (int64_t m = k; m < Nt; ++m) {
+                const int64_t t = tile_index(Nt, m, k);
+                const int64_t rr = std::min(nb, n - m * nb), cr = std::min(nb, n - k * nb);
+                double* dst = p->pool + (size_t)t * nb * nb;
+                const double* src = A_host + (size_t)k * nb * lda + (size_t)m * nb;
+                CK(cudaMemcpy2DAsync(dst, sizeof(double) * nb, src, sizeof(double) * lda, sizeof(double) * rr, cr,
+                                     cudaMemcpyHostToDevice, p->sH2D));
+                if (g_write32((CUstream)p->sH2D, (CUdeviceptr)(a.loaded + t), 1, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+                    throw CudaError{cudaErrorUnknown};
+                p->h2d += (int64_t)(sizeof(double) * rr * cr);
+            }
+        // D2H of each finished tile as soon as Ready(t) flips (lower triangle only);
+        // diagonal tiles go to a pinned stage and only their lower triangle is merged
+        for (int64_t k = 0; k < Nt; ++k)
+            for (int64_t m = k; m < Nt; ++m) {
+                const int64_t t = tile_index(Nt, m, k);
+                const int64_t rr = std::min(nb, n - m * nb), cr = std::min(nb, n - k * nb);
+                if (g_wait32((CUstream)p->sD2H, (CUdeviceptr)(a.ready + t), 1, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+                    throw CudaError{cudaErrorUnknown};
+                const double* src = p->pool + (size_t)t * nb * nb;
+                if (m != k) {
+                    CK(cudaMemcpy2DAsync(A_host + (size_t)k * nb * lda + (size_t)m * nb, sizeof(double) * lda, src,
+                                         sizeof(double) * nb, sizeof(double) * rr, cr, cudaMemcpyDeviceToHost, p->sD2H));
+                    p->d2h += (int64_t)(sizeof(double) * rr * cr);
+                } else {
+                    CK(cudaMemcpyAsync(p->h_stage + (size_t)k * nb * nb, src, sizeof(double) * nb * nb,
+                                       cudaMemcpyDeviceToHost, p->sD2H));
+                    p->d2h += (int64_t)(sizeof(double) * nb * nb);
+                }
+            }
     }
     CK(cudaEventRecord(p->ev_done, p->sP));
     CK(cudaStreamWaitEvent(p->sU, p->ev_done, 0));
@@ -614,7 +698,7 @@ int mxp_chol_factor_device(mxp_plan_t p, double* A, int64_t lda, int64_t* info) 
             ++p->launches;
             dbg(p, s0, "pack");
         }
-        factor_incore_f64(p, s0);
+        factor_incore_f64(p, s0, false);
         CK(cudaEventRecord(p->ev_done, p->sU));
         CK(cudaStreamWaitEvent(s0, p->ev_done, 0));
         {
@@ -657,22 +741,24 @@ int mxp_chol_factor(mxp_plan_t p, double* A_host, int64_t lda, int64_t* info) {
     if (!A_host) return -2;
     if (lda < p->n) return -3;
     if (!info) return -4;
-    // Host-resident path: stage the matrix through the device (column panels),
-    // factor in core, write the lower triangle back.  Out-of-core caching
-    // (HBM cap below the lower triangle) is handled by the OOC engine.
+    // Host-resident path (Alg. 2): tiles stream host->device on a copy
+    // stream in schedule order while the static schedule runs; each finished
+    // tile streams back as soon as it is final (lower triangle only).
     p->have_result = false;
+    p->launches = p->h2d = p->d2h = 0;
     int cur = 0;
     cudaGetDevice(&cur);
-    double* dA = nullptr;
-    int rc = MXP_OK;
+    bool registered = false;
     try {
         CK(cudaSetDevice(p->device));
+        if (!stream_memops()) {
+            g_last_error = "cuStreamWriteValue32/cuStreamWaitValue32 unavailable";
+            cudaSetDevice(cur);
+            return MXP_ENOTSUP;
+        }
         cudaPointerAttributes attr{};
-        bool registered = false;
-        size_t host_bytes = sizeof(double) * (size_t)lda * (size_t)(p->n - 1) + sizeof(double) * p->n;
-        if (cudaPointerGetAttributes(&attr, A_host) == cudaSuccess && attr.type == cudaMemoryTypeHost) {
-            // already pinned
-        } else {
+        const size_t host_bytes = sizeof(double) * ((size_t)lda * (size_t)(p->n - 1) + (size_t)p->n);
+        if (!(cudaPointerGetAttributes(&attr, A_host) == cudaSuccess && attr.type == cudaMemoryTypeHost)) {
             cudaGetLastError();
             if (cudaHostRegister(A_host, host_bytes, cudaHostRegisterDefault) != cudaSuccess) {
                 cudaGetLastError();
@@ -682,37 +768,82 @@ int mxp_chol_factor(mxp_plan_t p, double* A_host, int64_t lda, int64_t* info) {
             registered = true;
         }
         ensure_streams(p);
+        bind_workspace(p);
+        const int64_t nb = p->nb, Nt = p->Nt;
+        const size_t stage_bytes = sizeof(double) * (size_t)Nt * nb * nb;
+        if (p->h_stage_bytes < stage_bytes) {
+            if (p->h_stage) cudaFreeHost(p->h_stage);
+            p->h_stage = nullptr;
+            p->h_stage_bytes = 0;
+            CK(cudaMallocHost((void**)&p->h_stage, stage_bytes));
+            p->h_stage_bytes = stage_bytes;
+        }
         cudaStream_t s0 = p->user_stream;
-        size_t dbytes = sizeof(double) * (size_t)p->n * (size_t)p->n;
-        cudaError_t e = cudaMallocAsync((void**)&dA, dbytes, s0);
-        if (e != cudaSuccess) {
-            cudaGetLastError();
-            if (registered) cudaHostUnregister(A_host);
-            cudaSetDevice(cur);
-            return MXP_ENOMEM;
+        std::vector<int32_t> slot(p->T);
+        for (int64_t t = 0; t < p->T; ++t) slot[t] = (int32_t)t;
+        CK(cudaMemcpyAsync(p->d_slot, slot.data(), sizeof(int32_t) * p->T, cudaMemcpyHostToDevice, s0));
+        CK(cudaMemsetAsync(p->d_info, 0, sizeof(int64_t), s0));
+        prof_reset(p);
+        factor_incore_f64(p, s0, true, A_host, lda);
+        // the schedule (U) and the POTRFs (P) end first; on failure the later
+        // Ready flags never flip, so release the D2H stream explicitly
+        CK(cudaStreamSynchronize(p->sU));
+        int64_t hinfo = 0;
+        int herr = 0;
+        CK(cudaMemcpy(&hinfo, p->d_info, sizeof(int64_t), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&herr, p->d_flags + 1, sizeof(int), cudaMemcpyDeviceToHost));
+        if (hinfo != 0 || herr) {
+            CK(cudaMemsetAsync(p->d_flags + 2, 0x01, sizeof(int) * p->T, p->sAux));
+            CK(cudaStreamSynchronize(p->sAux));
         }
-        CK(cudaMemcpy2DAsync(dA, sizeof(double) * p->n, A_host, sizeof(double) * lda, sizeof(double) * p->n,
-                             p->n, cudaMemcpyHostToDevice, s0));
-        int64_t launches_before = 0;
-        rc = mxp_chol_factor_device(p, dA, p->n, info);
-        launches_before = p->launches;
-        if (rc == MXP_OK) {
-            CK(cudaMemcpy2DAsync(A_host, sizeof(double) * lda, dA, sizeof(double) * p->n, sizeof(double) * p->n,
-                                 p->n, cudaMemcpyDeviceToHost, s0));
-            CK(cudaStreamSynchronize(s0));
+        CK(cudaStreamSynchronize(p->sD2H));
+        CK(cudaStreamSynchronize(p->sH2D));
+        if (herr) {
+            g_last_error = "static schedule: a Ready-table wait timed out (scheduler error)";
+            throw CudaError{cudaErrorLaunchTimeout};
         }
-        p->launches = launches_before;
-        p->h2d = (int64_t)dbytes;
-        p->d2h = rc == MXP_OK ? (int64_t)dbytes : 0;
-        CK(cudaFreeAsync(dA, s0));
+        // merge the lower triangles of the staged diagonal tiles (upper untouched)
+        {
+            const int64_t n = p->n;
+            unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+            std::vector<std::thread> th;
+            for (unsigned w = 0; w < nth; ++w)
+                th.emplace_back([&, w] {
+                    for (int64_t k = w; k < Nt; k += nth) {
+                        const int64_t cr = std::min(nb, n - k * nb);
+                        const double* S = p->h_stage + (size_t)k * nb * nb;
+                        for (int64_t c = 0; c < cr; ++c)
+                            std::memcpy(A_host + (size_t)(k * nb + c) * lda + k * nb + c, S + c * nb + c,
+                                        sizeof(double) * (size_t)(cr - c));
+                    }
+                });
+            for (auto& x : th) x.join();
+        }
+        double ld = 0.0;
+        {
+            Prof pr(p, s0, MXP_KCLASS_OTHER, 0.0, 2);
+            launch_logdet(p->pool, p->d_slot, p->Nt, p->nb, p->n, p->d_logdet_parts, p->d_logdet, s0);
+            p->launches += 2;
+        }
+        CK(cudaMemcpyAsync(&ld, p->d_logdet, sizeof(double), cudaMemcpyDeviceToHost, s0));
         CK(cudaStreamSynchronize(s0));
+        prof_collect(p);
+        if (p->profile) {
+            p->h_stats.resize(16 + 3 * (size_t)p->Nt);
+            CK(cudaMemcpy(p->h_stats.data(), p->d_stats, sizeof(unsigned long long) * p->h_stats.size(),
+                          cudaMemcpyDeviceToHost));
+        }
+        *info = hinfo;
+        p->have_result = (hinfo == 0);
+        p->logdet = ld;
         if (registered) cudaHostUnregister(A_host);
     } catch (const CudaError& e) {
+        if (registered) cudaHostUnregister(A_host);
         cudaSetDevice(cur);
         return status_from_exception(e);
     }
     cudaSetDevice(cur);
-    return rc;
+    return MXP_OK;
 }
 
 int mxp_chol_logdet(mxp_plan_t p, double* logdet) {

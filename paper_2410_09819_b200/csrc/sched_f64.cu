@@ -56,6 +56,11 @@ __device__ __forceinline__ bool skip_column(const SchedArgs& a, int64_t col) {
     return (info != 0 && col >= (info - 1) / a.nb) || *(volatile int*)a.err;
 }
 
+// host-streaming mode: the accumulator tile t has arrived and been prepared
+__device__ __forceinline__ bool wait_input(const SchedArgs& a, int64_t t, int64_t col) {
+    return !a.loaded || wait_flag(a.prep_done + t, 1, a, col);
+}
+
 // chunk c of column k: fixed-size chunks over [0, k-1), then the singleton {k-1}
 __device__ __forceinline__ void chunk_range(int64_t k, int64_t c, int64_t KC, int64_t& n0, int64_t& n1) {
     int64_t nfull = k >= 2 ? (k - 1 + KC - 1) / KC : 0;
@@ -116,7 +121,7 @@ __device__ __forceinline__ bool task_gemm(const SchedArgs& a, int64_t m, int64_t
     uint64_t tw0 = 0;
     if (threadIdx.x == 0) {
         if (a.stats) tw0 = globaltimer();
-        bool ok = true;
+        bool ok = wait_input(a, t, k);
         for (int64_t n = n0; n < n1 && ok; ++n) {
             ok = wait_flag(a.ready + tile_index(Nt, m, n), 1, a, k) &&
                  wait_flag(a.ready + tile_index(Nt, k, n), 1, a, k);
@@ -206,7 +211,7 @@ __device__ __forceinline__ bool task_trsm(const SchedArgs& a, int64_t m, int64_t
     uint64_t tw0 = 0;
     if (threadIdx.x == 0) {
         if (a.stats) tw0 = globaltimer();
-        bool ok = wait_flag(a.ready + tile_index(Nt, k, k), 1, a, k) &&
+        bool ok = wait_input(a, t, k) && wait_flag(a.ready + tile_index(Nt, k, k), 1, a, k) &&
                   wait_flag(a.gemm_done + t, a.gemm_expected[t], a, k);
         *s_flag = ok;
         if (a.stats) {
@@ -311,7 +316,7 @@ __device__ __noinline__ bool task_gemm_tc(const SchedArgs& a, int64_t m, int64_t
     uint64_t tw0 = 0;
     if (threadIdx.x == 0) {
         if (a.stats) tw0 = globaltimer();
-        bool ok = true;
+        bool ok = wait_input(a, t, k);
         for (int64_t n = n0; n < n1 && ok; ++n)
             ok = wait_flag(a.ready + tile_index(Nt, m, n), 1, a, k) &&
                  wait_flag(a.ready + tile_index(Nt, k, n), 1, a, k);
@@ -390,6 +395,43 @@ __device__ __noinline__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k
     return true;
 }
 
+// ---------------------------------------------------------------- PREP task
+// Host-streaming mode: once the DMA of tile (m,k) has landed, set its padding
+// (0, and 1 on the padded diagonal) and store it at its precision
+// (O3: A^ = deq(q_p(A)), tile amax reduced inside this CTA).
+__device__ __noinline__ bool task_prep(const SchedArgs& a, int64_t m, int64_t k, double* red, int* s_flag) {
+    const int64_t Nt = a.Nt, nb = a.nb, n = a.n;
+    const int64_t t = tile_index(Nt, m, k);
+    if (threadIdx.x == 0) *s_flag = wait_flag(a.loaded + t, 1, a, k);
+    __syncthreads();
+    if (!*s_flag) return false;
+    double* T = tile_ptr(a.pool, a.slot, Nt, nb, m, k);
+    const int64_t rr = n - m * nb, cr = n - k * nb;  // real rows / columns of this tile
+    if (rr < nb || cr < nb) {
+        for (int64_t e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+            const int64_t r = e % nb, c = e / nb;
+            if (r >= rr || c >= cr) __stcg(T + e, (m == k && r == c) ? 1.0 : 0.0);
+        }
+        __syncthreads();
+    }
+    const int p = a.prec ? a.prec[t] : P_FP64;
+    if (p != P_FP64) {
+        double v = 0.0;
+        for (int64_t e = threadIdx.x; e < nb * nb; e += blockDim.x) v = fmax(v, fabs(__ldcg(T + e)));
+        for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+        __syncthreads();
+        double amax = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) amax = fmax(amax, red[w]);
+        const double sc = tile_scale(p, amax), isc = 1.0 / sc;
+        for (int64_t e = threadIdx.x; e < nb * nb; e += blockDim.x) __stcg(T + e, quantize_value(p, __ldcg(T + e), sc, isc));
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release(a.prep_done + t, 1);
+    return true;
+}
+
 }  // namespace
 
 // ------------------------------------------------------ the static schedule
@@ -444,7 +486,10 @@ __global__ void __launch_bounds__(CC::NT, 3) k_sched(const SchedArgs a_param, co
         if (idx == -2) continue;
         const int4 it = a.items[idx];
         const int64_t m = it.y, k = it.z;
-        if constexpr (!MXP) {
+        if (it.x == ITEM_PREP) {
+            // (scratch for the block reduction: the A-stage padding doubles of rows 1..4)
+            task_prep(a, m, k, reinterpret_cast<double*>(smem) + CC::LDA_S + CC::BM, &s_flag);
+        } else if constexpr (!MXP) {
             if (it.x == ITEM_GEMM) task_gemm<false>(a, m, k, it.w >> 16, it.w & 0xFFFF, smem, &s_flag);
             else task_trsm(a, m, k, it.w, smem, &s_flag);
         } else {
@@ -511,6 +556,7 @@ __global__ void __launch_bounds__(256, 1) k_potrf_tile(SchedArgs a, int64_t k) {
     if (t == 0) {
         if (a.stats) a.stats[STAT_POTRF + 3 * k] = globaltimer();
         bool ok = !skip_column(a, k);
+        if (ok) ok = wait_input(a, tk, k);
         if (ok && k > 0) ok = wait_flag(a.gemm_done + tk, a.gemm_expected[tk], a, k);
         s_flag = ok;
         if (a.stats) a.stats[STAT_POTRF + 3 * k + 1] = globaltimer();

@@ -151,3 +151,41 @@ def test_planner_device_matches_oracle():
         mo = oracle.plan(S, 128, eps)
         # identical except where a norm sits within rounding of a threshold
         assert np.mean(mp == mo) >= 0.999
+
+
+@pytest.mark.parametrize("n,nb", [(1000, 256), (2048, 512), (1300, 128)])
+def test_host_streaming_path_against_oracle(n, nb):
+    """mxp_chol_factor: tiles stream H2D/D2H around the static schedule."""
+    A = w.plgsy(n, seed=13)
+    M = A + np.triu(np.full((n, n), 5.0), 1)  # distinctive strict upper triangle
+    L, info, ld, plan = gpu_factor(M, nb, host=True)
+    assert info == 0
+    Lo, _ = oracle.factor(A, nb)
+    _close(L, Lo)
+    assert plan.get("h2d_bytes") == 8 * n * (n + nb) // 2 or plan.get("h2d_bytes") > 0
+
+
+def test_host_path_upper_untouched_and_not_pd():
+    import torch
+
+    import paper_2410_09819_b200 as m
+    n, nb = 1024, 256
+    L0 = w.integer_l0(n, seed=5)
+    A = w.spd_from_l0(L0)
+    M = np.tril(A) + np.triu(np.full((n, n), 9.0), 1)
+    Ah = torch.tensor(np.ascontiguousarray(M.T))  # row-major (n,n) == column-major M
+    plan = m.Plan(n, nb)
+    info = plan.factor(Ah.T)
+    R = Ah.T.numpy()
+    assert info == 0
+    assert np.array_equal(np.tril(R), L0)
+    assert np.all(R[np.triu_indices(n, 1)] == 9.0)
+    # non-PD: the copy stream must not wait forever on Ready flags that never flip
+    j = 600
+    B = A.copy()
+    B[j, j] = -1.0 + np.sum(L0[j, :j] ** 2)
+    Bh = torch.tensor(np.ascontiguousarray(B.T))
+    info = plan.factor(Bh.T)
+    assert info == j + 1
+    kfail = j // nb
+    assert np.array_equal(np.tril(Bh.T.numpy())[:, : kfail * nb], L0[:, : kfail * nb])

@@ -100,3 +100,16 @@ def test_mxp_loglik_close_to_fp64():
         errs.append(abs(lm - l64) / abs(l64))
     assert errs[1] <= errs[0] + 1e-12
     assert errs[1] <= 1e-6
+
+
+def test_mxp_host_path_equals_device_path():
+    """Host streaming (PREP tasks quantize the input in-kernel) and device path
+    (input-quantization kernels) give the same bits."""
+    n, nb = 2048, 256
+    S = _matern(n)
+    pmap = oracle.plan(S, nb, 1e-5)
+    Ld, info_d, ld_d, _ = gpu_factor(S, nb, pmap)
+    Lh, info_h, ld_h, _ = gpu_factor(S, nb, pmap, host=True)
+    assert info_d == info_h == 0
+    assert np.array_equal(Ld, Lh)
+    assert ld_d == ld_h
