@@ -63,7 +63,9 @@ typedef enum mxp_attr {
                                      deterministic for a fixed value */
     MXP_ATTR_LOOKAHEAD = 4,       /* reserved (the task list always carries one column of lookahead) */
     MXP_ATTR_DEBUG_SYNC = 5,      /* 1 = synchronize and check after every kernel; 2 = GEMM-throughput
-                                     probe (GEMM tasks only, Ready pre-set, no POTRF: result is garbage) */
+                                     probe (GEMM tasks only, Ready pre-set, no POTRF: result is garbage);
+                                     3 = no dedicated POTRF kernels (the scheduler's fallback factors every
+                                     diagonal tile) */
     MXP_ATTR_PROFILE = 6,         /* 1 = time every launch with CUDA events on its stream (mxp_chol_kernel_stats) */
     MXP_ATTR_TC_ENGINE = 7,       /* 1 (default) = GEMM tasks of tiles below FP64 on tcgen05 (kind::tf32: 3xTF32 for
                                      FP32 tiles, 1xTF32 for FP16/FP8 values); 0 = FP64 DMMA with the same casts */

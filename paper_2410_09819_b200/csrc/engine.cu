@@ -199,6 +199,9 @@ void build_task_list(mxp_plan_s* p) {
             int64_t last = nchunks(k, KC) - 1;
             gemm_col(k, last, last + 1);
         }
+        // POTRF(k): normally claimed by the dedicated kernel; listed so the
+        // schedule can also complete on its own (fallback, see sched_f64.cu)
+        p->items.push_back(make_int4(ITEM_POTRF, (int)k, (int)k, 0));
         if (k + 1 < Nt) {
             int64_t nb1 = nchunks(k + 1, KC) - 1;  // bulk chunks of column k+1
             gemm_col(k + 1, 0, nb1);
@@ -227,7 +230,8 @@ size_t list_bytes(const mxp_plan_s* p) {
     cnt += (Nt * (Nt - 1) / 2) * (nb / 64);
     for (int64_t k = 0; k < Nt; ++k)
         for (int64_t m = k + 1; m < Nt; ++m) cnt += (p->map[tile_index(Nt, m, k)] != MXP_FP64) * (nb / 64);
-    cnt += p->T;  // PREP tasks (host-streaming mode)
+    cnt += p->T;   // PREP tasks (host-streaming mode)
+    cnt += Nt;     // POTRF claims
     return sizeof(int4) * (size_t)cnt;
 }
 
@@ -241,8 +245,9 @@ Layout layout(const mxp_plan_s* p) {
     L.slot = off;
     off += align_up(sizeof(int32_t) * p->T, 256);
     L.flags = off;
-    // counter, err, ready, gemm_done, trsm_done, quant_done, loaded, prep_done, blk_chunk; then amax_x
-    L.flags_bytes = align_up(sizeof(int) * (size_t)(2 + 6 * p->T + p->T * blocks_per_tile(p->nb)), 8) +
+    // counter, err, ready, gemm_done, trsm_done, quant_done, loaded, prep_done, blk_chunk, potrf_claim;
+    // then amax_x
+    L.flags_bytes = align_up(sizeof(int) * (size_t)(2 + 6 * p->T + p->T * blocks_per_tile(p->nb) + p->Nt), 8) +
                     sizeof(unsigned long long) * (size_t)p->T;
     off += align_up(L.flags_bytes, 256);
     L.expected = off;
@@ -296,7 +301,8 @@ void bind_workspace(mxp_plan_s* p) {
     p->d_amax_s = (double*)(p->ws + L.amax_s);
     p->d_args = (SchedArgs*)(p->ws + L.args);
     p->d_amax_x = (unsigned long long*)(p->ws + L.flags +
-                                        align_up(sizeof(int) * (size_t)(2 + 6 * p->T + p->T * blocks_per_tile(p->nb)), 8));
+                                        align_up(sizeof(int) * (size_t)(2 + 6 * p->T + p->T * blocks_per_tile(p->nb) +
+                                                                        p->Nt), 8));
     p->pool = (double*)(p->ws + L.pool);
 }
 
@@ -422,6 +428,7 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     int* loaded = a.quant_done + T;
     a.prep_done = loaded + T;
     a.blk_chunk = a.prep_done + T;
+    a.potrf_claim = a.blk_chunk + T * blocks_per_tile(p->nb);
     a.loaded = p->host_mode ? loaded : nullptr;
     a.n = p->n;
     a.prec = p->mxp ? p->d_prec : nullptr;
@@ -462,7 +469,7 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     }
     {
         Prof pr(p, p->sP, MXP_KCLASS_POTRF, (double)Nt * nb3 / 3.0, Nt);
-        if (p->debug_sync != 2) {
+        if (p->debug_sync != 2 && p->debug_sync != 3) {  // 3: every POTRF by the scheduler fallback
             for (int64_t k = 0; k < Nt; ++k) launch_potrf_tile(a, k, p->sP);
             p->launches += Nt;
         }
@@ -592,7 +599,7 @@ int mxp_chol_plan_set(mxp_plan_t p, mxp_attr_t key, int64_t v) {
         return MXP_OK;
     case MXP_ATTR_LOOKAHEAD: p->lookahead = v ? 1 : 0; return MXP_OK;
     case MXP_ATTR_DEBUG_SYNC:
-        if (v < 0 || v > 2) return -3;
+        if (v < 0 || v > 3) return -3;
         if ((v == 2) != (p->debug_sync == 2)) p->list_uploaded = false;
         p->debug_sync = (int)v;
         return MXP_OK;

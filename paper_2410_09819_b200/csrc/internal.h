@@ -16,7 +16,7 @@ __host__ __device__ inline int64_t tile_index(int64_t Nt, int64_t i, int64_t j) 
 // ---- device-resident static schedule (sched_f64.cu) ----------------------
 // Task list entries (int4): {type, m, k, w}; GEMM: w = (block << 16) | chunk,
 // TRSM: w = 64-row block index.
-enum { ITEM_GEMM = 0, ITEM_TRSM = 1, ITEM_QUANT = 2, ITEM_PREP = 3 };
+enum { ITEM_GEMM = 0, ITEM_TRSM = 1, ITEM_QUANT = 2, ITEM_PREP = 3, ITEM_POTRF = 4 };
 
 struct SchedArgs {
     double* pool;
@@ -44,6 +44,7 @@ struct SchedArgs {
     const int* loaded;         // [T] set to 1 by the copy stream after a tile's H2D; NULL = device mode
     int* prep_done;            // [T] PREP task finished (padding + input quantization)
     int64_t n;                 // real matrix order (padding of edge tiles)
+    int* potrf_claim;          // [Nt] POTRF(k) taken (dedicated kernel or scheduler fallback)
     int reserved_sms;          // SMs (smid < this) left to the POTRF kernels
     unsigned long long* stats; // optional diagnostics (MXP_ATTR_PROFILE): see STAT_*
 };

@@ -434,6 +434,182 @@ __device__ __noinline__ bool task_prep(const SchedArgs& a, int64_t m, int64_t k,
 
 }  // namespace
 
+namespace {
+constexpr int PK = 128 * 129 / 2;  // packed lower-triangle length
+__device__ __forceinline__ int pidx_c(int i, int j) { return j * 128 - j * (j - 1) / 2 + (i - j); }  // col-major
+__device__ __forceinline__ int pidx_r(int i, int j) { return i * (i + 1) / 2 + j; }                  // row-major
+
+template <class C>
+__device__ void store_acc(double (&acc)[C::MI][C::NI][2], double* Ct, int64_t ld, bool subtract) {
+#pragma unroll
+    for (int mi = 0; mi < C::MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < C::NI; ++ni)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                int r, c;
+                frag_pos<C>(mi, ni, i, r, c);
+                double* p = Ct + r + (int64_t)c * ld;
+                __stcg(p, subtract ? __ldcg(p) - acc[mi][ni][i] : acc[mi][ni][i]);
+            }
+}
+}  // namespace
+
+// Factor the diagonal tile (the claim for column k is already held).
+// NT = 256: the dedicated kernel (W_J in shared memory, 128x128 DMMA blocks);
+// NT = 128: the scheduler-CTA fallback (77 KB budget: W_J through global
+// memory, 64x128 DMMA blocks in two row halves).  Returns false on a non-PD
+// pivot (info set) -- the caller must not publish Ready.
+template <int NT>
+__device__ bool potrf_tile_body(const SchedArgs& a, int64_t k, double* smem, int* s_flag) {
+    const int t = threadIdx.x;
+    const int64_t Nt = a.Nt, nb = a.nb;
+    const int S = (int)(nb / 128);
+    double* D = tile_ptr(a.pool, a.slot, Nt, nb, k, k);
+    double* Wk = a.wbuf + k * S * (128 * 128);
+    // packed L_JJ (column-major lower); the fallback keeps the first 128
+    // doubles free (scheduler scratch lives in that stage padding)
+    double* P = smem + (NT == 256 ? 0 : 128);
+    double* R = P + PK;      // packed W_J, row-major lower (NT = 256 only)
+    using G = typename std::conditional<NT == 256, PC, CC>::type;
+    for (int J = 0; J < S; ++J) {
+        double* DJJ = D + (int64_t)J * 128 * (1 + nb);
+        double* W = Wk + J * (128 * 128);
+        for (int idx = t; idx < 128 * 128; idx += NT) {
+            int c = idx >> 7, r = idx & 127;
+            if (r >= c) P[pidx_c(r, c)] = __ldcg(DJJ + r + (int64_t)c * nb);
+        }
+        if (t == 0) *s_flag = 0;
+        __syncthreads();
+        // ---- unblocked right-looking Cholesky (kij); thread = (row, column parity)
+        const int i = t & 127, par = NT == 256 ? (t >> 7) : 0, step = NT == 256 ? 2 : 1;
+        for (int j = 0; j < 128; ++j) {
+            if (t == 0) {
+                double d = P[pidx_c(j, j)];
+                if (!(d > 0.0)) {
+                    *s_flag = 1;
+                    *(volatile int64_t*)a.dinfo = k * nb + (int64_t)J * 128 + j + 1;
+                } else {
+                    P[pidx_c(j, j)] = sqrt(d);
+                }
+            }
+            __syncthreads();
+            if (*s_flag) return false;
+            if (t > j && t < 128) P[pidx_c(t, j)] = P[pidx_c(t, j)] / P[pidx_c(j, j)];
+            __syncthreads();
+            if (i > j && t < 128 * step) {
+                const double lij = P[pidx_c(i, j)];
+                int c0 = j + 1;
+                if (step == 2 && (c0 & 1) != par) ++c0;
+                for (int c = c0; c <= i; c += step) P[pidx_c(i, c)] -= lij * P[pidx_c(c, j)];
+            }
+            __syncthreads();
+        }
+        // ---- W = L^-1 by forward substitution, one column per thread (t < 128)
+        if (t < 128) {
+            const int c = t;
+            for (int r = 0; r < 128; ++r) {
+                double s0 = (r == c) ? 1.0 : 0.0, s1 = 0.0;
+                int q = 0;
+                if (NT == 256) {
+                    for (; q + 1 < r; q += 2) {
+                        double w0 = (q >= c) ? R[pidx_r(q, c)] : 0.0;
+                        double w1 = (q + 1 >= c) ? R[pidx_r(q + 1, c)] : 0.0;
+                        s0 -= P[pidx_c(r, q)] * w0;
+                        s1 -= P[pidx_c(r, q + 1)] * w1;
+                    }
+                    if (q < r) s0 -= P[pidx_c(r, q)] * ((q >= c) ? R[pidx_r(q, c)] : 0.0);
+                    if (r >= c) R[pidx_r(r, c)] = (s0 + s1) / P[pidx_c(r, r)];
+                } else {
+                    for (q = c; q + 1 < r; q += 2) {  // own column of W, through L2
+                        s0 -= P[pidx_c(r, q)] * __ldcg(W + q + c * 128);
+                        s1 -= P[pidx_c(r, q + 1)] * __ldcg(W + q + 1 + c * 128);
+                    }
+                    if (q < r && q >= c) s0 -= P[pidx_c(r, q)] * __ldcg(W + q + c * 128);
+                    __stcg(W + r + c * 128, r >= c ? (s0 + s1) / P[pidx_c(r, r)] : 0.0);
+                }
+            }
+        }
+        __syncthreads();
+        // ---- write L_JJ (zero upper) [and W_J, col-major, zero upper]
+        for (int idx = t; idx < 128 * 128; idx += NT) {
+            int c = idx >> 7, r = idx & 127;
+            __stcg(DJJ + r + (int64_t)c * nb, r >= c ? P[pidx_c(r, c)] : 0.0);
+            if (NT == 256) __stcg(W + r + c * 128, r >= c ? R[pidx_r(r, c)] : 0.0);
+        }
+        __threadfence_block();
+        __syncthreads();
+        // ---- TRSM of the blocks below: D[I,J] = D[I,J] W^T (the mainloop
+        //      consumes all of D[I,J] before the epilogue overwrites it)
+        for (int I = J + 1; I < S; ++I)
+            for (int h = 0; h < 128 / G::BM; ++h) {
+                double acc[G::MI][G::NI][2];
+                zero_acc<G>(acc);
+                double* DIJ = D + (int64_t)I * 128 + h * G::BM + (int64_t)J * 128 * nb;
+                auto src = [&](int it, const double*& pa, const double*& pb) {
+                    pa = DIJ + (int64_t)it * BK * nb;
+                    pb = W + it * BK * 128;
+                };
+                gemm_mainloop<G>(acc, src, nb, 128, 128 / BK, smem);
+                store_acc<G>(acc, DIJ, nb, false);
+                __threadfence_block();
+                __syncthreads();
+            }
+        // ---- trailing update inside the tile
+        for (int Jp = J + 1; Jp < S; ++Jp)
+            for (int I = Jp; I < S; ++I)
+                for (int h = 0; h < 128 / G::BM; ++h) {
+                    double acc[G::MI][G::NI][2];
+                    zero_acc<G>(acc);
+                    const double* Ab = D + (int64_t)I * 128 + h * G::BM + (int64_t)J * 128 * nb;
+                    const double* Bb = D + (int64_t)Jp * 128 + (int64_t)J * 128 * nb;
+                    auto src = [&](int it, const double*& pa, const double*& pb) {
+                        pa = Ab + (int64_t)it * BK * nb;
+                        pb = Bb + (int64_t)it * BK * nb;
+                    };
+                    gemm_mainloop<G>(acc, src, nb, nb, 128 / BK, smem);
+                    store_acc<G>(acc, D + (int64_t)I * 128 + h * G::BM + (int64_t)Jp * 128 * nb, nb, true);
+                    __threadfence_block();
+                    __syncthreads();
+                }
+    }
+    return true;
+}
+
+// Thread 0: wait until tile (k,k) is fully updated, then try to take the
+// claim for POTRF(k).  `grace_ns` > 0: give the dedicated kernel that long to
+// take it first (the scheduler-CTA fallback).  Sets *s_flag = 1 iff claimed.
+__device__ void claim_potrf(const SchedArgs& a, int64_t k, uint64_t grace_ns, int* s_flag) {
+    const int64_t tk = tile_index(a.Nt, k, k);
+    bool ok = !skip_column(a, k);
+    if (ok) ok = wait_input(a, tk, k);
+    if (ok && k > 0) ok = wait_flag(a.gemm_done + tk, a.gemm_expected[tk], a, k);
+    if (ok && grace_ns) {
+        uint64_t t0 = globaltimer();
+        while (*(volatile int*)(a.potrf_claim + k) == 0 && globaltimer() - t0 < grace_ns) __nanosleep(1000);
+    }
+    *s_flag = ok && atomicCAS(a.potrf_claim + k, 0, 1) == 0;
+}
+
+__device__ void publish_potrf(const SchedArgs& a, int64_t k) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        st_release(a.ready + tile_index(a.Nt, k, k), 1);
+        if (a.stats) a.stats[STAT_POTRF + 3 * k + 2] = globaltimer();
+    }
+}
+
+// POTRF(k) in the task list: normally taken by the dedicated kernel; if it has
+// not claimed it 200 us after the tile is ready (e.g. kernels serialized by a
+// profiler, or the reserved SM busy) a scheduler CTA factors the tile itself.
+__device__ __noinline__ void task_potrf_fallback(const SchedArgs& a, int64_t k, double* smem, int* s_flag) {
+    if (threadIdx.x == 0) claim_potrf(a, k, 200000, s_flag);
+    __syncthreads();
+    if (!*s_flag) return;
+    if (potrf_tile_body<CC::NT>(a, k, smem, s_flag)) publish_potrf(a, k);
+}
+
 // ------------------------------------------------------ the static schedule
 // The arguments live in global memory (copied once per factorization) so the
 // out-of-line task functions can take them by reference without a local copy.
@@ -486,9 +662,13 @@ __global__ void __launch_bounds__(CC::NT, 3) k_sched(const SchedArgs a_param, co
         if (idx == -2) continue;
         const int4 it = a.items[idx];
         const int64_t m = it.y, k = it.z;
-        if (it.x == ITEM_PREP) {
+        // out-of-line tasks take the global copy of the arguments (*ap): a
+        // reference to the by-value kernel parameter would force a local copy
+        if (it.x == ITEM_POTRF) {
+            task_potrf_fallback(*ap, k, smem, &s_flag);
+        } else if (it.x == ITEM_PREP) {
             // (scratch for the block reduction: the A-stage padding doubles of rows 1..4)
-            task_prep(a, m, k, reinterpret_cast<double*>(smem) + CC::LDA_S + CC::BM, &s_flag);
+            task_prep(*ap, m, k, reinterpret_cast<double*>(smem) + CC::LDA_S + CC::BM, &s_flag);
         } else if constexpr (!MXP) {
             if (it.x == ITEM_GEMM) task_gemm<false>(a, m, k, it.w >> 16, it.w & 0xFFFF, smem, &s_flag);
             else task_trsm(a, m, k, it.w, smem, &s_flag);
@@ -498,15 +678,15 @@ __global__ void __launch_bounds__(CC::NT, 3) k_sched(const SchedArgs a_param, co
                 if (cp == P_FP64)
                     task_gemm<false>(a, m, k, it.w >> 16, it.w & 0xFFFF, smem, &s_flag);
                 else if (!a.tc_engine)
-                    task_gemm_cast(a, m, k, it.w >> 16, it.w & 0xFFFF, smem, &s_flag);
+                    task_gemm_cast(*ap, m, k, it.w >> 16, it.w & 0xFFFF, smem, &s_flag);
                 else if (cp == P_FP32)
-                    task_gemm_tc<true>(a, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_b, mbar, tmem, &s_flag);
+                    task_gemm_tc<true>(*ap, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_b, mbar, tmem, &s_flag);
                 else
-                    task_gemm_tc<false>(a, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_b, mbar, tmem, &s_flag);
+                    task_gemm_tc<false>(*ap, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_b, mbar, tmem, &s_flag);
             } else if (it.x == ITEM_TRSM) {
-                task_trsm_ool(a, m, k, it.w, smem, &s_flag);
+                task_trsm_ool(*ap, m, k, it.w, smem, &s_flag);
             } else {
-                task_quant(a, m, k, it.w, &s_flag);
+                task_quant(*ap, m, k, it.w, &s_flag);
             }
         }
         __syncthreads();
@@ -525,146 +705,18 @@ __global__ void __launch_bounds__(CC::NT, 3) k_sched(const SchedArgs a_param, co
 //   L_JJ = chol(D_JJ) (packed in smem, kij order) and W_J = L_JJ^-1,
 //   D[I,J] = D[I,J] W_J^T (I > J),  D[I,J'] -= D[I,J] D[J',J]^T (J < J' <= I).
 // Writes L_kk in place, W_J to wbuf (for the TRSM tasks), sets Ready(k,k).
-namespace {
-constexpr int PK = 128 * 129 / 2;  // packed lower-triangle length
-__device__ __forceinline__ int pidx_c(int i, int j) { return j * 128 - j * (j - 1) / 2 + (i - j); }  // col-major
-__device__ __forceinline__ int pidx_r(int i, int j) { return i * (i + 1) / 2 + j; }                  // row-major
-
-template <class C>
-__device__ void store_acc(double (&acc)[C::MI][C::NI][2], double* Ct, int64_t ld, bool subtract) {
-#pragma unroll
-    for (int mi = 0; mi < C::MI; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < C::NI; ++ni)
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                int r, c;
-                frag_pos<C>(mi, ni, i, r, c);
-                double* p = Ct + r + (int64_t)c * ld;
-                __stcg(p, subtract ? __ldcg(p) - acc[mi][ni][i] : acc[mi][ni][i]);
-            }
-}
-}  // namespace
-
+// The dedicated POTRF kernel: one CTA (256 threads) on a reserved SM.
 __global__ void __launch_bounds__(256, 1) k_potrf_tile(SchedArgs a, int64_t k) {
     extern __shared__ __align__(16) double smem[];
     __shared__ int s_flag;
-    const int t = threadIdx.x;
-    const int64_t Nt = a.Nt, nb = a.nb;
-    const int S = (int)(nb / 128);
-    const int64_t tk = tile_index(Nt, k, k);
-    if (t == 0) {
+    if (threadIdx.x == 0) {
         if (a.stats) a.stats[STAT_POTRF + 3 * k] = globaltimer();
-        bool ok = !skip_column(a, k);
-        if (ok) ok = wait_input(a, tk, k);
-        if (ok && k > 0) ok = wait_flag(a.gemm_done + tk, a.gemm_expected[tk], a, k);
-        s_flag = ok;
-        if (a.stats) a.stats[STAT_POTRF + 3 * k + 1] = globaltimer();
+        claim_potrf(a, k, 0, &s_flag);
+        if (a.stats && s_flag) a.stats[STAT_POTRF + 3 * k + 1] = globaltimer();
     }
     __syncthreads();
     if (!s_flag) return;
-    double* D = tile_ptr(a.pool, a.slot, Nt, nb, k, k);
-    double* Wk = a.wbuf + k * S * (128 * 128);
-    double* P = smem;        // packed L_JJ, column-major lower
-    double* R = smem + PK;   // packed W_J, row-major lower
-
-    for (int J = 0; J < S; ++J) {
-        double* DJJ = D + (int64_t)J * 128 * (1 + nb);
-        // ---- load D_JJ (lower) into packed smem
-        for (int idx = t; idx < 128 * 128; idx += 256) {
-            int c = idx >> 7, r = idx & 127;
-            if (r >= c) P[pidx_c(r, c)] = __ldcg(DJJ + r + (int64_t)c * nb);
-        }
-        if (t == 0) s_flag = 0;
-        __syncthreads();
-        // ---- unblocked right-looking Cholesky; thread = (row i, column parity p)
-        const int i = t & 127, par = t >> 7;
-        for (int j = 0; j < 128; ++j) {
-            if (t == 0) {
-                double d = P[pidx_c(j, j)];
-                if (!(d > 0.0)) {
-                    s_flag = 1;
-                    *(volatile int64_t*)a.dinfo = k * nb + (int64_t)J * 128 + j + 1;
-                } else {
-                    P[pidx_c(j, j)] = sqrt(d);
-                }
-            }
-            __syncthreads();
-            if (s_flag) return;
-            if (t > j && t < 128) P[pidx_c(t, j)] = P[pidx_c(t, j)] / P[pidx_c(j, j)];
-            __syncthreads();
-            if (i > j) {
-                const double lij = P[pidx_c(i, j)];
-                int c0 = j + 1;
-                if ((c0 & 1) != par) ++c0;
-                for (int c = c0; c <= i; c += 2) P[pidx_c(i, c)] -= lij * P[pidx_c(c, j)];
-            }
-            __syncthreads();
-        }
-        // ---- W = L^-1 by forward substitution, one column per thread (t < 128)
-        if (t < 128) {
-            const int c = t;
-            for (int r = 0; r < 128; ++r) {
-                double s0 = (r == c) ? 1.0 : 0.0, s1 = 0.0;
-                int q = 0;
-                for (; q + 1 < r; q += 2) {
-                    double w0 = (q >= c) ? R[pidx_r(q, c)] : 0.0;
-                    double w1 = (q + 1 >= c) ? R[pidx_r(q + 1, c)] : 0.0;
-                    s0 -= P[pidx_c(r, q)] * w0;
-                    s1 -= P[pidx_c(r, q + 1)] * w1;
-                }
-                if (q < r) s0 -= P[pidx_c(r, q)] * ((q >= c) ? R[pidx_r(q, c)] : 0.0);
-                if (r >= c) R[pidx_r(r, c)] = (s0 + s1) / P[pidx_c(r, r)];
-            }
-        }
-        __syncthreads();
-        // ---- write L_JJ (zero upper) and W_J (col-major, zero upper)
-        double* W = Wk + J * (128 * 128);
-        for (int idx = t; idx < 128 * 128; idx += 256) {
-            int c = idx >> 7, r = idx & 127;
-            __stcg(DJJ + r + (int64_t)c * nb, r >= c ? P[pidx_c(r, c)] : 0.0);
-            __stcg(W + r + c * 128, r >= c ? R[pidx_r(r, c)] : 0.0);
-        }
-        __threadfence_block();
-        __syncthreads();
-        // ---- TRSM of the blocks below: D[I,J] = D[I,J] W^T (mainloop consumes
-        //      all of D[I,J] before the epilogue overwrites it)
-        for (int I = J + 1; I < S; ++I) {
-            double acc[PC::MI][PC::NI][2];
-            zero_acc<PC>(acc);
-            double* DIJ = D + (int64_t)I * 128 + (int64_t)J * 128 * nb;
-            auto src = [&](int it, const double*& pa, const double*& pb) {
-                pa = DIJ + (int64_t)it * BK * nb;
-                pb = W + it * BK * 128;
-            };
-            gemm_mainloop<PC>(acc, src, nb, 128, 128 / BK, smem);
-            store_acc<PC>(acc, DIJ, nb, false);
-            __threadfence_block();
-            __syncthreads();
-        }
-        // ---- trailing update inside the tile
-        for (int Jp = J + 1; Jp < S; ++Jp)
-            for (int I = Jp; I < S; ++I) {
-                double acc[PC::MI][PC::NI][2];
-                zero_acc<PC>(acc);
-                const double* Ab = D + (int64_t)I * 128 + (int64_t)J * 128 * nb;
-                const double* Bb = D + (int64_t)Jp * 128 + (int64_t)J * 128 * nb;
-                auto src = [&](int it, const double*& pa, const double*& pb) {
-                    pa = Ab + (int64_t)it * BK * nb;
-                    pb = Bb + (int64_t)it * BK * nb;
-                };
-                gemm_mainloop<PC>(acc, src, nb, nb, 128 / BK, smem);
-                store_acc<PC>(acc, D + (int64_t)I * 128 + (int64_t)Jp * 128 * nb, nb, true);
-                __threadfence_block();
-                __syncthreads();
-            }
-    }
-    __threadfence();
-    __syncthreads();
-    if (t == 0) {
-        st_release(a.ready + tk, 1);
-        if (a.stats) a.stats[STAT_POTRF + 3 * k + 2] = globaltimer();
-    }
+    if (potrf_tile_body<256>(a, k, smem, &s_flag)) publish_potrf(a, k);
 }
 
 // ------------------------------------------------------ input quantization

@@ -189,3 +189,22 @@ def test_host_path_upper_untouched_and_not_pd():
     assert info == j + 1
     kfail = j // nb
     assert np.array_equal(np.tril(Bh.T.numpy())[:, : kfail * nb], L0[:, : kfail * nb])
+
+
+@pytest.mark.parametrize("host", [False, True])
+def test_potrf_fallback_inside_the_schedule(host):
+    """debug_sync=3: no dedicated POTRF kernels; the scheduler CTAs claim and
+    factor every diagonal tile themselves (the path a kernel-serializing
+    profiler exercises).  Same parity bar."""
+    A = w.kms(1024, 0.5)
+    L, info, ld, _ = gpu_factor(A, 256, attrs={"debug_sync": 3}, host=host)
+    assert info == 0
+    Lo, _ = oracle.factor(A, 256)
+    _close(L, Lo)
+    L0 = w.integer_l0(1024, seed=3)
+    L, info, _, _ = gpu_factor(w.spd_from_l0(L0), 256, attrs={"debug_sync": 3}, host=host)
+    assert info == 0 and np.array_equal(L, L0)
+    B = w.spd_from_l0(L0)
+    B[700, 700] = -1.0 + np.sum(L0[700, :700] ** 2)
+    _, info, _, _ = gpu_factor(B, 256, attrs={"debug_sync": 3}, host=host)
+    assert info == 701
