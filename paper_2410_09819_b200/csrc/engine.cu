@@ -97,6 +97,8 @@ struct mxp_plan_s {
     SchedArgs* d_args = nullptr;
     SchedArgs h_args{};
     bool host_mode = false;        // task list built for the host-streaming path (PREP tasks)
+    int64_t slots = 0;             // tile slots in the device pool (T in core; fewer out of core)
+    std::vector<int32_t> slot_plan, prev_owner;  // out-of-core slot assignment (host mode)
     cudaStream_t sH2D = 0, sD2H = 0, sAux = 0;
     double* h_stage = nullptr;     // pinned staging for the diagonal tiles (upper triangle untouched)
     size_t h_stage_bytes = 0;
@@ -235,6 +237,61 @@ size_t list_bytes(const mxp_plan_s* p) {
     return sizeof(int4) * (size_t)cnt;
 }
 
+size_t flag_ints(const mxp_plan_s* p) {
+    return (size_t)(2 + 7 * p->T + p->T * blocks_per_tile(p->nb) + 2 * p->Nt);
+}
+
+// Tile slots of the device pool: every lower tile in core; with
+// MXP_ATTR_HBM_BYTES_CAP the pool shrinks to the cap and the host-streaming
+// path recycles the slots of dead tiles (out of core).
+int64_t pool_slots(const mxp_plan_s* p) {
+    if (p->hbm_cap <= 0) return p->T;
+    const int64_t tile_bytes = (int64_t)sizeof(double) * p->nb * p->nb;
+    return std::max<int64_t>(1, std::min<int64_t>(p->T, p->hbm_cap / tile_bytes));
+}
+
+// (m, n) of the column-major lower-tile index t
+void tile_coords(int64_t Nt, int64_t t, int64_t& m, int64_t& n) {
+    n = 0;
+    while (t >= Nt - n) {
+        t -= Nt - n;
+        ++n;
+    }
+    m = n + t;
+}
+
+// Static slot plan for the streaming path (the schedule is known in advance,
+// P:152): tile (c, n) is dead once column c is final (its last uses are
+// column c's GEMMs as B operand / row c as A operand, and TRSM(., c) for the
+// diagonal), so the tiles born for column j (loaded during iteration j-1)
+// may take the slots freed by columns <= j-2.  prev_owner[t] is the tile whose
+// death (and write-back) the H2D of t must wait for.  Returns false if the
+// pool cannot hold the live set (re-fetching evicted live tiles, the paper's
+// V2 regime, is not implemented: MXP_ENOMEM).
+bool plan_slots(mxp_plan_s* p, int64_t C) {
+    const int64_t Nt = p->Nt, T = p->T;
+    p->slot_plan.assign(T, -1);
+    p->prev_owner.assign(T, -1);
+    std::vector<int32_t> owner(C, -1), freelist;
+    for (int64_t s = C - 1; s >= 0; --s) freelist.push_back((int32_t)s);
+    std::vector<std::vector<int32_t>> freed_at(Nt);
+    for (int64_t j = 0; j < Nt; ++j) {
+        if (j >= 2)
+            for (int32_t s : freed_at[j - 2]) freelist.push_back(s);
+        for (int64_t m = j; m < Nt; ++m) {
+            if (freelist.empty()) return false;
+            const int32_t s = freelist.back();
+            freelist.pop_back();
+            const int64_t t = tile_index(Nt, m, j);
+            p->slot_plan[t] = s;
+            p->prev_owner[t] = owner[s];
+            owner[s] = (int32_t)t;
+        }
+        for (int64_t n = 0; n <= j; ++n) freed_at[j].push_back(p->slot_plan[tile_index(Nt, j, n)]);
+    }
+    return true;
+}
+
 struct Layout {
     size_t slot, flags, flags_bytes, expected, items, wbuf, stats, prec, amax_x, amax_s, args, pool, total;
 };
@@ -245,10 +302,9 @@ Layout layout(const mxp_plan_s* p) {
     L.slot = off;
     off += align_up(sizeof(int32_t) * p->T, 256);
     L.flags = off;
-    // counter, err, ready, gemm_done, trsm_done, quant_done, loaded, prep_done, blk_chunk, potrf_claim;
-    // then amax_x
-    L.flags_bytes = align_up(sizeof(int) * (size_t)(2 + 6 * p->T + p->T * blocks_per_tile(p->nb) + p->Nt), 8) +
-                    sizeof(unsigned long long) * (size_t)p->T;
+    // counter, err, ready, gemm_done, trsm_done, quant_done, loaded, prep_done, blk_chunk, potrf_claim,
+    // col_ready, d2h_done; then amax_x
+    L.flags_bytes = align_up(sizeof(int) * flag_ints(p), 8) + sizeof(unsigned long long) * (size_t)p->T;
     off += align_up(L.flags_bytes, 256);
     L.expected = off;
     off += align_up(sizeof(int) * p->T, 256);
@@ -265,7 +321,7 @@ Layout layout(const mxp_plan_s* p) {
     L.args = off;
     off += align_up(sizeof(SchedArgs), 256);
     L.pool = off;
-    off += sizeof(double) * (size_t)p->T * p->nb * p->nb;
+    off += sizeof(double) * (size_t)pool_slots(p) * p->nb * p->nb;
     L.total = off;
     return L;
 }
@@ -300,9 +356,7 @@ void bind_workspace(mxp_plan_s* p) {
     p->d_prec = (uint8_t*)(p->ws + L.prec);
     p->d_amax_s = (double*)(p->ws + L.amax_s);
     p->d_args = (SchedArgs*)(p->ws + L.args);
-    p->d_amax_x = (unsigned long long*)(p->ws + L.flags +
-                                        align_up(sizeof(int) * (size_t)(2 + 6 * p->T + p->T * blocks_per_tile(p->nb) +
-                                                                        p->Nt), 8));
+    p->d_amax_x = (unsigned long long*)(p->ws + L.flags + align_up(sizeof(int) * flag_ints(p), 8));
     p->pool = (double*)(p->ws + L.pool);
 }
 
@@ -429,6 +483,9 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     a.prep_done = loaded + T;
     a.blk_chunk = a.prep_done + T;
     a.potrf_claim = a.blk_chunk + T * blocks_per_tile(p->nb);
+    a.col_ready = a.potrf_claim + Nt;
+    int* d2h_done = a.col_ready + Nt;
+    a.logdet_parts = p->d_logdet_parts;
     a.loaded = p->host_mode ? loaded : nullptr;
     a.n = p->n;
     a.prec = p->mxp ? p->d_prec : nullptr;
@@ -484,8 +541,18 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
             for (int64_t m = k; m < Nt; ++m) {
                 const int64_t t = tile_index(Nt, m, k);
                 const int64_t rr = std::min(nb, n - m * nb), cr = std::min(nb, n - k * nb);
-                double* dst = p->pool + (size_t)t * nb * nb;
+                double* dst = p->pool + (size_t)p->slot_plan[t] * nb * nb;
                 const double* src = A_host + (size_t)k * nb * lda + (size_t)m * nb;
+                const int32_t prev = p->prev_owner[t];
+                if (prev >= 0) {  // out of core: the slot's previous tile must be dead and written back
+                    int64_t pm = 0, pc = 0;
+                    tile_coords(Nt, prev, pm, pc);
+                    if (g_wait32((CUstream)p->sH2D, (CUdeviceptr)(a.col_ready + pm), (cuuint32_t)(Nt - pm),
+                                 CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS ||
+                        g_wait32((CUstream)p->sH2D, (CUdeviceptr)(d2h_done + prev), 1, CU_STREAM_WAIT_VALUE_GEQ) !=
+                            CUDA_SUCCESS)
+                        throw CudaError{cudaErrorUnknown};
+                }
                 CK(cudaMemcpy2DAsync(dst, sizeof(double) * nb, src, sizeof(double) * lda, sizeof(double) * rr, cr,
                                      cudaMemcpyHostToDevice, p->sH2D));
                 if (g_write32((CUstream)p->sH2D, (CUdeviceptr)(a.loaded + t), 1, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
@@ -500,7 +567,7 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
                 const int64_t rr = std::min(nb, n - m * nb), cr = std::min(nb, n - k * nb);
                 if (g_wait32((CUstream)p->sD2H, (CUdeviceptr)(a.ready + t), 1, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
                     throw CudaError{cudaErrorUnknown};
-                const double* src = p->pool + (size_t)t * nb * nb;
+                const double* src = p->pool + (size_t)p->slot_plan[t] * nb * nb;
                 if (m != k) {
                     CK(cudaMemcpy2DAsync(A_host + (size_t)k * nb * lda + (size_t)m * nb, sizeof(double) * lda, src,
                                          sizeof(double) * nb, sizeof(double) * rr, cr, cudaMemcpyDeviceToHost, p->sD2H));
@@ -510,6 +577,9 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
                                        cudaMemcpyDeviceToHost, p->sD2H));
                     p->d2h += (int64_t)(sizeof(double) * nb * nb);
                 }
+                if (g_write32((CUstream)p->sD2H, (CUdeviceptr)(d2h_done + t), 1, CU_STREAM_WRITE_VALUE_DEFAULT) !=
+                    CUDA_SUCCESS)
+                    throw CudaError{cudaErrorUnknown};
             }
     }
     CK(cudaEventRecord(p->ev_done, p->sP));
@@ -584,6 +654,12 @@ int mxp_chol_plan_set(mxp_plan_t p, mxp_attr_t key, int64_t v) {
     case MXP_ATTR_STREAM: p->user_stream = (cudaStream_t)(intptr_t)v; return MXP_OK;
     case MXP_ATTR_HBM_BYTES_CAP:
         if (v < 0) return -3;
+        if (p->ws && !p->ws_owned) return MXP_ESTATE;  // changes the workspace size
+        if (p->ws_owned) {
+            cudaFree(p->ws);
+            p->ws = nullptr;
+            p->ws_owned = false;
+        }
         p->hbm_cap = v;
         return MXP_OK;
     case MXP_ATTR_SPLITK_TILES:
@@ -651,7 +727,7 @@ int mxp_chol_plan_get(mxp_plan_t p, mxp_attr_t key, int64_t* v) {
     case MXP_ATTR_GPU_LAUNCHES: *v = p->launches; return MXP_OK;
     case MXP_ATTR_H2D_BYTES: *v = p->h2d; return MXP_OK;
     case MXP_ATTR_D2H_BYTES: *v = p->d2h; return MXP_OK;
-    case MXP_ATTR_POOL_SLOTS: *v = p->T; return MXP_OK;
+    case MXP_ATTR_POOL_SLOTS: *v = pool_slots(p); return MXP_OK;
     case MXP_ATTR_NT: *v = p->Nt; return MXP_OK;
     default: return -2;
     }
@@ -690,6 +766,11 @@ int mxp_chol_factor_device(mxp_plan_t p, double* A, int64_t lda, int64_t* info) 
     cudaGetDevice(&cur);
     try {
         CK(cudaSetDevice(p->device));
+        if (pool_slots(p) < p->T) {
+            g_last_error = "device-resident factorization needs every tile in the pool (HBM cap below the lower triangle)";
+            cudaSetDevice(cur);
+            return MXP_ENOMEM;
+        }
         ensure_streams(p);
         bind_workspace(p);
         cudaStream_t s0 = p->user_stream;
@@ -711,8 +792,8 @@ int mxp_chol_factor_device(mxp_plan_t p, double* A, int64_t lda, int64_t* info) 
         {
             Prof pr(p, s0, MXP_KCLASS_OTHER, 0.0, 3);
             launch_unpack_f64(A, lda, p->n, p->pool, p->d_slot, p->Nt, p->nb, 0, p->Nt, s0);
-            launch_logdet(p->pool, p->d_slot, p->Nt, p->nb, p->n, p->d_logdet_parts, p->d_logdet, s0);
-            p->launches += 3;
+            launch_logdet_final(p->d_logdet_parts, p->Nt, p->d_logdet, s0);
+            p->launches += 2;
             dbg(p, s0, "unpack");
         }
         int64_t hinfo = 0;
@@ -786,9 +867,15 @@ int mxp_chol_factor(mxp_plan_t p, double* A_host, int64_t lda, int64_t* info) {
             p->h_stage_bytes = stage_bytes;
         }
         cudaStream_t s0 = p->user_stream;
-        std::vector<int32_t> slot(p->T);
-        for (int64_t t = 0; t < p->T; ++t) slot[t] = (int32_t)t;
-        CK(cudaMemcpyAsync(p->d_slot, slot.data(), sizeof(int32_t) * p->T, cudaMemcpyHostToDevice, s0));
+        const int64_t C = pool_slots(p);
+        if (!plan_slots(p, C)) {
+            g_last_error = "HBM cap below the out-of-core working set (live tiles of two columns)";
+            if (registered) cudaHostUnregister(A_host);
+            cudaSetDevice(cur);
+            return MXP_ENOMEM;
+        }
+        p->slots = C;
+        CK(cudaMemcpyAsync(p->d_slot, p->slot_plan.data(), sizeof(int32_t) * p->T, cudaMemcpyHostToDevice, s0));
         CK(cudaMemsetAsync(p->d_info, 0, sizeof(int64_t), s0));
         prof_reset(p);
         factor_incore_f64(p, s0, true, A_host, lda);
@@ -800,7 +887,10 @@ int mxp_chol_factor(mxp_plan_t p, double* A_host, int64_t lda, int64_t* info) {
         CK(cudaMemcpy(&hinfo, p->d_info, sizeof(int64_t), cudaMemcpyDeviceToHost));
         CK(cudaMemcpy(&herr, p->d_flags + 1, sizeof(int), cudaMemcpyDeviceToHost));
         if (hinfo != 0 || herr) {
+            // release the copy streams: Ready flags (D2H gates) and column counters (slot reuse gates)
             CK(cudaMemsetAsync(p->d_flags + 2, 0x01, sizeof(int) * p->T, p->sAux));
+            int* col_ready = p->d_flags + 2 + 6 * p->T + p->T * blocks_per_tile(p->nb) + p->Nt;
+            CK(cudaMemsetAsync(col_ready, 0x7f, sizeof(int) * p->Nt, p->sAux));
             CK(cudaStreamSynchronize(p->sAux));
         }
         CK(cudaStreamSynchronize(p->sD2H));
@@ -829,8 +919,8 @@ int mxp_chol_factor(mxp_plan_t p, double* A_host, int64_t lda, int64_t* info) {
         double ld = 0.0;
         {
             Prof pr(p, s0, MXP_KCLASS_OTHER, 0.0, 2);
-            launch_logdet(p->pool, p->d_slot, p->Nt, p->nb, p->n, p->d_logdet_parts, p->d_logdet, s0);
-            p->launches += 2;
+            launch_logdet_final(p->d_logdet_parts, p->Nt, p->d_logdet, s0);
+            p->launches += 1;
         }
         CK(cudaMemcpyAsync(&ld, p->d_logdet, sizeof(double), cudaMemcpyDeviceToHost, s0));
         CK(cudaStreamSynchronize(s0));

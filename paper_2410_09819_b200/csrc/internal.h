@@ -45,6 +45,9 @@ struct SchedArgs {
     int* prep_done;            // [T] PREP task finished (padding + input quantization)
     int64_t n;                 // real matrix order (padding of edge tiles)
     int* potrf_claim;          // [Nt] POTRF(k) taken (dedicated kernel or scheduler fallback)
+    int* col_ready;            // [Nt] tiles of column k that are final (== Nt-k: column complete;
+                               //      out-of-core slot reuse waits on it)
+    double* logdet_parts;      // [Nt] sum of log L_ii over diagonal tile k (written by its POTRF)
     int reserved_sms;          // SMs (smid < this) left to the POTRF kernels
     unsigned long long* stats; // optional diagnostics (MXP_ATTR_PROFILE): see STAT_*
 };
@@ -67,9 +70,8 @@ void launch_pack_f64(const double* A, int64_t lda, int64_t n, double* pool, cons
                      int64_t Nt, int64_t nb, int64_t col0, int64_t col1, cudaStream_t s);
 void launch_unpack_f64(double* A, int64_t lda, int64_t n, const double* pool, const int32_t* slot,
                        int64_t Nt, int64_t nb, int64_t col0, int64_t col1, cudaStream_t s);
-// logdet = 2 sum_{i<n} log L_ii, fixed reduction order (deterministic)
-void launch_logdet(const double* pool, const int32_t* slot, int64_t Nt, int64_t nb, int64_t n,
-                   double* parts, double* out, cudaStream_t s);
+// logdet = 2 sum_k parts[k] in ascending k (parts from the POTRFs; deterministic)
+void launch_logdet_final(const double* parts, int64_t Nt, double* out, cudaStream_t s);
 // planner: per-tile Frobenius norms (fp64) of the lower tiles of an lda matrix
 void launch_tile_norms(const double* A, int64_t lda, int64_t n, int64_t nb, double* norms,
                        cudaStream_t s);

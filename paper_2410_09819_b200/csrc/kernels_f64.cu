@@ -55,32 +55,14 @@ void launch_unpack_f64(double* A, int64_t lda, int64_t n, const double* pool, co
 }
 
 // -------------------------------------------------------------- log-det
-// parts[j] = sum over the real diagonal entries of tile j of log L_ii (fixed
-// tree order); out = 2 * sum_j parts[j] in ascending j.
-__global__ void k_logdet_parts(const double* pool, const int32_t* slot, int64_t Nt, int64_t nb,
-                               int64_t n, double* parts) {
-    __shared__ double red[256];
-    const int64_t j = blockIdx.x;
-    const double* T = pool + (int64_t)slot[tile_index(Nt, j, j)] * nb * nb;
-    double s = 0.0;
-    for (int64_t r = threadIdx.x; r < nb; r += blockDim.x)
-        if (j * nb + r < n) s += log(T[r + r * nb]);
-    red[threadIdx.x] = s;
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
-        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) parts[j] = red[0];
-}
+// out = 2 * sum_j parts[j] in ascending j; parts[j] = sum of log L_ii
+// over the real diagonal of tile j, written by the POTRF of column j.
 __global__ void k_logdet_final(const double* parts, int64_t Nt, double* out) {
     double s = 0.0;
     for (int64_t j = 0; j < Nt; ++j) s += parts[j];
     *out = 2.0 * s;
 }
-void launch_logdet(const double* pool, const int32_t* slot, int64_t Nt, int64_t nb, int64_t n,
-                   double* parts, double* out, cudaStream_t s) {
-    k_logdet_parts<<<(unsigned)Nt, 256, 0, s>>>(pool, slot, Nt, nb, n, parts);
+void launch_logdet_final(const double* parts, int64_t Nt, double* out, cudaStream_t s) {
     k_logdet_final<<<1, 1, 0, s>>>(parts, Nt, out);
 }
 

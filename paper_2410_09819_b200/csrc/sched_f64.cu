@@ -285,6 +285,7 @@ __device__ __forceinline__ bool task_trsm(const SchedArgs& a, int64_t m, int64_t
             a.amax_s[t] = amax_of(a.amax_x + t);
             __threadfence();
             st_release(a.ready + t, 1);
+            atom_add_release(a.col_ready + k, 1);
         }
         if (a.stats) {
             atomicAdd(a.stats + STAT_TRSM_BUSY, globaltimer() - tw0);
@@ -390,7 +391,10 @@ __device__ __noinline__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k
         a.amax_s[t] = quantize_value(p, amax, sc);  // q is monotone: max|q(x)| = q(max|x|)
         __threadfence();
         int old = atom_add_release(a.quant_done + t, 1);
-        if (old + 1 == (int)(nb / 64)) st_release(a.ready + t, 1);
+        if (old + 1 == (int)(nb / 64)) {
+            st_release(a.ready + t, 1);
+            atom_add_release(a.col_ready + k, 1);
+        }
     }
     return true;
 }
@@ -591,11 +595,28 @@ __device__ void claim_potrf(const SchedArgs& a, int64_t k, uint64_t grace_ns, in
     *s_flag = ok && atomicCAS(a.potrf_claim + k, 0, 1) == 0;
 }
 
-__device__ void publish_potrf(const SchedArgs& a, int64_t k) {
+__device__ void publish_potrf(const SchedArgs& a, int64_t k, double* red) {
+    // this tile's share of log|A| = 2 sum log L_ii: fixed-order tree
+    // reduction over the real diagonal entries (deterministic)
+    const int64_t nb = a.nb;
+    const double* D = tile_ptr(a.pool, a.slot, a.Nt, nb, k, k);
+    const int64_t real = a.n - k * nb < nb ? a.n - k * nb : nb;
+    double v = 0.0;
+    for (int64_t r = threadIdx.x; r < real; r += blockDim.x) v += log(__ldcg(D + r + r * nb));
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sum = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) sum += red[w];
+        a.logdet_parts[k] = sum;
+    }
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
         st_release(a.ready + tile_index(a.Nt, k, k), 1);
+        atom_add_release(a.col_ready + k, 1);
         if (a.stats) a.stats[STAT_POTRF + 3 * k + 2] = globaltimer();
     }
 }
@@ -607,7 +628,7 @@ __device__ __noinline__ void task_potrf_fallback(const SchedArgs& a, int64_t k, 
     if (threadIdx.x == 0) claim_potrf(a, k, 200000, s_flag);
     __syncthreads();
     if (!*s_flag) return;
-    if (potrf_tile_body<CC::NT>(a, k, smem, s_flag)) publish_potrf(a, k);
+    if (potrf_tile_body<CC::NT>(a, k, smem, s_flag)) publish_potrf(a, k, smem + CC::LDA_S + CC::BM);
 }
 
 // ------------------------------------------------------ the static schedule
@@ -716,7 +737,7 @@ __global__ void __launch_bounds__(256, 1) k_potrf_tile(SchedArgs a, int64_t k) {
     }
     __syncthreads();
     if (!s_flag) return;
-    if (potrf_tile_body<256>(a, k, smem, &s_flag)) publish_potrf(a, k);
+    if (potrf_tile_body<256>(a, k, smem, &s_flag)) publish_potrf(a, k, smem);
 }
 
 // ------------------------------------------------------ input quantization

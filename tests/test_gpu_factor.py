@@ -208,3 +208,54 @@ def test_potrf_fallback_inside_the_schedule(host):
     B[700, 700] = -1.0 + np.sum(L0[700, :700] ** 2)
     _, info, _, _ = gpu_factor(B, 256, attrs={"debug_sync": 3}, host=host)
     assert info == 701
+
+
+@pytest.mark.parametrize("n,nb,frac", [(4096, 256, 0.6), (3000, 256, 0.65), (4096, 512, 0.7)])
+def test_out_of_core_bitwise_equals_in_core(n, nb, frac):
+    """HBM cap below the lower triangle: the streaming path recycles the slots
+    of dead tiles (each tile H2D once, D2H once); same bits as in core."""
+    import torch
+
+    import paper_2410_09819_b200 as m
+    A = w.plgsy(n, seed=21)
+    Lin, info, ld_in, _ = gpu_factor(A, nb, host=True)
+    assert info == 0
+    Nt = -(-n // nb)
+    T = Nt * (Nt + 1) // 2
+    cap = int(frac * T) * nb * nb * 8
+    plan = m.Plan(n, nb)
+    plan.set("hbm_bytes_cap", cap)
+    assert plan.get("pool_slots") < T
+    Lo, info, ld_o, plan = gpu_factor(A, nb, host=True, plan=plan)
+    assert info == 0
+    assert np.array_equal(Lo, Lin)
+    assert ld_o == ld_in
+    assert plan.get("h2d_bytes") == 8 * sum(min(nb, n - i * nb) * min(nb, n - j * nb)
+                                            for j in range(Nt) for i in range(j, Nt))
+
+
+def test_out_of_core_cap_too_small():
+    import paper_2410_09819_b200 as m
+    n, nb = 4096, 256
+    plan = m.Plan(n, nb)
+    plan.set("hbm_bytes_cap", 20 * nb * nb * 8)  # 20 slots < the live set
+    with pytest.raises(m.MxpError) as e:
+        gpu_factor(w.plgsy(n, 1), nb, host=True, plan=plan)
+    assert e.value.status == -1002
+    Ad = __import__("torch").zeros((n, n), dtype=__import__("torch").float64, device="cuda").T
+    with pytest.raises(m.MxpError):
+        plan.factor_device(Ad)  # device-resident input needs every tile in the pool
+
+
+def test_out_of_core_mxp():
+    import paper_2410_09819_b200 as m
+    n, nb = 4096, 256
+    xy = w.matern_locations(n, seed=1)
+    S = w.matern_cov(xy, 1.0, 0.02627)
+    pmap = oracle.plan(S, nb, 1e-8)
+    Lin, info, _, _ = gpu_factor(S, nb, pmap, host=True)
+    plan = m.Plan(n, nb, pmap)
+    plan.set("hbm_bytes_cap", 80 * nb * nb * 8)
+    Lo, info2, _, _ = gpu_factor(S, nb, pmap, host=True, plan=plan)
+    assert info == info2 == 0
+    assert np.array_equal(Lo, Lin)
