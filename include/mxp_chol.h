@@ -131,6 +131,37 @@ int mxp_chol_factor_device(mxp_plan_t plan, double* A_dev, int64_t lda, int64_t*
 int mxp_chol_factor(mxp_plan_t plan, double* A_host, int64_t lda, int64_t* info);
 
 /*
+ * mxp_chol_factor_matern -- factor the Matern nu = 0.5 covariance of n
+ * locations (Eq. 2, the paper's geospatial workload P:168-190)
+ * WITHOUT materializing it: every tile is generated on the device by the
+ * schedule's PREP task right before its first use (fused generation; SURVEY
+ * N2), then stored at its precision.  L stays in the plan's pool (read it
+ * with mxp_chol_get_factor_device / mxp_chol_tile_device_ptr) when the pool
+ * holds every tile; under MXP_ATTR_HBM_BYTES_CAP dead tiles are recycled and
+ * only the log-determinant survives.
+ *   xy_dev   device array of 2n doubles (x0,y0,x1,y1,...)               (arg 2)
+ *   sigma2, range_a, nugget   theta = (sigma^2, a) and a diagonal nugget  (args 3-5)
+ *   info     host pointer, receives info                                 (arg 6)
+ */
+int mxp_chol_factor_matern(mxp_plan_t plan, const double* xy_dev, double sigma2, double range_a, double nugget,
+                           int64_t* info);
+
+/* Planner (as mxp_precision_map_from_matrix_device) for the generated Matern
+ * covariance: tile norms are computed while generating the entries. */
+int mxp_precision_map_matern_device(int64_t n, int64_t nb, const double* xy_dev, double sigma2, double range_a,
+                                    double nugget, double eps, uint32_t allowed_mask, uint8_t* map_out,
+                                    double* norms_out);
+
+/* Copy the resident factor L (lower triangle) of the last successful
+ * factorization into a caller-owned device matrix (column-major, ldl >= n);
+ * MXP_ESTATE if the factor is not resident (out-of-core run). */
+int mxp_chol_get_factor_device(mxp_plan_t plan, double* L_dev, int64_t ldl);
+
+/* Device pointer to tile (i, j) of the resident factor (nb x nb, column-major,
+ * ld = nb), valid until the plan's next factorization. */
+int mxp_chol_tile_device_ptr(mxp_plan_t plan, int64_t i, int64_t j, double** ptr);
+
+/*
  * mxp_chol_logdet -- log|A| = 2 sum_i log L_ii (Eq. 1) of the
  * last successful factorization of this plan, reduced in fp64 on the device.
  * Returns MXP_ESTATE if no factorization succeeded.

@@ -23,7 +23,8 @@ EXPORTS = [
     "mxp_chol_plan", "mxp_chol_plan_set", "mxp_chol_plan_get", "mxp_chol_workspace_size",
     "mxp_chol_set_workspace", "mxp_chol_factor_device", "mxp_chol_factor", "mxp_chol_logdet",
     "mxp_precision_map_from_matrix_device", "mxp_generate_plgsy_device", "mxp_generate_kms_device",
-    "mxp_generate_matern_device",
+    "mxp_generate_matern_device", "mxp_chol_factor_matern", "mxp_precision_map_matern_device",
+    "mxp_chol_get_factor_device", "mxp_chol_tile_device_ptr",
     "mxp_chol_plan_destroy", "mxp_host_alloc", "mxp_host_free", "mxp_strerror", "mxp_last_error",
     "mxp_chol_abi_version", "mxp_chol_kernel_stats", "mxp_chol_sched_diagnostics",
 ]
@@ -79,6 +80,11 @@ def lib():
         L.mxp_last_error.restype = ctypes.c_char_p
         L.mxp_chol_abi_version.argtypes = []
         L.mxp_chol_kernel_stats.argtypes = [vp, i32, pi64, pd, pd]
+        L.mxp_chol_factor_matern.argtypes = [vp, vp, ctypes.c_double, ctypes.c_double, ctypes.c_double, pi64]
+        L.mxp_precision_map_matern_device.argtypes = [i64, i64, vp, ctypes.c_double, ctypes.c_double,
+                                                      ctypes.c_double, ctypes.c_double, ctypes.c_uint32, vp, vp]
+        L.mxp_chol_get_factor_device.argtypes = [vp, vp, i64]
+        L.mxp_chol_tile_device_ptr.argtypes = [vp, i64, i64, ctypes.POINTER(vp)]
         L.mxp_chol_sched_diagnostics.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64), i64, pi64]
         _lib = L
         return L
@@ -195,6 +201,29 @@ class Plan:
         _check("mxp_chol_factor", lib().mxp_chol_factor(self._h, ptr, lda, ctypes.byref(info)))
         return info.value
 
+    def factor_matern(self, xy, sigma2: float = 1.0, range_a: float = 0.02627, nugget: float = 0.0,
+                      stream_from_torch: bool = True) -> int:
+        """Factor the Matern covariance of locations xy (n x 2), generated tile by
+        tile on the device (never stored densely).  Returns info."""
+        import torch
+        xyd = torch.as_tensor(xy, dtype=torch.float64).to("cuda").contiguous()
+        if stream_from_torch:
+            self._stream_from_torch()
+        info = ctypes.c_int64()
+        _check("mxp_chol_factor_matern", lib().mxp_chol_factor_matern(
+            self._h, xyd.data_ptr(), float(sigma2), float(range_a), float(nugget), ctypes.byref(info)))
+        self._xy = xyd
+        return info.value
+
+    def get_factor(self, L=None):
+        """Resident factor as a (column-major view of a) device tensor."""
+        import torch
+        if L is None:
+            L = torch.zeros((self.n, self.n), dtype=torch.float64, device="cuda").T
+        ptr, ld, _ = _colmajor_ptr(L, self.n)
+        _check("mxp_chol_get_factor_device", lib().mxp_chol_get_factor_device(self._h, ptr, ld))
+        return L
+
     def kernel_stats(self) -> dict:
         """{class: (launches, ms, flops)} of the last factorization (profile=1)."""
         out = {}
@@ -241,6 +270,22 @@ def precision_map_from_matrix_device(A, nb: int, eps: float, allowed: int = 0xF)
     _check("mxp_precision_map_from_matrix_device",
            lib().mxp_precision_map_from_matrix_device(n, nb, ptr, lda, float(eps), allowed,
                                                       m.ctypes.data, f.ctypes.data))
+    return m, f
+
+
+def precision_map_matern_device(xy, nb: int, eps: float, sigma2: float = 1.0, range_a: float = 0.02627,
+                                nugget: float = 0.0, allowed: int = 0xF):
+    """Planner on the generated Matern covariance -> (uint8 map, tile norms)."""
+    import numpy as np
+    import torch
+    xyd = torch.as_tensor(xy, dtype=torch.float64).to("cuda").contiguous()
+    n = xyd.shape[0]
+    Nt = -(-n // nb)
+    m = np.empty(Nt * (Nt + 1) // 2, np.uint8)
+    f = np.empty(Nt * (Nt + 1) // 2, np.float64)
+    _check("mxp_precision_map_matern_device",
+           lib().mxp_precision_map_matern_device(n, nb, xyd.data_ptr(), float(sigma2), float(range_a),
+                                                 float(nugget), float(eps), allowed, m.ctypes.data, f.ctypes.data))
     return m, f
 
 

@@ -77,6 +77,7 @@ struct mxp_plan_s {
     double* d_logdet = nullptr;
     double* d_logdet_parts = nullptr;
     int32_t* d_slot = nullptr;
+    int32_t* d_prev = nullptr;     // previous tile of each tile's slot (out-of-core reuse)
     int* d_flags = nullptr;        // counter, err, ready[T], gemm_done[T], trsm_done[T], blk_chunk[T*NB]
     size_t flags_bytes = 0;
     int* d_expected = nullptr;     // gemm_expected[T]
@@ -272,6 +273,10 @@ bool plan_slots(mxp_plan_s* p, int64_t C) {
     const int64_t Nt = p->Nt, T = p->T;
     p->slot_plan.assign(T, -1);
     p->prev_owner.assign(T, -1);
+    if (C >= T) {  // in core: every tile keeps its own slot (L stays resident)
+        for (int64_t t = 0; t < T; ++t) p->slot_plan[t] = (int32_t)t;
+        return true;
+    }
     std::vector<int32_t> owner(C, -1), freelist;
     for (int64_t s = C - 1; s >= 0; --s) freelist.push_back((int32_t)s);
     std::vector<std::vector<int32_t>> freed_at(Nt);
@@ -293,13 +298,15 @@ bool plan_slots(mxp_plan_s* p, int64_t C) {
 }
 
 struct Layout {
-    size_t slot, flags, flags_bytes, expected, items, wbuf, stats, prec, amax_x, amax_s, args, pool, total;
+    size_t slot, prev, flags, flags_bytes, expected, items, wbuf, stats, prec, amax_x, amax_s, args, pool, total;
 };
 
 Layout layout(const mxp_plan_s* p) {
     Layout L{};
     size_t off = 256 + align_up(sizeof(double) * (p->Nt + 2), 256);  // info, logdet parts
     L.slot = off;
+    off += align_up(sizeof(int32_t) * p->T, 256);
+    L.prev = off;
     off += align_up(sizeof(int32_t) * p->T, 256);
     L.flags = off;
     // counter, err, ready, gemm_done, trsm_done, quant_done, loaded, prep_done, blk_chunk, potrf_claim,
@@ -347,6 +354,7 @@ void bind_workspace(mxp_plan_s* p) {
     p->d_logdet = (double*)(p->ws + 256);
     p->d_logdet_parts = p->d_logdet + 1;
     p->d_slot = (int32_t*)(p->ws + L.slot);
+    p->d_prev = (int32_t*)(p->ws + L.prev);
     p->d_flags = (int*)(p->ws + L.flags);
     p->flags_bytes = L.flags_bytes;
     p->d_expected = (int*)(p->ws + L.expected);
@@ -440,8 +448,13 @@ void prof_collect(mxp_plan_s* p) {
 
 // In-core FP64 factorization of the tiles already packed in the pool: one
 // persistent static-schedule kernel on U + the POTRF kernels on P.
+struct GenSource {  // fused on-device generation of the input tiles (N2)
+    const double* xy = nullptr;
+    double sigma2 = 1.0, range = 1.0, nugget = 0.0;
+};
+
 void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A_host = nullptr,
-                       int64_t lda = 0) {
+                       int64_t lda = 0, const GenSource* gen = nullptr) {
     const int64_t Nt = p->Nt, T = p->T;
     if (p->host_mode != host_mode) {
         p->host_mode = host_mode;
@@ -486,8 +499,16 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     a.col_ready = a.potrf_claim + Nt;
     int* d2h_done = a.col_ready + Nt;
     a.logdet_parts = p->d_logdet_parts;
-    a.loaded = p->host_mode ? loaded : nullptr;
+    a.loaded = (p->host_mode && !gen) ? loaded : nullptr;
     a.n = p->n;
+    a.gen_mode = gen ? 1 : 0;
+    a.prev_owner = p->d_prev;
+    if (gen) {
+        a.gen_xy = gen->xy;
+        a.gen_sigma2 = gen->sigma2;
+        a.gen_range = gen->range;
+        a.gen_nugget = gen->nugget;
+    }
     a.prec = p->mxp ? p->d_prec : nullptr;
     a.tc_engine = p->tc_engine;
     a.amax_x = p->d_amax_x;
@@ -532,7 +553,7 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
         }
         CK(cudaGetLastError());
     }
-    if (host_mode) {
+    if (host_mode && !gen) {
         // H2D in schedule (column) order; the GPU front-end publishes loaded[t]
         CK(cudaStreamWaitEvent(p->sH2D, p->ev_start, 0));
         CK(cudaStreamWaitEvent(p->sD2H, p->ev_start, 0));
@@ -775,9 +796,11 @@ int mxp_chol_factor_device(mxp_plan_t p, double* A, int64_t lda, int64_t* info) 
         bind_workspace(p);
         cudaStream_t s0 = p->user_stream;
         // slot table (identity in-core) + info reset, ordered on the user stream
-        std::vector<int32_t> slot(p->T);
-        for (int64_t t = 0; t < p->T; ++t) slot[t] = (int32_t)t;
-        CK(cudaMemcpyAsync(p->d_slot, slot.data(), sizeof(int32_t) * p->T, cudaMemcpyHostToDevice, s0));
+        p->slot_plan.resize(p->T);
+        p->prev_owner.assign(p->T, -1);
+        for (int64_t t = 0; t < p->T; ++t) p->slot_plan[t] = (int32_t)t;
+        CK(cudaMemcpyAsync(p->d_slot, p->slot_plan.data(), sizeof(int32_t) * p->T, cudaMemcpyHostToDevice, s0));
+        CK(cudaMemcpyAsync(p->d_prev, p->prev_owner.data(), sizeof(int32_t) * p->T, cudaMemcpyHostToDevice, s0));
         CK(cudaMemsetAsync(p->d_info, 0, sizeof(int64_t), s0));
         prof_reset(p);
         {
@@ -876,6 +899,7 @@ int mxp_chol_factor(mxp_plan_t p, double* A_host, int64_t lda, int64_t* info) {
         }
         p->slots = C;
         CK(cudaMemcpyAsync(p->d_slot, p->slot_plan.data(), sizeof(int32_t) * p->T, cudaMemcpyHostToDevice, s0));
+        CK(cudaMemcpyAsync(p->d_prev, p->prev_owner.data(), sizeof(int32_t) * p->T, cudaMemcpyHostToDevice, s0));
         CK(cudaMemsetAsync(p->d_info, 0, sizeof(int64_t), s0));
         prof_reset(p);
         factor_incore_f64(p, s0, true, A_host, lda);
@@ -951,29 +975,13 @@ int mxp_chol_logdet(mxp_plan_t p, double* logdet) {
     return MXP_OK;
 }
 
-int mxp_precision_map_from_matrix_device(int64_t n, int64_t nb, const double* A, int64_t lda, double eps,
-                                         uint32_t allowed, uint8_t* map_out, double* norms_out) {
-    if (n < 1) return -1;
-    if (nb < 1) return -2;
-    if (!A) return -3;
-    if (lda < n) return -4;
-    if (!(eps > 0.0 && eps < 1.0)) return -5;
-    if (!(allowed & 1u) || (allowed & ~0xFu)) return -6;
-    if (!map_out) return -7;
-    int64_t Nt = (n + nb - 1) / nb, T = Nt * (Nt + 1) / 2;
-    double* dn = nullptr;
-    std::vector<double> f(T);
-    try {
-        CK(cudaMalloc(&dn, sizeof(double) * T));
-        launch_tile_norms(A, lda, n, nb, dn, 0);
-        CK(cudaGetLastError());
-        CK(cudaMemcpy(f.data(), dn, sizeof(double) * T, cudaMemcpyDeviceToHost));
-        CK(cudaFree(dn));
-    } catch (const CudaError& e) {
-        if (dn) cudaFree(dn);
-        return status_from_exception(e);
-    }
-    // F with off-diagonal tiles counted twice; criterion P:335 (G6)
+}  // extern "C"
+
+namespace {
+// P:335 criterion (G6) from per-tile norms: F with off-diagonal tiles counted
+// twice; least precise allowed p with Nt f_ij / F < eps / u_p.
+int plan_from_norms(int64_t Nt, const std::vector<double>& f, double eps, uint32_t allowed, uint8_t* map_out,
+                    double* norms_out) {
     double ss = 0.0;
     for (int64_t j = 0; j < Nt; ++j)
         for (int64_t i = j; i < Nt; ++i) {
@@ -1000,6 +1008,162 @@ int mxp_precision_map_from_matrix_device(int64_t n, int64_t nb, const double* A,
             map_out[t] = c;
             if (norms_out) norms_out[t] = f[t];
         }
+    return MXP_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int mxp_precision_map_from_matrix_device(int64_t n, int64_t nb, const double* A, int64_t lda, double eps,
+                                         uint32_t allowed, uint8_t* map_out, double* norms_out) {
+    if (n < 1) return -1;
+    if (nb < 1) return -2;
+    if (!A) return -3;
+    if (lda < n) return -4;
+    if (!(eps > 0.0 && eps < 1.0)) return -5;
+    if (!(allowed & 1u) || (allowed & ~0xFu)) return -6;
+    if (!map_out) return -7;
+    int64_t Nt = (n + nb - 1) / nb, T = Nt * (Nt + 1) / 2;
+    double* dn = nullptr;
+    std::vector<double> f(T);
+    try {
+        CK(cudaMalloc(&dn, sizeof(double) * T));
+        launch_tile_norms(A, lda, n, nb, dn, 0);
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(f.data(), dn, sizeof(double) * T, cudaMemcpyDeviceToHost));
+        CK(cudaFree(dn));
+    } catch (const CudaError& e) {
+        if (dn) cudaFree(dn);
+        return status_from_exception(e);
+    }
+    return plan_from_norms(Nt, f, eps, allowed, map_out, norms_out);
+}
+
+int mxp_precision_map_matern_device(int64_t n, int64_t nb, const double* xy_dev, double sigma2, double range_a,
+                                    double nugget, double eps, uint32_t allowed, uint8_t* map_out,
+                                    double* norms_out) {
+    if (n < 1) return -1;
+    if (nb < 1) return -2;
+    if (!xy_dev) return -3;
+    if (!(sigma2 > 0.0)) return -4;
+    if (!(range_a > 0.0)) return -5;
+    if (!(nugget >= 0.0)) return -6;
+    if (!(eps > 0.0 && eps < 1.0)) return -7;
+    if (!(allowed & 1u) || (allowed & ~0xFu)) return -8;
+    if (!map_out) return -9;
+    int64_t Nt = (n + nb - 1) / nb, T = Nt * (Nt + 1) / 2;
+    double* dn = nullptr;
+    std::vector<double> f(T);
+    try {
+        CK(cudaMalloc(&dn, sizeof(double) * T));
+        launch_matern_tile_norms(xy_dev, n, nb, sigma2, range_a, nugget, dn, 0);
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(f.data(), dn, sizeof(double) * T, cudaMemcpyDeviceToHost));
+        CK(cudaFree(dn));
+    } catch (const CudaError& e) {
+        if (dn) cudaFree(dn);
+        return status_from_exception(e);
+    }
+    return plan_from_norms(Nt, f, eps, allowed, map_out, norms_out);
+}
+
+int mxp_chol_factor_matern(mxp_plan_t p, const double* xy_dev, double sigma2, double range_a, double nugget,
+                           int64_t* info) {
+    if (!p) return -1;
+    if (!xy_dev) return -2;
+    if (!(sigma2 > 0.0)) return -3;
+    if (!(range_a > 0.0)) return -4;
+    if (!(nugget >= 0.0)) return -5;
+    if (!info) return -6;
+    p->have_result = false;
+    p->launches = p->h2d = p->d2h = 0;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    try {
+        CK(cudaSetDevice(p->device));
+        ensure_streams(p);
+        bind_workspace(p);
+        cudaStream_t s0 = p->user_stream;
+        const int64_t C = pool_slots(p);
+        if (!plan_slots(p, C)) {
+            g_last_error = "HBM cap below the out-of-core working set (live tiles of two columns)";
+            cudaSetDevice(cur);
+            return MXP_ENOMEM;
+        }
+        p->slots = C;
+        CK(cudaMemcpyAsync(p->d_slot, p->slot_plan.data(), sizeof(int32_t) * p->T, cudaMemcpyHostToDevice, s0));
+        CK(cudaMemcpyAsync(p->d_prev, p->prev_owner.data(), sizeof(int32_t) * p->T, cudaMemcpyHostToDevice, s0));
+        CK(cudaMemsetAsync(p->d_info, 0, sizeof(int64_t), s0));
+        prof_reset(p);
+        GenSource g;
+        g.xy = xy_dev;
+        g.sigma2 = sigma2;
+        g.range = range_a;
+        g.nugget = nugget;
+        factor_incore_f64(p, s0, true, nullptr, 0, &g);
+        CK(cudaEventRecord(p->ev_done, p->sU));
+        CK(cudaStreamWaitEvent(s0, p->ev_done, 0));
+        {
+            Prof pr(p, s0, MXP_KCLASS_OTHER, 0.0, 1);
+            launch_logdet_final(p->d_logdet_parts, p->Nt, p->d_logdet, s0);
+            p->launches += 1;
+        }
+        int64_t hinfo = 0;
+        double ld = 0.0;
+        int herr = 0;
+        CK(cudaMemcpyAsync(&hinfo, p->d_info, sizeof(int64_t), cudaMemcpyDeviceToHost, s0));
+        CK(cudaMemcpyAsync(&ld, p->d_logdet, sizeof(double), cudaMemcpyDeviceToHost, s0));
+        CK(cudaMemcpyAsync(&herr, p->d_flags + 1, sizeof(int), cudaMemcpyDeviceToHost, s0));
+        CK(cudaStreamSynchronize(s0));
+        if (herr) {
+            g_last_error = "static schedule: a Ready-table wait timed out (scheduler error)";
+            throw CudaError{cudaErrorLaunchTimeout};
+        }
+        prof_collect(p);
+        if (p->profile) {
+            p->h_stats.resize(16 + 3 * (size_t)p->Nt);
+            CK(cudaMemcpy(p->h_stats.data(), p->d_stats, sizeof(unsigned long long) * p->h_stats.size(),
+                          cudaMemcpyDeviceToHost));
+        }
+        *info = hinfo;
+        p->have_result = (hinfo == 0);
+        p->logdet = ld;
+    } catch (const CudaError& e) {
+        cudaSetDevice(cur);
+        return status_from_exception(e);
+    }
+    cudaSetDevice(cur);
+    return MXP_OK;
+}
+
+int mxp_chol_get_factor_device(mxp_plan_t p, double* L_dev, int64_t ldl) {
+    if (!p) return -1;
+    if (!L_dev) return -2;
+    if (ldl < p->n) return -3;
+    if (!p->have_result) return MXP_ESTATE;
+    if (!p->pool || p->slot_plan.empty() || pool_slots(p) < p->T) return MXP_ESTATE;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    try {
+        CK(cudaSetDevice(p->device));
+        launch_unpack_f64(L_dev, ldl, p->n, p->pool, p->d_slot, p->Nt, p->nb, 0, p->Nt, p->user_stream);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(p->user_stream));
+    } catch (const CudaError& e) {
+        cudaSetDevice(cur);
+        return status_from_exception(e);
+    }
+    cudaSetDevice(cur);
+    return MXP_OK;
+}
+
+int mxp_chol_tile_device_ptr(mxp_plan_t p, int64_t i, int64_t j, double** ptr) {
+    if (!p) return -1;
+    if (i < 0 || i >= p->Nt) return -2;
+    if (j < 0 || j > i) return -3;
+    if (!ptr) return -4;
+    if (!p->pool || p->slot_plan.empty() || pool_slots(p) < p->T) return MXP_ESTATE;
+    *ptr = p->pool + (size_t)p->slot_plan[tile_index(p->Nt, i, j)] * p->nb * p->nb;
     return MXP_OK;
 }
 

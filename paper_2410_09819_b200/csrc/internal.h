@@ -44,6 +44,10 @@ struct SchedArgs {
     const int* loaded;         // [T] set to 1 by the copy stream after a tile's H2D; NULL = device mode
     int* prep_done;            // [T] PREP task finished (padding + input quantization)
     int64_t n;                 // real matrix order (padding of edge tiles)
+    int gen_mode;              // 0: tiles come from A; 1: PREP generates Matern nu=0.5 tiles (no input copy)
+    const int32_t* prev_owner; // [T] previous tile in t's slot (-1: none); generated mode waits for its death
+    const double* gen_xy;      // [2n] locations (device)
+    double gen_sigma2, gen_range, gen_nugget;
     int* potrf_claim;          // [Nt] POTRF(k) taken (dedicated kernel or scheduler fallback)
     int* col_ready;            // [Nt] tiles of column k that are final (== Nt-k: column complete;
                                //      out-of-core slot reuse waits on it)
@@ -72,6 +76,10 @@ void launch_unpack_f64(double* A, int64_t lda, int64_t n, const double* pool, co
                        int64_t Nt, int64_t nb, int64_t col0, int64_t col1, cudaStream_t s);
 // logdet = 2 sum_k parts[k] in ascending k (parts from the POTRFs; deterministic)
 void launch_logdet_final(const double* parts, int64_t Nt, double* out, cudaStream_t s);
+// planner on a generated Matern covariance: per-tile Frobenius norms computed
+// while generating the entries (nothing stored)
+void launch_matern_tile_norms(const double* xy, int64_t n, int64_t nb, double sigma2, double range_a,
+                              double nugget, double* norms, cudaStream_t s);
 // planner: per-tile Frobenius norms (fp64) of the lower tiles of an lda matrix
 void launch_tile_norms(const double* A, int64_t lda, int64_t n, int64_t nb, double* norms,
                        cudaStream_t s);

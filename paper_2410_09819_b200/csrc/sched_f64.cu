@@ -56,9 +56,16 @@ __device__ __forceinline__ bool skip_column(const SchedArgs& a, int64_t col) {
     return (info != 0 && col >= (info - 1) / a.nb) || *(volatile int*)a.err;
 }
 
-// host-streaming mode: the accumulator tile t has arrived and been prepared
+// streaming modes (host input or generated tiles): tile t has been prepared
 __device__ __forceinline__ bool wait_input(const SchedArgs& a, int64_t t, int64_t col) {
-    return !a.loaded || wait_flag(a.prep_done + t, 1, a, col);
+    return !(a.loaded || a.gen_mode) || wait_flag(a.prep_done + t, 1, a, col);
+}
+
+// Matern nu = 0.5 covariance entry (Eq. 2 closed form)
+__device__ __forceinline__ double matern_entry(const SchedArgs& a, int64_t i, int64_t j) {
+    const double dx = a.gen_xy[2 * i] - a.gen_xy[2 * j], dy = a.gen_xy[2 * i + 1] - a.gen_xy[2 * j + 1];
+    double v = a.gen_sigma2 * exp(-sqrt(dx * dx + dy * dy) / a.gen_range);
+    return i == j ? v + a.gen_nugget : v;
 }
 
 // chunk c of column k: fixed-size chunks over [0, k-1), then the singleton {k-1}
@@ -406,12 +413,36 @@ __device__ __noinline__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k
 __device__ __noinline__ bool task_prep(const SchedArgs& a, int64_t m, int64_t k, double* red, int* s_flag) {
     const int64_t Nt = a.Nt, nb = a.nb, n = a.n;
     const int64_t t = tile_index(Nt, m, k);
-    if (threadIdx.x == 0) *s_flag = wait_flag(a.loaded + t, 1, a, k);
+    if (threadIdx.x == 0) {
+        bool ok;
+        if (a.gen_mode) {
+            ok = !skip_column(a, k);
+            const int32_t prev = a.prev_owner[t];
+            if (ok && prev >= 0) {  // out of core: the slot's previous tile (pm, .) dies with column pm
+                int64_t pm = 0, pc = 0, r = prev;
+                while (r >= Nt - pc) { r -= Nt - pc; ++pc; }
+                pm = pc + r;
+                ok = wait_flag(a.col_ready + pm, (int)(Nt - pm), a, k);
+            }
+        } else {
+            ok = wait_flag(a.loaded + t, 1, a, k);
+        }
+        *s_flag = ok;
+    }
     __syncthreads();
     if (!*s_flag) return false;
     double* T = tile_ptr(a.pool, a.slot, Nt, nb, m, k);
     const int64_t rr = n - m * nb, cr = n - k * nb;  // real rows / columns of this tile
-    if (rr < nb || cr < nb) {
+    if (a.gen_mode) {  // N2: generate the tile in place (fused generation, no input copy)
+        for (int64_t e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+            const int64_t r = e % nb, c = e / nb;
+            double v;
+            if (r < rr && c < cr) v = matern_entry(a, m * nb + r, k * nb + c);
+            else v = (m == k && r == c) ? 1.0 : 0.0;
+            __stcg(T + e, v);
+        }
+        __syncthreads();
+    } else if (rr < nb || cr < nb) {
         for (int64_t e = threadIdx.x; e < nb * nb; e += blockDim.x) {
             const int64_t r = e % nb, c = e / nb;
             if (r >= rr || c >= cr) __stcg(T + e, (m == k && r == c) ? 1.0 : 0.0);
@@ -738,6 +769,35 @@ __global__ void __launch_bounds__(256, 1) k_potrf_tile(SchedArgs a, int64_t k) {
     __syncthreads();
     if (!s_flag) return;
     if (potrf_tile_body<256>(a, k, smem, &s_flag)) publish_potrf(a, k, smem);
+}
+
+// ------------------------------------------------- generated-matrix planner
+__global__ void k_matern_tile_norms(const double* __restrict__ xy, int64_t n, int64_t nb, int64_t Nt, double sigma2,
+                                    double range_a, double nugget, double* norms) {
+    __shared__ double red[256];
+    const int64_t j = blockIdx.y, i = j + blockIdx.x;
+    if (i >= Nt) return;
+    double s = 0.0;
+    for (int64_t c = j * nb; c < (j + 1) * nb && c < n; ++c)
+        for (int64_t r = i * nb + threadIdx.x; r < (i + 1) * nb && r < n; r += blockDim.x) {
+            const double dx = xy[2 * r] - xy[2 * c], dy = xy[2 * r + 1] - xy[2 * c + 1];
+            double v = sigma2 * exp(-sqrt(dx * dx + dy * dy) / range_a);
+            if (r == c) v += nugget;
+            s += v * v;
+        }
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) norms[tile_index(Nt, i, j)] = sqrt(red[0]);
+}
+void launch_matern_tile_norms(const double* xy, int64_t n, int64_t nb, double sigma2, double range_a,
+                              double nugget, double* norms, cudaStream_t s) {
+    int64_t Nt = (n + nb - 1) / nb;
+    dim3 grid((unsigned)Nt, (unsigned)Nt, 1);
+    k_matern_tile_norms<<<grid, 256, 0, s>>>(xy, n, nb, Nt, sigma2, range_a, nugget, norms);
 }
 
 // ------------------------------------------------------ input quantization

@@ -113,3 +113,41 @@ def test_mxp_host_path_equals_device_path():
     assert info_d == info_h == 0
     assert np.array_equal(Ld, Lh)
     assert ld_d == ld_h
+
+
+@pytest.mark.parametrize("eps", [None, 1e-5, 1e-8])
+def test_generated_matern_against_oracle(eps):
+    """mxp_chol_factor_matern: tiles generated on the device inside the
+    schedule (N2).  The oracle factors the host-built matrix of the same
+    locations (device and host exp may differ in the last ulp)."""
+    import paper_2410_09819_b200 as m
+    n, nb = 2048, 256
+    xy = w.matern_locations(n, seed=1)
+    S = w.matern_cov(xy, 1.0, 0.02627)
+    pmap = None
+    if eps is not None:
+        pmap, f = m.precision_map_matern_device(xy, nb, eps)
+        mo = oracle.plan(S, nb, eps)
+        assert np.mean(pmap == mo) >= 0.999
+        fo = oracle.tile_norms(S, nb)
+        assert np.max(np.abs(f - fo) / fo) <= 1e-12
+    plan = m.Plan(n, nb, pmap)
+    info = plan.factor_matern(xy, 1.0, 0.02627)
+    assert info == 0
+    L = np.tril(plan.get_factor().cpu().numpy())
+    Lo, _ = oracle.factor(S, nb, pmap)
+    tol = 1e-10 if eps is None else 1e-4
+    assert np.max(np.abs(L - Lo)) <= tol * np.max(np.abs(Lo))
+    assert abs(plan.logdet() - oracle.logdet(Lo)) <= 1e-8 * abs(oracle.logdet(Lo))
+
+
+def test_generated_matern_out_of_core_logdet():
+    import paper_2410_09819_b200 as m
+    n, nb = 4096, 256
+    xy = w.matern_locations(n, seed=1)
+    p1 = m.Plan(n, nb)
+    assert p1.factor_matern(xy, 1.0, 0.078809) == 0
+    p2 = m.Plan(n, nb)
+    p2.set("hbm_bytes_cap", 80 * nb * nb * 8)
+    assert p2.factor_matern(xy, 1.0, 0.078809) == 0
+    assert p2.logdet() == p1.logdet()
