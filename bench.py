@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-cusolver", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-mxp", action="store_true")
+    ap.add_argument("--mxp-n", type=int, default=131072)
+    ap.add_argument("--mxp-eps", type=float, nargs="*", default=[1e-8, 1e-5])
     return ap.parse_args()
 
 
@@ -339,6 +342,58 @@ def run_ours(args):
                "how": "mxp_chol_factor on a pinned host n x n matrix; CUDA events around the call"}
         p2.close()
 
+    # C3 (BASELINE configs[2]): Matern nu=0.5 weak correlation, 4-precision map,
+    # n = 131072, generated tile by tile on the device inside the schedule;
+    # log-likelihood at y = 0 (Eq. 3 convention, G16) vs the FP64 factorization
+    mxp = None
+    if not args.no_mxp:
+        import math
+
+        import numpy as np
+
+        import workloads as w
+        torch.cuda.empty_cache()
+        nm, nbm, theta = args.mxp_n, args.nb, (1.0, 0.02627, 0.5)
+        xy = w.matern_locations(nm, seed=1)
+        xyd = torch.as_tensor(xy, device=dev).contiguous()
+        flops_m = nm ** 3 / 3
+
+        def run(pmap, reps):
+            pl = m.Plan(nm, nbm, pmap)
+            pl.set("profile", 0)
+            ts = []
+            for i in range(reps):
+                torch.cuda.synchronize()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                inf = pl.factor_matern(xyd, theta[0], theta[1])
+                e1.record(stream)
+                torch.cuda.synchronize()
+                assert inf == 0, inf
+                ts.append(e0.elapsed_time(e1) / 1e3)
+            ld_ = pl.logdet()
+            pl.close()
+            torch.cuda.empty_cache()
+            return min(ts[1:] if len(ts) > 1 else ts), ld_
+
+        t64, ld64 = run(None, 1 + max(1, args.steps // 3))
+        ll64 = -0.5 * nm * math.log(2 * math.pi) - 0.5 * ld64
+        mxp = {"workload": f"C3: Matern nu=0.5 theta=(1, 0.02627, 0.5) (weak), n={nm}, nb={nbm}, Morton-sorted "
+                           f"uniform locations (seed 1), tiles generated on the device inside the schedule",
+               "fp64": {"tflops": flops_m / t64 / 1e12, "ms": t64 * 1e3, "logdet": ld64}, "maps": {}}
+        for eps in args.mxp_eps:
+            pmap, _ = m.precision_map_matern_device(xyd, nbm, eps, theta[0], theta[1])
+            tm, ldm = run(pmap, 1 + max(1, args.steps // 3))
+            llm = -0.5 * nm * math.log(2 * math.pi) - 0.5 * ldm
+            mxp["maps"][f"{eps:g}"] = {
+                "tflops": flops_m / tm / 1e12, "ms": tm * 1e3, "speedup_vs_fp64": t64 / tm,
+                "tile_fractions_fp64_fp32_fp16_fp8": [round(float(np.mean(pmap == c)), 4) for c in range(4)],
+                "loglik_y0_rel_err": abs(llm - ll64) / abs(ll64), "logdet_abs_diff": abs(ldm - ld64),
+                "kl_eq3": ll64 - llm}
+        mxp["note"] = ("value/units: TFLOP/s = (n^3/3)/t, t = factorization incl. fused generation; loglik at "
+                       "y=0 vs the FP64 run of the same pipeline (G16); 1 warm-up + timed reps, best")
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         cpu = cpu_oracle_sample(2048, 256, args.seed)
@@ -357,6 +412,7 @@ def run_ours(args):
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": ck,
             "baselines": {"cusolver_potrf": cusolver},
+            "mxp_c3": mxp,
             "sched": sched,
             "check": {"backward_error_probe": probe, "logdet": logdet},
             "kernels": kstats,
