@@ -69,6 +69,11 @@ typedef enum mxp_attr {
     MXP_ATTR_PROFILE = 6,         /* 1 = time every launch with CUDA events on its stream (mxp_chol_kernel_stats) */
     MXP_ATTR_TC_ENGINE = 7,       /* 1 (default) = GEMM tasks of tiles below FP64 on tcgen05 (kind::tf32: 3xTF32 for
                                      FP32 tiles, 1xTF32 for FP16/FP8 values); 0 = FP64 DMMA with the same casts */
+    MXP_ATTR_RANK = 8,            /* this plan's rank in a row-cyclic distribution (tile (m,n) on rank m mod nranks) */
+    MXP_ATTR_NRANKS = 9,          /* ranks (GPUs) sharing the factorization, <= 8; peers attached with
+                                     mxp_chol_ipc_attach / mxp_chol_attach_peer_plan */
+    MXP_ATTR_SM_FIRST = 10,       /* first SM of this plan's scheduler partition (ranks co-located on one GPU) */
+    MXP_ATTR_SM_COUNT = 11,       /* SMs in the partition (0 = all) */
     MXP_ATTR_GPU_LAUNCHES = 100,  /* (get only) kernels launched by the last factorization */
     MXP_ATTR_H2D_BYTES = 101,     /* (get only) host->device bytes moved by the last factorization */
     MXP_ATTR_D2H_BYTES = 102,     /* (get only) device->host bytes moved by the last factorization */
@@ -231,6 +236,30 @@ int mxp_chol_kernel_stats(mxp_plan_t plan, int kernel_class, int64_t* launches, 
  *   written  receives the number of entries available (16 + 3 Nt)       (arg 4)
  */
 int mxp_chol_sched_diagnostics(mxp_plan_t plan, uint64_t* out, int64_t count, int64_t* written);
+
+/*
+ * Multi-GPU (SURVEY 8(e), row-cyclic P x 1; P:343-363 distributes 1D
+ * block-cyclic as well).  Every rank builds an identical plan (same n, nb, map,
+ * attributes) with its own MXP_ATTR_RANK / MXP_ATTR_NRANKS, maps its peers'
+ * workspaces, and then all ranks call the same factorization entry point
+ * (mxp_chol_factor_device with a replicated input, or mxp_chol_factor_matern).
+ * Each rank runs the tasks of its rows; every finished tile is pushed by the
+ * copy engines into each peer's pool (NVLink P2P), so every rank ends with
+ * the whole factor.  Ranks must not start factorization i+1 before every rank
+ * returned from factorization i (a barrier between calls).
+ *   mxp_chol_ipc_handle   exports this plan's workspace: handle_out receives
+ *                         a 64-byte cudaIpcMemHandle, ws_bytes its size.
+ *   mxp_chol_ipc_attach   maps peer `peer_rank`'s exported workspace (other
+ *                         process); -4 if the layouts differ.
+ *   mxp_chol_attach_peer_plan  same, for a peer plan in this process.
+ */
+int mxp_chol_ipc_handle(mxp_plan_t plan, void* handle_out, uint64_t* ws_bytes);
+/* Host-only description of this rank's static task list (no GPU work):
+ * counts[0..4] = GEMM, TRSM, QUANT, PREP, POTRF tasks; counts[5] = tiles this
+ * rank owns.  streaming != 0 describes the host/generated-input list. */
+int mxp_chol_describe(mxp_plan_t plan, int streaming, int64_t* counts);
+int mxp_chol_ipc_attach(mxp_plan_t plan, int peer_rank, const void* handle, uint64_t ws_bytes);
+int mxp_chol_attach_peer_plan(mxp_plan_t plan, int peer_rank, mxp_plan_t peer);
 
 /* Destroy a plan and every device resource it owns. NULL is a no-op. */
 void mxp_chol_plan_destroy(mxp_plan_t plan);

@@ -14,7 +14,8 @@ _lock = threading.Lock()
 
 ATTR = {
     "device": 0, "stream": 1, "hbm_bytes_cap": 2, "splitk_tiles": 3, "lookahead": 4,
-    "debug_sync": 5, "profile": 6, "tc_engine": 7, "gpu_launches": 100, "h2d_bytes": 101, "d2h_bytes": 102,
+    "debug_sync": 5, "profile": 6, "tc_engine": 7, "rank": 8, "nranks": 9, "sm_first": 10,
+    "sm_count": 11, "gpu_launches": 100, "h2d_bytes": 101, "d2h_bytes": 102,
     "pool_slots": 103, "nt": 104,
 }
 
@@ -24,7 +25,8 @@ EXPORTS = [
     "mxp_chol_set_workspace", "mxp_chol_factor_device", "mxp_chol_factor", "mxp_chol_logdet",
     "mxp_precision_map_from_matrix_device", "mxp_generate_plgsy_device", "mxp_generate_kms_device",
     "mxp_generate_matern_device", "mxp_chol_factor_matern", "mxp_precision_map_matern_device",
-    "mxp_chol_get_factor_device", "mxp_chol_tile_device_ptr",
+    "mxp_chol_get_factor_device", "mxp_chol_tile_device_ptr", "mxp_chol_ipc_handle", "mxp_chol_ipc_attach",
+    "mxp_chol_attach_peer_plan", "mxp_chol_describe",
     "mxp_chol_plan_destroy", "mxp_host_alloc", "mxp_host_free", "mxp_strerror", "mxp_last_error",
     "mxp_chol_abi_version", "mxp_chol_kernel_stats", "mxp_chol_sched_diagnostics",
 ]
@@ -84,6 +86,10 @@ def lib():
         L.mxp_precision_map_matern_device.argtypes = [i64, i64, vp, ctypes.c_double, ctypes.c_double,
                                                       ctypes.c_double, ctypes.c_double, ctypes.c_uint32, vp, vp]
         L.mxp_chol_get_factor_device.argtypes = [vp, vp, i64]
+        L.mxp_chol_ipc_handle.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_uint64)]
+        L.mxp_chol_ipc_attach.argtypes = [vp, i32, vp, ctypes.c_uint64]
+        L.mxp_chol_attach_peer_plan.argtypes = [vp, i32, vp]
+        L.mxp_chol_describe.argtypes = [vp, i32, pi64]
         L.mxp_chol_tile_device_ptr.argtypes = [vp, i64, i64, ctypes.POINTER(vp)]
         L.mxp_chol_sched_diagnostics.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64), i64, pi64]
         _lib = L
@@ -223,6 +229,26 @@ class Plan:
         ptr, ld, _ = _colmajor_ptr(L, self.n)
         _check("mxp_chol_get_factor_device", lib().mxp_chol_get_factor_device(self._h, ptr, ld))
         return L
+
+    def describe(self, streaming: bool = False) -> dict:
+        """Host-only task-list census of this rank (no GPU needed)."""
+        c = (ctypes.c_int64 * 6)()
+        _check("mxp_chol_describe", lib().mxp_chol_describe(self._h, int(streaming), c))
+        return dict(zip(["gemm", "trsm", "quant", "prep", "potrf", "owned_tiles"], list(c)))
+
+    def ipc_handle(self) -> tuple[bytes, int]:
+        """(64-byte cudaIpcMemHandle of this plan's workspace, workspace bytes)."""
+        buf = (ctypes.c_uint8 * 64)()
+        nbytes = ctypes.c_uint64()
+        _check("mxp_chol_ipc_handle", lib().mxp_chol_ipc_handle(self._h, buf, ctypes.byref(nbytes)))
+        return bytes(buf), nbytes.value
+
+    def ipc_attach(self, peer_rank: int, handle: bytes, ws_bytes: int):
+        buf = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+        _check("mxp_chol_ipc_attach", lib().mxp_chol_ipc_attach(self._h, peer_rank, buf, ws_bytes))
+
+    def attach_peer(self, peer_rank: int, peer: "Plan"):
+        _check("mxp_chol_attach_peer_plan", lib().mxp_chol_attach_peer_plan(self._h, peer_rank, peer._h))
 
     def kernel_stats(self) -> dict:
         """{class: (launches, ms, flops)} of the last factorization (profile=1)."""

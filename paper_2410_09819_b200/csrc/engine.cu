@@ -98,6 +98,15 @@ struct mxp_plan_s {
     SchedArgs* d_args = nullptr;
     SchedArgs h_args{};
     bool host_mode = false;        // task list built for the host-streaming path (PREP tasks)
+    int epoch = 0;                 // factorization counter: Ready entries equal to it are current
+    int rank = 0, nranks = 1;      // row-cyclic distribution (tile (m, n) on rank m mod nranks)
+    int sm_first = 0, sm_count = 0;  // SM partition of the scheduler (0 = all SMs)
+    char* peer_ws[MAX_RANKS] = {};   // peers' workspaces (same layout), mapped in this process
+    bool peer_ipc[MAX_RANKS] = {};
+    cudaStream_t sPush = 0;
+    int* d_epoch = nullptr;          // device word holding the current epoch (pushed to peers' Ready)
+    int* d_entered = nullptr;        // [MAX_RANKS] epoch each peer has entered (start barrier)
+    bool ready_dirty = false;        // Ready words may exceed the next epoch (probe / drained failure)
     int64_t slots = 0;             // tile slots in the device pool (T in core; fewer out of core)
     std::vector<int32_t> slot_plan, prev_owner;  // out-of-core slot assignment (host mode)
     cudaStream_t sH2D = 0, sD2H = 0, sAux = 0;
@@ -107,7 +116,8 @@ struct mxp_plan_s {
     bool streams_ready = false;
     cudaStream_t sU = 0, sP = 0;
     std::vector<cudaEvent_t> ev_panel, ev_bulk;
-    cudaEvent_t ev_start = nullptr, ev_done = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_done = nullptr, ev_join = nullptr;
+    cudaStream_t sMain = nullptr;      // ordering stream of a multi-rank call (joined to user_stream)
 
     int64_t launches = 0, h2d = 0, d2h = 0;
     int profile = 0;
@@ -143,6 +153,11 @@ mxp_plan_s::~mxp_plan_s() {
     if (sH2D) cudaStreamDestroy(sH2D);
     if (sD2H) cudaStreamDestroy(sD2H);
     if (sAux) cudaStreamDestroy(sAux);
+    if (sPush) cudaStreamDestroy(sPush);
+    if (sMain) cudaStreamDestroy(sMain);
+    if (ev_join) cudaEventDestroy(ev_join);
+    for (int q = 0; q < MAX_RANKS; ++q)
+        if (peer_ipc[q] && peer_ws[q]) cudaIpcCloseMemHandle(peer_ws[q]);
     if (h_stage) cudaFreeHost(h_stage);
     cudaSetDevice(cur);
 }
@@ -183,9 +198,11 @@ void build_task_list(mxp_plan_s* p) {
     const int64_t Nt = p->Nt, nb = p->nb, KC = p->splitk_tiles, NB = blocks_per_tile(nb);
     p->items.clear();
     p->expected.assign(p->T, 0);
+    auto owned = [&](int64_t m) { return m % p->nranks == p->rank; };
     auto gemm_col = [&](int64_t k, int64_t c0, int64_t c1) {
         for (int64_t c = c0; c < c1; ++c)
             for (int64_t m = k; m < Nt; ++m)
+                if (owned(m))
                 for (int64_t b = 0; b < gemm_blocks(p, m, k); ++b)
                     if (block_needed(m, k, b, nb)) {
                         p->items.push_back(make_int4(ITEM_GEMM, (int)m, (int)k, (int)((b << 16) | c)));
@@ -193,7 +210,8 @@ void build_task_list(mxp_plan_s* p) {
                     }
     };
     auto prep_col = [&](int64_t k) {
-        for (int64_t m = k; m < Nt; ++m) p->items.push_back(make_int4(ITEM_PREP, (int)m, (int)k, 0));
+        for (int64_t m = k; m < Nt; ++m)
+            if (owned(m)) p->items.push_back(make_int4(ITEM_PREP, (int)m, (int)k, 0));
     };
     if (p->host_mode) prep_col(0);
     for (int64_t k = 0; k < Nt; ++k) {
@@ -204,16 +222,18 @@ void build_task_list(mxp_plan_s* p) {
         }
         // POTRF(k): normally claimed by the dedicated kernel; listed so the
         // schedule can also complete on its own (fallback, see sched_f64.cu)
-        p->items.push_back(make_int4(ITEM_POTRF, (int)k, (int)k, 0));
+        if (owned(k)) p->items.push_back(make_int4(ITEM_POTRF, (int)k, (int)k, 0));
         if (k + 1 < Nt) {
             int64_t nb1 = nchunks(k + 1, KC) - 1;  // bulk chunks of column k+1
             gemm_col(k + 1, 0, nb1);
         }
         if (p->debug_sync == 2) continue;  // GEMM-throughput probe: no TRSM tasks
         for (int64_t m = k + 1; m < Nt; ++m)
-            for (int64_t r = 0; r < nb / 64; ++r) p->items.push_back(make_int4(ITEM_TRSM, (int)m, (int)k, (int)r));
+            if (owned(m))
+                for (int64_t r = 0; r < nb / 64; ++r)
+                    p->items.push_back(make_int4(ITEM_TRSM, (int)m, (int)k, (int)r));
         for (int64_t m = k + 1; m < Nt; ++m)
-            if (p->map[tile_index(Nt, m, k)] != MXP_FP64)
+            if (owned(m) && p->map[tile_index(Nt, m, k)] != MXP_FP64)
                 for (int64_t r = 0; r < nb / 64; ++r)
                     p->items.push_back(make_int4(ITEM_QUANT, (int)m, (int)k, (int)r));
     }
@@ -298,7 +318,7 @@ bool plan_slots(mxp_plan_s* p, int64_t C) {
 }
 
 struct Layout {
-    size_t slot, prev, flags, flags_bytes, expected, items, wbuf, stats, prec, amax_x, amax_s, args, pool, total;
+    size_t slot, prev, epoch, flags, flags_bytes, expected, items, wbuf, stats, prec, amax_x, amax_s, args, pool, total;
 };
 
 Layout layout(const mxp_plan_s* p) {
@@ -308,6 +328,8 @@ Layout layout(const mxp_plan_s* p) {
     off += align_up(sizeof(int32_t) * p->T, 256);
     L.prev = off;
     off += align_up(sizeof(int32_t) * p->T, 256);
+    L.epoch = off;
+    off += 256;
     L.flags = off;
     // counter, err, ready, gemm_done, trsm_done, quant_done, loaded, prep_done, blk_chunk, potrf_claim,
     // col_ready, d2h_done; then amax_x
@@ -349,12 +371,16 @@ void bind_workspace(mxp_plan_s* p) {
         p->ws_bytes = L.total;
         p->ws_owned = true;
         p->list_uploaded = false;
+        p->epoch = 0;
+        CK(cudaMemset(p->ws, 0, L.pool));  // Ready table and all metadata start at zero
     }
     p->d_info = (int64_t*)p->ws;
     p->d_logdet = (double*)(p->ws + 256);
     p->d_logdet_parts = p->d_logdet + 1;
     p->d_slot = (int32_t*)(p->ws + L.slot);
     p->d_prev = (int32_t*)(p->ws + L.prev);
+    p->d_epoch = (int*)(p->ws + L.epoch);
+    p->d_entered = (int*)(p->ws + L.epoch + 64);
     p->d_flags = (int*)(p->ws + L.flags);
     p->flags_bytes = L.flags_bytes;
     p->d_expected = (int*)(p->ws + L.expected);
@@ -377,6 +403,7 @@ void ensure_streams(mxp_plan_s* p) {
     CK(cudaStreamCreateWithFlags(&p->sH2D, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&p->sD2H, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&p->sAux, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&p->sPush, cudaStreamNonBlocking));
     p->ev_panel.resize(p->Nt);
     p->ev_bulk.resize(p->Nt);
     for (int64_t k = 0; k < p->Nt; ++k) {
@@ -385,7 +412,21 @@ void ensure_streams(mxp_plan_s* p) {
     }
     CK(cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+    CK(cudaStreamCreateWithFlags(&p->sMain, cudaStreamNonBlocking));
     p->streams_ready = true;
+}
+
+// The stream a call orders its work on.  Single rank: the user's stream.
+// Several ranks: a private stream joined after the user's pending work --
+// co-located ranks may share one user stream (e.g. the legacy default
+// stream), and a rank's start-barrier wait must not block its peers' work.
+// Every entry point synchronizes this stream before returning.
+cudaStream_t entry_stream(mxp_plan_s* p) {
+    if (p->nranks <= 1) return p->user_stream;
+    CK(cudaEventRecord(p->ev_join, p->user_stream));
+    CK(cudaStreamWaitEvent(p->sMain, p->ev_join, 0));
+    return p->sMain;
 }
 
 void dbg(mxp_plan_s* p, cudaStream_t s, const char* what) {
@@ -448,6 +489,106 @@ void prof_collect(mxp_plan_s* p) {
 
 // In-core FP64 factorization of the tiles already packed in the pool: one
 // persistent static-schedule kernel on U + the POTRF kernels on P.
+// Multi-GPU exchange: every tile this rank finishes is
+// pushed, in schedule order, into each peer's pool by the copy engines (D2D
+// over NVLink P2P -- no SM is taken from the persistent schedules), followed
+// by its Ready word (= epoch), so peers use it exactly like a local tile.
+// Diagonal tiles carry their W blocks (TRSM inverses) and log-det share;
+// MxP tiles their amax.  Tiles of row k are needed by every rank at column k.
+template <class T>
+T* peer_addr(const mxp_plan_s* p, int q, const T* local) {
+    return (T*)(p->peer_ws[q] + ((const char*)local - p->ws));
+}
+void push_tiles(mxp_plan_s* p, const SchedArgs& a) {
+    const int64_t Nt = p->Nt, nb = p->nb, S = nb / 128;
+    if (!stream_memops()) {
+        g_last_error = "cuStreamWaitValue32 unavailable";
+        throw CudaError{cudaErrorNotSupported};
+    }
+    CK(cudaStreamWaitEvent(p->sPush, p->ev_start, 0));
+    for (int64_t n = 0; n < Nt; ++n)
+        for (int64_t k = n; k < Nt; ++k) {
+            if (k % p->nranks != p->rank) continue;
+            const int64_t t = tile_index(Nt, k, n);
+            if (g_wait32((CUstream)p->sPush, (CUdeviceptr)(a.ready + t), (cuuint32_t)p->epoch,
+                         CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+                throw CudaError{cudaErrorUnknown};
+            const double* tile = p->pool + (size_t)p->slot_plan[t] * nb * nb;
+            for (int q = 0; q < p->nranks; ++q) {
+                if (q == p->rank) continue;
+                CK(cudaMemcpyAsync(peer_addr(p, q, tile), tile, sizeof(double) * nb * nb, cudaMemcpyDeviceToDevice,
+                                   p->sPush));
+                if (k == n) {
+                    const double* W = p->d_wbuf + (size_t)k * S * 128 * 128;
+                    CK(cudaMemcpyAsync(peer_addr(p, q, W), W, sizeof(double) * S * 128 * 128,
+                                       cudaMemcpyDeviceToDevice, p->sPush));
+                    CK(cudaMemcpyAsync(peer_addr(p, q, p->d_logdet_parts + k), p->d_logdet_parts + k, sizeof(double),
+                                       cudaMemcpyDeviceToDevice, p->sPush));
+                }
+                if (p->mxp)
+                    CK(cudaMemcpyAsync(peer_addr(p, q, p->d_amax_s + t), p->d_amax_s + t, sizeof(double),
+                                       cudaMemcpyDeviceToDevice, p->sPush));
+                CK(cudaMemcpyAsync(peer_addr(p, q, a.ready + t), p->d_epoch, sizeof(int), cudaMemcpyDeviceToDevice,
+                                   p->sPush));
+            }
+        }
+}
+
+// Ready words hold the epoch (factorization counter) of the run that made the
+// tile final, so they are never cleared between runs: stale values compare
+// below the current epoch (cuStreamWaitValue32 GEQ is a cyclic comparison).
+// The rest of the flag area is reset per run.  With several ranks this is
+// followed by a start barrier: every rank writes its epoch into each peer's
+// entered[rank] word after its own resets (stream order on s0) and waits for
+// all peers' words before any kernel of the run -- no peer pushes into this
+// pool, or writes its Ready/info words, before they have been reset, and a
+// peer enters run e+1 only after its run-e pushes into this pool completed.
+void begin_epoch(mxp_plan_s* p, cudaStream_t s0) {
+    // (ranks run the same sequence of factorizations, so their epochs agree)
+    if (++p->epoch >= (1 << 24)) p->epoch = 1, p->ready_dirty = true;
+    if (p->ready_dirty) {  // clear the table
+        CK(cudaMemsetAsync(p->d_flags + 2, 0, sizeof(int) * p->T, s0));
+        p->ready_dirty = false;
+    }
+    CK(cudaMemsetAsync(p->d_flags, 0, 2 * sizeof(int), s0));  // ticket, err
+    const size_t rest = 2 * sizeof(int) + sizeof(int) * p->T;
+    CK(cudaMemsetAsync((char*)p->d_flags + rest, 0, p->flags_bytes - rest, s0));
+    if (p->nranks <= 1) {
+        CK(cudaMemcpyAsync(p->d_epoch, &p->epoch, sizeof(int), cudaMemcpyHostToDevice, s0));
+        return;
+    }
+    if (!stream_memops()) {
+        g_last_error = "multi-rank factorization needs cuStreamWaitValue32";
+        throw CudaError{cudaErrorNotSupported};
+    }
+    for (int q = 0; q < p->nranks; ++q)
+        if (!p->peer_ws[q] && q != p->rank) {
+            g_last_error = "peer workspace of rank " + std::to_string(q) + " not attached";
+            throw CudaError{cudaErrorInvalidValue};
+        }
+    const cuuint32_t e = (cuuint32_t)p->epoch;
+    if (g_write32((CUstream)s0, (CUdeviceptr)p->d_epoch, e, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+        throw CudaError{cudaErrorUnknown};
+    for (int q = 0; q < p->nranks; ++q)
+        if (q != p->rank &&
+            g_write32((CUstream)s0, (CUdeviceptr)peer_addr(p, q, p->d_entered + p->rank), e,
+                      CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+            throw CudaError{cudaErrorUnknown};
+    for (int q = 0; q < p->nranks; ++q)
+        if (q != p->rank &&
+            g_wait32((CUstream)s0, (CUdeviceptr)(p->d_entered + q), e, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+            throw CudaError{cudaErrorUnknown};
+}
+
+// tile index of the last tile rank q pushes (push order of push_tiles), -1 if none
+int64_t last_pushed_tile(const mxp_plan_s* p, int q) {
+    int64_t last = -1;
+    for (int64_t n = 0; n < p->Nt; ++n)
+        for (int64_t k = n; k < p->Nt; ++k)
+            if (k % p->nranks == q) last = tile_index(p->Nt, k, n);
+    return last;
+}
+
 struct GenSource {  // fused on-device generation of the input tiles (N2)
     const double* xy = nullptr;
     double sigma2 = 1.0, range = 1.0, nugget = 0.0;
@@ -468,16 +609,19 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
         CK(cudaStreamSynchronize(s0));
         p->list_uploaded = true;
     }
-    CK(cudaMemsetAsync(p->d_flags, 0, p->flags_bytes, s0));
+    begin_epoch(p, s0);
     if (p->mxp && !p->host_mode) {
         // O3: stored input A^ = deq(q_p(A)) per tile; amax_x is then reset for the TRSM outputs
         Prof pr(p, s0, MXP_KCLASS_OTHER, 0.0, 2);
-        launch_input_quantize(p->pool, p->d_slot, p->d_prec, Nt, p->nb, p->d_amax_x, p->d_amax_s, s0);
+        launch_input_quantize(p->pool, p->d_slot, p->d_prec, Nt, p->nb, p->d_amax_x, p->d_amax_s, s0, p->rank,
+                              p->nranks);
         p->launches += 2;
         CK(cudaMemsetAsync(p->d_amax_x, 0, sizeof(unsigned long long) * T, s0));
     }
-    if (p->debug_sync == 2)  // GEMM-throughput probe: every tile "ready", no POTRF (values are garbage)
+    if (p->debug_sync == 2) {  // GEMM-throughput probe: every tile "ready", no POTRF (values are garbage)
         CK(cudaMemsetAsync(p->d_flags + 2, 1, sizeof(int) * T, s0));
+        p->ready_dirty = true;
+    }
     CK(cudaEventRecord(p->ev_start, s0));
     CK(cudaStreamWaitEvent(p->sU, p->ev_start, 0));
     CK(cudaStreamWaitEvent(p->sP, p->ev_start, 0));
@@ -522,6 +666,11 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     a.nitems = (int)p->items.size();
     a.wbuf = p->d_wbuf;
     a.reserved_sms = p->reserved_sms;
+    a.epoch = p->epoch;
+    a.rank = p->rank;
+    a.nranks = p->nranks;
+    for (int q = 0; q < MAX_RANKS; ++q)
+        a.peer_dinfo[q] = (q != p->rank && q < p->nranks && p->peer_ws[q]) ? (int64_t*)p->peer_ws[q] : nullptr;
     a.stats = nullptr;
     const size_t nstat = 16 + 3 * (size_t)Nt;
     if (p->profile) {
@@ -534,6 +683,8 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
 
     int dev = p->device, nsm = 0;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    a.sm_lo = p->sm_count > 0 ? p->sm_first : 0;
+    a.sm_hi = p->sm_count > 0 ? std::min(nsm, p->sm_first + p->sm_count) : nsm;
     int occ = sched_ctas_per_sm();
     const double nb3 = (double)p->nb * p->nb * p->nb;
     const double total = (double)Nt * Nt * Nt * nb3 / 3.0;
@@ -548,8 +699,10 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     {
         Prof pr(p, p->sP, MXP_KCLASS_POTRF, (double)Nt * nb3 / 3.0, Nt);
         if (p->debug_sync != 2 && p->debug_sync != 3) {  // 3: every POTRF by the scheduler fallback
-            for (int64_t k = 0; k < Nt; ++k) launch_potrf_tile(a, k, p->sP);
-            p->launches += Nt;
+            for (int64_t k = p->rank; k < Nt; k += p->nranks) {  // diagonal tiles this rank owns
+                launch_potrf_tile(a, k, p->sP);
+                ++p->launches;
+            }
         }
         CK(cudaGetLastError());
     }
@@ -586,7 +739,8 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
             for (int64_t m = k; m < Nt; ++m) {
                 const int64_t t = tile_index(Nt, m, k);
                 const int64_t rr = std::min(nb, n - m * nb), cr = std::min(nb, n - k * nb);
-                if (g_wait32((CUstream)p->sD2H, (CUdeviceptr)(a.ready + t), 1, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+                if (g_wait32((CUstream)p->sD2H, (CUdeviceptr)(a.ready + t), (cuuint32_t)p->epoch,
+                             CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
                     throw CudaError{cudaErrorUnknown};
                 const double* src = p->pool + (size_t)p->slot_plan[t] * nb * nb;
                 if (m != k) {
@@ -603,8 +757,42 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
                     throw CudaError{cudaErrorUnknown};
             }
     }
+    if (p->nranks > 1) push_tiles(p, a);
     CK(cudaEventRecord(p->ev_done, p->sP));
     CK(cudaStreamWaitEvent(p->sU, p->ev_done, 0));
+}
+
+// Multi-rank epilogue: once this rank's schedule has ended, a failure (info)
+// leaves Ready words unset that the push stream waits on -- release them so
+// the stream drains -- then order the pushes before s0.
+void finish_pushes(mxp_plan_s* p, cudaStream_t s0) {
+    if (p->nranks <= 1) {
+        return;
+    }
+    CK(cudaStreamSynchronize(p->sU));
+    int64_t hinfo = 0;
+    int herr = 0;
+    CK(cudaMemcpy(&hinfo, p->d_info, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&herr, p->d_flags + 1, sizeof(int), cudaMemcpyDeviceToHost));
+    const bool failed = hinfo != 0 || herr || p->debug_sync == 2;
+    if (failed) {  // release the push stream's waits (the pushed tiles are not a result)
+        CK(cudaMemsetAsync(p->d_flags + 2, 0x7f, sizeof(int) * p->T, p->sAux));
+        CK(cudaStreamSynchronize(p->sAux));
+    }
+    CK(cudaEventRecord(p->ev_start, p->sPush));
+    CK(cudaStreamWaitEvent(s0, p->ev_start, 0));
+    if (!failed) {
+        // every peer's pushes into this pool have landed: each peer pushes in
+        // one stream, so its last Ready write orders all its earlier copies
+        for (int q = 0; q < p->nranks; ++q) {
+            const int64_t t = q == p->rank ? -1 : last_pushed_tile(p, q);
+            if (t >= 0 && g_wait32((CUstream)s0, (CUdeviceptr)(p->d_flags + 2 + t), (cuuint32_t)p->epoch,
+                                   CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+                throw CudaError{cudaErrorUnknown};
+        }
+    } else {
+        p->ready_dirty = true;  // drained words are ahead of every later epoch
+    }
 }
 
 int status_from_exception(const CudaError& e) {
@@ -701,6 +889,24 @@ int mxp_chol_plan_set(mxp_plan_t p, mxp_attr_t key, int64_t v) {
         p->debug_sync = (int)v;
         return MXP_OK;
     case MXP_ATTR_PROFILE: p->profile = v ? 1 : 0; return MXP_OK;
+    case MXP_ATTR_RANK:
+        if (v < 0 || v >= MAX_RANKS) return -3;
+        p->rank = (int)v;
+        p->list_uploaded = false;
+        return MXP_OK;
+    case MXP_ATTR_NRANKS:
+        if (v < 1 || v > MAX_RANKS) return -3;
+        p->nranks = (int)v;
+        p->list_uploaded = false;
+        return MXP_OK;
+    case MXP_ATTR_SM_FIRST:
+        if (v < 0) return -3;
+        p->sm_first = (int)v;
+        return MXP_OK;
+    case MXP_ATTR_SM_COUNT:
+        if (v < 0) return -3;
+        p->sm_count = (int)v;
+        return MXP_OK;
     case MXP_ATTR_TC_ENGINE:
         if (p->ws && !p->ws_owned) return MXP_ESTATE;  // changes the task list size
         if (p->ws_owned) {
@@ -745,6 +951,10 @@ int mxp_chol_plan_get(mxp_plan_t p, mxp_attr_t key, int64_t* v) {
     case MXP_ATTR_DEBUG_SYNC: *v = p->debug_sync; return MXP_OK;
     case MXP_ATTR_PROFILE: *v = p->profile; return MXP_OK;
     case MXP_ATTR_TC_ENGINE: *v = p->tc_engine; return MXP_OK;
+    case MXP_ATTR_RANK: *v = p->rank; return MXP_OK;
+    case MXP_ATTR_NRANKS: *v = p->nranks; return MXP_OK;
+    case MXP_ATTR_SM_FIRST: *v = p->sm_first; return MXP_OK;
+    case MXP_ATTR_SM_COUNT: *v = p->sm_count; return MXP_OK;
     case MXP_ATTR_GPU_LAUNCHES: *v = p->launches; return MXP_OK;
     case MXP_ATTR_H2D_BYTES: *v = p->h2d; return MXP_OK;
     case MXP_ATTR_D2H_BYTES: *v = p->d2h; return MXP_OK;
@@ -773,6 +983,16 @@ int mxp_chol_set_workspace(mxp_plan_t p, void* dev, size_t bytes) {
     p->ws_bytes = bytes;
     p->ws_owned = false;
     p->list_uploaded = false;
+    p->epoch = 0;
+    {
+        Layout L = layout(p);
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(p->device);
+        cudaError_t e = cudaMemset(p->ws, 0, L.pool);
+        cudaSetDevice(cur);
+        if (e != cudaSuccess) return MXP_ECUDA;
+    }
     return MXP_OK;
 }
 
@@ -794,7 +1014,7 @@ int mxp_chol_factor_device(mxp_plan_t p, double* A, int64_t lda, int64_t* info) 
         }
         ensure_streams(p);
         bind_workspace(p);
-        cudaStream_t s0 = p->user_stream;
+        cudaStream_t s0 = entry_stream(p);
         // slot table (identity in-core) + info reset, ordered on the user stream
         p->slot_plan.resize(p->T);
         p->prev_owner.assign(p->T, -1);
@@ -805,13 +1025,14 @@ int mxp_chol_factor_device(mxp_plan_t p, double* A, int64_t lda, int64_t* info) 
         prof_reset(p);
         {
             Prof pr(p, s0, MXP_KCLASS_OTHER, 0.0);
-            launch_pack_f64(A, lda, p->n, p->pool, p->d_slot, p->Nt, p->nb, 0, p->Nt, s0);
+            launch_pack_f64(A, lda, p->n, p->pool, p->d_slot, p->Nt, p->nb, 0, p->Nt, s0, p->rank, p->nranks);
             ++p->launches;
             dbg(p, s0, "pack");
         }
         factor_incore_f64(p, s0, false);
         CK(cudaEventRecord(p->ev_done, p->sU));
         CK(cudaStreamWaitEvent(s0, p->ev_done, 0));
+        finish_pushes(p, s0);
         {
             Prof pr(p, s0, MXP_KCLASS_OTHER, 0.0, 3);
             launch_unpack_f64(A, lda, p->n, p->pool, p->d_slot, p->Nt, p->nb, 0, p->Nt, s0);
@@ -855,6 +1076,10 @@ int mxp_chol_factor(mxp_plan_t p, double* A_host, int64_t lda, int64_t* info) {
     // Host-resident path (Alg. 2): tiles stream host->device on a copy
     // stream in schedule order while the static schedule runs; each finished
     // tile streams back as soon as it is final (lower triangle only).
+    if (p->nranks > 1) {
+        g_last_error = "host-resident input with several ranks: not in this build (use the device or generated path)";
+        return MXP_ENOTSUP;
+    }
     p->have_result = false;
     p->launches = p->h2d = p->d2h = 0;
     int cur = 0;
@@ -889,7 +1114,7 @@ int mxp_chol_factor(mxp_plan_t p, double* A_host, int64_t lda, int64_t* info) {
             CK(cudaMallocHost((void**)&p->h_stage, stage_bytes));
             p->h_stage_bytes = stage_bytes;
         }
-        cudaStream_t s0 = p->user_stream;
+        cudaStream_t s0 = entry_stream(p);
         const int64_t C = pool_slots(p);
         if (!plan_slots(p, C)) {
             g_last_error = "HBM cap below the out-of-core working set (live tiles of two columns)";
@@ -912,7 +1137,7 @@ int mxp_chol_factor(mxp_plan_t p, double* A_host, int64_t lda, int64_t* info) {
         CK(cudaMemcpy(&herr, p->d_flags + 1, sizeof(int), cudaMemcpyDeviceToHost));
         if (hinfo != 0 || herr) {
             // release the copy streams: Ready flags (D2H gates) and column counters (slot reuse gates)
-            CK(cudaMemsetAsync(p->d_flags + 2, 0x01, sizeof(int) * p->T, p->sAux));
+            CK(cudaMemsetAsync(p->d_flags + 2, 0x7f, sizeof(int) * p->T, p->sAux));
             int* col_ready = p->d_flags + 2 + 6 * p->T + p->T * blocks_per_tile(p->nb) + p->Nt;
             CK(cudaMemsetAsync(col_ready, 0x7f, sizeof(int) * p->Nt, p->sAux));
             CK(cudaStreamSynchronize(p->sAux));
@@ -1083,7 +1308,7 @@ int mxp_chol_factor_matern(mxp_plan_t p, const double* xy_dev, double sigma2, do
         CK(cudaSetDevice(p->device));
         ensure_streams(p);
         bind_workspace(p);
-        cudaStream_t s0 = p->user_stream;
+        cudaStream_t s0 = entry_stream(p);
         const int64_t C = pool_slots(p);
         if (!plan_slots(p, C)) {
             g_last_error = "HBM cap below the out-of-core working set (live tiles of two columns)";
@@ -1103,6 +1328,7 @@ int mxp_chol_factor_matern(mxp_plan_t p, const double* xy_dev, double sigma2, do
         factor_incore_f64(p, s0, true, nullptr, 0, &g);
         CK(cudaEventRecord(p->ev_done, p->sU));
         CK(cudaStreamWaitEvent(s0, p->ev_done, 0));
+        finish_pushes(p, s0);
         {
             Prof pr(p, s0, MXP_KCLASS_OTHER, 0.0, 1);
             launch_logdet_final(p->d_logdet_parts, p->Nt, p->d_logdet, s0);
@@ -1128,6 +1354,106 @@ int mxp_chol_factor_matern(mxp_plan_t p, const double* xy_dev, double sigma2, do
         *info = hinfo;
         p->have_result = (hinfo == 0);
         p->logdet = ld;
+    } catch (const CudaError& e) {
+        cudaSetDevice(cur);
+        return status_from_exception(e);
+    }
+    cudaSetDevice(cur);
+    return MXP_OK;
+}
+
+int mxp_chol_describe(mxp_plan_t p, int streaming, int64_t* counts) {
+    if (!p) return -1;
+    if (!counts) return -3;
+    const bool saved = p->host_mode;
+    p->host_mode = streaming != 0;
+    build_task_list(p);
+    p->host_mode = saved;
+    p->list_uploaded = false;
+    for (int i = 0; i < 6; ++i) counts[i] = 0;
+    for (const int4& it : p->items) counts[it.x]++;
+    for (int64_t k = 0; k < p->Nt; ++k)
+        for (int64_t m = k; m < p->Nt; ++m)
+            if (m % p->nranks == p->rank) counts[5]++;
+    return MXP_OK;
+}
+
+int mxp_chol_ipc_handle(mxp_plan_t p, void* handle_out, uint64_t* ws_bytes) {
+    if (!p) return -1;
+    if (!handle_out) return -2;
+    if (!ws_bytes) return -3;
+    if (p->ws && !p->ws_owned) return MXP_ESTATE;  // IPC needs the plan's own cudaMalloc'd workspace
+    int cur = 0;
+    cudaGetDevice(&cur);
+    try {
+        CK(cudaSetDevice(p->device));
+        ensure_streams(p);
+        bind_workspace(p);
+        cudaIpcMemHandle_t h;
+        CK(cudaIpcGetMemHandle(&h, p->ws));
+        std::memcpy(handle_out, &h, sizeof(h));
+        *ws_bytes = p->ws_bytes;
+    } catch (const CudaError& e) {
+        cudaSetDevice(cur);
+        return status_from_exception(e);
+    }
+    cudaSetDevice(cur);
+    return MXP_OK;
+}
+
+int mxp_chol_ipc_attach(mxp_plan_t p, int peer_rank, const void* handle, uint64_t ws_bytes) {
+    if (!p) return -1;
+    if (peer_rank < 0 || peer_rank >= p->nranks || peer_rank == p->rank) return -2;
+    if (!handle) return -3;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    try {
+        CK(cudaSetDevice(p->device));
+        ensure_streams(p);
+        bind_workspace(p);
+        if (ws_bytes != p->ws_bytes) {
+            cudaSetDevice(cur);
+            return -4;  // peers must use identical plans (same layout)
+        }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof(h));
+        void* ptr = nullptr;
+        CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        if (p->peer_ipc[peer_rank] && p->peer_ws[peer_rank]) cudaIpcCloseMemHandle(p->peer_ws[peer_rank]);
+        p->peer_ws[peer_rank] = (char*)ptr;
+        p->peer_ipc[peer_rank] = true;
+    } catch (const CudaError& e) {
+        cudaSetDevice(cur);
+        return status_from_exception(e);
+    }
+    cudaSetDevice(cur);
+    return MXP_OK;
+}
+
+int mxp_chol_attach_peer_plan(mxp_plan_t p, int peer_rank, mxp_plan_t peer) {
+    if (!p) return -1;
+    if (peer_rank < 0 || peer_rank >= p->nranks || peer_rank == p->rank) return -2;
+    if (!peer || peer == p) return -3;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    try {
+        CK(cudaSetDevice(peer->device));
+        ensure_streams(peer);
+        bind_workspace(peer);
+        CK(cudaSetDevice(p->device));
+        ensure_streams(p);
+        bind_workspace(p);
+        if (peer->ws_bytes != p->ws_bytes) {
+            cudaSetDevice(cur);
+            return -3;
+        }
+        if (peer->device != p->device) {
+            cudaError_t e = cudaDeviceEnablePeerAccess(peer->device, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+            cudaGetLastError();
+        }
+        p->peer_ws[peer_rank] = peer->ws;
+        p->peer_ipc[peer_rank] = false;
     } catch (const CudaError& e) {
         cudaSetDevice(cur);
         return status_from_exception(e);

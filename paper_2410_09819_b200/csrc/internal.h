@@ -17,6 +17,7 @@ __host__ __device__ inline int64_t tile_index(int64_t Nt, int64_t i, int64_t j) 
 // Task list entries (int4): {type, m, k, w}; GEMM: w = (block << 16) | chunk,
 // TRSM: w = 64-row block index.
 enum { ITEM_GEMM = 0, ITEM_TRSM = 1, ITEM_QUANT = 2, ITEM_PREP = 3, ITEM_POTRF = 4 };
+constexpr int MAX_RANKS = 8;
 
 struct SchedArgs {
     double* pool;
@@ -29,7 +30,9 @@ struct SchedArgs {
     const int4* items;
     int nitems;
     int* counter;              // next task ticket
-    int* ready;                // [T] Ready table: tile final
+    int* ready;                // [T] Ready table: tile final and present in this rank's pool
+                               //     (== epoch of the factorization; peers write it after pushing a tile)
+    int epoch;                 // factorization counter (Ready entries are compared against it)
     int* gemm_done;            // [T] completed GEMM tasks of the tile
     const int* gemm_expected;  // [T]
     int* trsm_done;            // [T] completed TRSM row tasks of the tile
@@ -52,6 +55,10 @@ struct SchedArgs {
     int* col_ready;            // [Nt] tiles of column k that are final (== Nt-k: column complete;
                                //      out-of-core slot reuse waits on it)
     double* logdet_parts;      // [Nt] sum of log L_ii over diagonal tile k (written by its POTRF)
+    // multi-GPU (row-cyclic: tile (m, n) belongs to rank m mod nranks)
+    int rank, nranks;
+    int sm_lo, sm_hi;          // SM partition of this rank's scheduler (co-located ranks)
+    int64_t* peer_dinfo[MAX_RANKS];  // peers' info words (a failed pivot stops every rank)
     int reserved_sms;          // SMs (smid < this) left to the POTRF kernels
     unsigned long long* stats; // optional diagnostics (MXP_ATTR_PROFILE): see STAT_*
 };
@@ -64,14 +71,16 @@ enum {
 int sched_ctas_per_sm();
 // input stage of MxP (a3, O3): per-tile amax, then A^ = deq(q_p(A)) in place
 void launch_input_quantize(double* pool, const int32_t* slot, const uint8_t* prec, int64_t Nt, int64_t nb,
-                           unsigned long long* amax_x, double* amax_s, cudaStream_t s);
+                           unsigned long long* amax_x, double* amax_s, cudaStream_t s, int rank = 0,
+                           int nranks = 1);
 void launch_sched(const SchedArgs& a, const SchedArgs* a_dev, bool mxp, int grid, cudaStream_t s);  // a_dev: device copy of a
 void launch_potrf_tile(const SchedArgs& a, int64_t k, cudaStream_t s);
 
 // ---- layout / utility kernels --------------------------------------------
 // lda matrix <-> pool tiles (padding: zeros, 1 on the padded diagonal)
 void launch_pack_f64(const double* A, int64_t lda, int64_t n, double* pool, const int32_t* slot,
-                     int64_t Nt, int64_t nb, int64_t col0, int64_t col1, cudaStream_t s);
+                     int64_t Nt, int64_t nb, int64_t col0, int64_t col1, cudaStream_t s, int rank = 0,
+                     int nranks = 1);
 void launch_unpack_f64(double* A, int64_t lda, int64_t n, const double* pool, const int32_t* slot,
                        int64_t Nt, int64_t nb, int64_t col0, int64_t col1, cudaStream_t s);
 // logdet = 2 sum_k parts[k] in ascending k (parts from the POTRFs; deterministic)

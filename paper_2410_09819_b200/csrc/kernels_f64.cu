@@ -12,10 +12,10 @@ namespace mxp {
 // grid: (column-of-tile groups, tile columns j, tile rows i) -- one CTA per
 // (tile, 8 columns); rows are contiguous in both layouts -> coalesced.
 __global__ void k_pack(const double* __restrict__ A, int64_t lda, int64_t n, double* pool,
-                       const int32_t* slot, int64_t Nt, int64_t nb, int64_t col0) {
+                       const int32_t* slot, int64_t Nt, int64_t nb, int64_t col0, int rank, int nranks) {
     const int64_t j = col0 + blockIdx.y;
     const int64_t i = j + blockIdx.z;
-    if (i >= Nt) return;
+    if (i >= Nt || i % nranks != rank) return;  // only this rank's rows (peers push the rest)
     double* T = pool + (int64_t)slot[tile_index(Nt, i, j)] * nb * nb;
     for (int64_t c = blockIdx.x * 8; c < (int64_t)blockIdx.x * 8 + 8; ++c) {
         int64_t gj = j * nb + c;
@@ -44,9 +44,9 @@ __global__ void k_unpack(double* __restrict__ A, int64_t lda, int64_t n, const d
     }
 }
 void launch_pack_f64(const double* A, int64_t lda, int64_t n, double* pool, const int32_t* slot,
-                     int64_t Nt, int64_t nb, int64_t col0, int64_t col1, cudaStream_t s) {
+                     int64_t Nt, int64_t nb, int64_t col0, int64_t col1, cudaStream_t s, int rank, int nranks) {
     dim3 grid((unsigned)(nb / 8), (unsigned)(col1 - col0), (unsigned)(Nt - col0));
-    k_pack<<<grid, 256, 0, s>>>(A, lda, n, pool, slot, Nt, nb, col0);
+    k_pack<<<grid, 256, 0, s>>>(A, lda, n, pool, slot, Nt, nb, col0, rank, nranks);
 }
 void launch_unpack_f64(double* A, int64_t lda, int64_t n, const double* pool, const int32_t* slot,
                        int64_t Nt, int64_t nb, int64_t col0, int64_t col1, cudaStream_t s) {

@@ -130,8 +130,8 @@ __device__ __forceinline__ bool task_gemm(const SchedArgs& a, int64_t m, int64_t
         if (a.stats) tw0 = globaltimer();
         bool ok = wait_input(a, t, k);
         for (int64_t n = n0; n < n1 && ok; ++n) {
-            ok = wait_flag(a.ready + tile_index(Nt, m, n), 1, a, k) &&
-                 wait_flag(a.ready + tile_index(Nt, k, n), 1, a, k);
+            ok = wait_flag(a.ready + tile_index(Nt, m, n), a.epoch, a, k) &&
+                 wait_flag(a.ready + tile_index(Nt, k, n), a.epoch, a, k);
         }
         if (ok) ok = wait_flag(chunk_flag, (int)c, a, k);
         *s_flag = ok;
@@ -218,7 +218,7 @@ __device__ __forceinline__ bool task_trsm(const SchedArgs& a, int64_t m, int64_t
     uint64_t tw0 = 0;
     if (threadIdx.x == 0) {
         if (a.stats) tw0 = globaltimer();
-        bool ok = wait_input(a, t, k) && wait_flag(a.ready + tile_index(Nt, k, k), 1, a, k) &&
+        bool ok = wait_input(a, t, k) && wait_flag(a.ready + tile_index(Nt, k, k), a.epoch, a, k) &&
                   wait_flag(a.gemm_done + t, a.gemm_expected[t], a, k);
         *s_flag = ok;
         if (a.stats) {
@@ -291,7 +291,7 @@ __device__ __forceinline__ bool task_trsm(const SchedArgs& a, int64_t m, int64_t
             // FP64 tile: stored values are the TRSM result; amax_s drives later down-casts
             a.amax_s[t] = amax_of(a.amax_x + t);
             __threadfence();
-            st_release(a.ready + t, 1);
+            st_release(a.ready + t, a.epoch);
             atom_add_release(a.col_ready + k, 1);
         }
         if (a.stats) {
@@ -326,8 +326,8 @@ __device__ __noinline__ bool task_gemm_tc(const SchedArgs& a, int64_t m, int64_t
         if (a.stats) tw0 = globaltimer();
         bool ok = wait_input(a, t, k);
         for (int64_t n = n0; n < n1 && ok; ++n)
-            ok = wait_flag(a.ready + tile_index(Nt, m, n), 1, a, k) &&
-                 wait_flag(a.ready + tile_index(Nt, k, n), 1, a, k);
+            ok = wait_flag(a.ready + tile_index(Nt, m, n), a.epoch, a, k) &&
+                 wait_flag(a.ready + tile_index(Nt, k, n), a.epoch, a, k);
         if (ok) ok = wait_flag(chunk_flag, (int)c, a, k);
         *s_flag = ok;
         if (a.stats) {
@@ -399,7 +399,7 @@ __device__ __noinline__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k
         __threadfence();
         int old = atom_add_release(a.quant_done + t, 1);
         if (old + 1 == (int)(nb / 64)) {
-            st_release(a.ready + t, 1);
+            st_release(a.ready + t, a.epoch);
             atom_add_release(a.col_ready + k, 1);
         }
     }
@@ -523,7 +523,11 @@ __device__ bool potrf_tile_body(const SchedArgs& a, int64_t k, double* smem, int
                 double d = P[pidx_c(j, j)];
                 if (!(d > 0.0)) {
                     *s_flag = 1;
-                    *(volatile int64_t*)a.dinfo = k * nb + (int64_t)J * 128 + j + 1;
+                    const int64_t info = k * nb + (int64_t)J * 128 + j + 1;
+                    *(volatile int64_t*)a.dinfo = info;
+                    for (int q = 0; q < MAX_RANKS; ++q)  // other ranks stop at this column too
+                        if (a.peer_dinfo[q]) *(volatile int64_t*)a.peer_dinfo[q] = info;
+                    __threadfence_system();
                 } else {
                     P[pidx_c(j, j)] = sqrt(d);
                 }
@@ -616,7 +620,7 @@ __device__ bool potrf_tile_body(const SchedArgs& a, int64_t k, double* smem, int
 // take it first (the scheduler-CTA fallback).  Sets *s_flag = 1 iff claimed.
 __device__ void claim_potrf(const SchedArgs& a, int64_t k, uint64_t grace_ns, int* s_flag) {
     const int64_t tk = tile_index(a.Nt, k, k);
-    bool ok = !skip_column(a, k);
+    bool ok = !skip_column(a, k) && k % a.nranks == a.rank;  // only the owner of row k factors (k,k)
     if (ok) ok = wait_input(a, tk, k);
     if (ok && k > 0) ok = wait_flag(a.gemm_done + tk, a.gemm_expected[tk], a, k);
     if (ok && grace_ns) {
@@ -646,7 +650,7 @@ __device__ void publish_potrf(const SchedArgs& a, int64_t k, double* red) {
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
-        st_release(a.ready + tile_index(a.Nt, k, k), 1);
+        st_release(a.ready + tile_index(a.Nt, k, k), a.epoch);
         atom_add_release(a.col_ready + k, 1);
         if (a.stats) a.stats[STAT_POTRF + 3 * k + 2] = globaltimer();
     }
@@ -672,7 +676,10 @@ __device__ __noinline__ void task_potrf_fallback(const SchedArgs& a, int64_t k, 
 template <bool MXP>
 __global__ void __launch_bounds__(CC::NT, 3) k_sched(const SchedArgs a_param, const SchedArgs* __restrict__ ap) {
     const SchedArgs& a = MXP ? *ap : a_param;
-    if ((int)smid() < a.reserved_sms) return;  // leave these SMs to the POTRF kernels
+    // this rank's SM partition [sm_lo, sm_hi) (all SMs unless ranks share a GPU);
+    // its first `reserved_sms` SMs are left to the POTRF kernels
+    const int id = (int)smid();
+    if (id < a.sm_lo + a.reserved_sms || id >= a.sm_hi) return;
     extern __shared__ __align__(16) double smem[];
     // The task ticket and wait verdict live in the padding columns of the A
     // stage buffer (doubles BM..BM+PAD-1 of row 0 are never read or written by
@@ -803,9 +810,9 @@ void launch_matern_tile_norms(const double* xy, int64_t n, int64_t nb, double si
 // ------------------------------------------------------ input quantization
 // (O3, G14): the accumulator of every task starts from A^ = deq(q_p(A)).
 __global__ void k_tile_amax(const double* pool, const int32_t* slot, int64_t Nt, int64_t nb,
-                            unsigned long long* amax_x) {
+                            unsigned long long* amax_x, int rank, int nranks) {
     const int64_t j = blockIdx.y, i = j + blockIdx.x;
-    if (i >= Nt) return;
+    if (i >= Nt || i % nranks != rank) return;
     const int64_t t = tile_index(Nt, i, j);
     const double* T = pool + (int64_t)slot[t] * nb * nb;
     double v = 0.0;
@@ -815,9 +822,9 @@ __global__ void k_tile_amax(const double* pool, const int32_t* slot, int64_t Nt,
     if ((threadIdx.x & 31) == 0) atomic_max_abs(amax_x + t, v);
 }
 __global__ void k_tile_quantize(double* pool, const int32_t* slot, const uint8_t* prec, int64_t Nt, int64_t nb,
-                                const unsigned long long* amax_x, double* amax_s) {
+                                const unsigned long long* amax_x, double* amax_s, int rank, int nranks) {
     const int64_t j = blockIdx.y, i = j + blockIdx.x;
-    if (i >= Nt) return;
+    if (i >= Nt || i % nranks != rank) return;
     const int64_t t = tile_index(Nt, i, j);
     const int p = prec[t];
     const double amax = amax_of(amax_x + t);
@@ -829,10 +836,10 @@ __global__ void k_tile_quantize(double* pool, const int32_t* slot, const uint8_t
         T[e] = quantize_value(p, T[e], sc);
 }
 void launch_input_quantize(double* pool, const int32_t* slot, const uint8_t* prec, int64_t Nt, int64_t nb,
-                           unsigned long long* amax_x, double* amax_s, cudaStream_t s) {
+                           unsigned long long* amax_x, double* amax_s, cudaStream_t s, int rank, int nranks) {
     dim3 grid((unsigned)Nt, (unsigned)Nt, 8);
-    k_tile_amax<<<grid, 256, 0, s>>>(pool, slot, Nt, nb, amax_x);
-    k_tile_quantize<<<grid, 256, 0, s>>>(pool, slot, prec, Nt, nb, amax_x, amax_s);
+    k_tile_amax<<<grid, 256, 0, s>>>(pool, slot, Nt, nb, amax_x, rank, nranks);
+    k_tile_quantize<<<grid, 256, 0, s>>>(pool, slot, prec, Nt, nb, amax_x, amax_s, rank, nranks);
 }
 
 constexpr int POTRF_SMEM = (2 * PK * 8 > PC::SMEM_BYTES) ? 2 * PK * 8 : PC::SMEM_BYTES;

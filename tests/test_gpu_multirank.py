@@ -1,0 +1,97 @@
+"""-m gpu: multi-GPU path exercised with ranks co-located on one B200 (SM
+partitions; peer pools in the same process; copy-engine pushes).  The factor
+must be bitwise identical to the single-rank one."""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as w
+
+pytestmark = pytest.mark.gpu
+
+
+def _ranks(n, nb, P, pmap=None):
+    import paper_2410_09819_b200 as m
+    plans = [m.Plan(n, nb, pmap) for _ in range(P)]
+    share = 148 // P
+    for r, pl in enumerate(plans):
+        pl.set("rank", r)
+        pl.set("nranks", P)
+        pl.set("sm_first", r * share)
+        pl.set("sm_count", share)
+    for r, pl in enumerate(plans):
+        for q, other in enumerate(plans):
+            if q != r:
+                pl.attach_peer(q, other)
+    return plans
+
+
+def _run(plans, fn):
+    out = [None] * len(plans)
+    errs = []
+
+    def go(r):
+        try:
+            out[r] = fn(r, plans[r])
+        except Exception as e:  # noqa
+            errs.append(e)
+    th = [threading.Thread(target=go, args=(r,)) for r in range(len(plans))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errs, errs
+    return out
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_device_path_ranks_bitwise_equal_single(P):
+    import torch
+
+    from gpu_util import gpu_factor
+    n, nb = 2048, 256
+    A = w.plgsy(n, seed=17)
+    L1, info, ld1, _ = gpu_factor(A, nb)
+    plans = _ranks(n, nb, P)
+    As = [torch.tensor(np.ascontiguousarray(A.T), device="cuda").T for _ in range(P)]
+
+    def fn(r, pl):
+        info = pl.factor_device(As[r], stream_from_torch=False)
+        return info, pl.logdet()
+    res = _run(plans, fn)
+    torch.cuda.synchronize()
+    for r in range(P):
+        assert res[r][0] == 0
+        Lr = np.tril(As[r].cpu().numpy())
+        assert np.array_equal(Lr, L1)          # every rank ends with the whole factor
+        assert res[r][1] == ld1
+
+
+def test_generated_mxp_two_ranks():
+    import paper_2410_09819_b200 as m
+    n, nb = 4096, 256
+    xy = w.matern_locations(n, seed=1)
+    pmap, _ = m.precision_map_matern_device(xy, nb, 1e-8)
+    p1 = m.Plan(n, nb, pmap)
+    assert p1.factor_matern(xy, 1.0, 0.02627) == 0
+    L1 = p1.get_factor().cpu().numpy()
+    plans = _ranks(n, nb, 2, pmap)
+    res = _run(plans, lambda r, pl: (pl.factor_matern(xy, 1.0, 0.02627, stream_from_torch=False), pl.logdet()))
+    for r in range(2):
+        assert res[r][0] == 0
+        assert res[r][1] == p1.logdet()
+        assert np.array_equal(plans[r].get_factor().cpu().numpy(), L1)
+
+
+def test_ranks_not_pd():
+    import torch
+    n, nb = 1024, 256
+    L0 = w.integer_l0(n, seed=5)
+    A = w.spd_from_l0(L0)
+    A[700, 700] = -1.0 + np.sum(L0[700, :700] ** 2)
+    plans = _ranks(n, nb, 2)
+    As = [torch.tensor(np.ascontiguousarray(A.T), device="cuda").T for _ in range(2)]
+    res = _run(plans, lambda r, pl: pl.factor_device(As[r], stream_from_torch=False))
+    assert res == [701, 701]
