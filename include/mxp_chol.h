@@ -67,11 +67,18 @@ typedef enum mxp_attr {
                                      3 = no dedicated POTRF kernels (the scheduler's fallback factors every
                                      diagonal tile) */
     MXP_ATTR_PROFILE = 6,         /* 1 = time every launch with CUDA events on its stream (mxp_chol_kernel_stats) */
-    MXP_ATTR_TC_ENGINE = 7,       /* 1 (default) = GEMM tasks of tiles below FP64 on tcgen05 (kind::tf32: 3xTF32 for
-                                     FP32 tiles, 1xTF32 for FP16/FP8 values); 0 = FP64 DMMA with the same casts */
+    MXP_ATTR_TC_ENGINE = 7,       /* GEMM tasks of tiles below FP64 (G12):
+                                     1 (default) = tcgen05 kind::tf32 (3xTF32 for FP32 tiles, 1xTF32 for the exact
+                                       FP16/FP8 values) fed by bulk copies of per-tile fp32 operand images written
+                                       once by the QUANT tasks (in core; out of core it behaves as 2);
+                                     2 = tcgen05, operands converted from the fp64 tiles in registers;
+                                     0 = FP64 DMMA with the same casts (fp64 accumulation).
+                                     Changing it re-sizes the workspace (images: up to 4 nb^2 fp32 per tile). */
     MXP_ATTR_RANK = 8,            /* this plan's rank in a row-cyclic distribution (tile (m,n) on rank m mod nranks) */
     MXP_ATTR_NRANKS = 9,          /* ranks (GPUs) sharing the factorization, <= 8; peers attached with
-                                     mxp_chol_ipc_attach / mxp_chol_attach_peer_plan */
+                                     mxp_chol_ipc_attach / mxp_chol_attach_peer_plan.  Each rank keeps streams
+                                     parked on cuStreamWaitValue32; ranks co-located in one process need
+                                     CUDA_DEVICE_MAX_CONNECTIONS >= 8 * nranks (set before CUDA starts) */
     MXP_ATTR_SM_FIRST = 10,       /* first SM of this plan's scheduler partition (ranks co-located on one GPU) */
     MXP_ATTR_SM_COUNT = 11,       /* SMs in the partition (0 = all) */
     MXP_ATTR_GPU_LAUNCHES = 100,  /* (get only) kernels launched by the last factorization */

@@ -247,6 +247,28 @@ class Plan:
         buf = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
         _check("mxp_chol_ipc_attach", lib().mxp_chol_ipc_attach(self._h, peer_rank, buf, ws_bytes))
 
+    def connect(self, rank: int, world: int, group=None, sm_partition: bool = False):
+        """Join a row-cyclic multi-GPU factorization, one process per rank:
+        sets rank/nranks, exchanges the workspaces' IPC handles over the
+        torch.distributed ``group`` (object all-gather; plumbing only) and maps
+        every peer's workspace.  ``sm_partition``: ranks share one GPU (tests)
+        and split its SMs evenly.  Collective: every rank must call it."""
+        import torch.distributed as dist
+        self.set("rank", rank)
+        self.set("nranks", world)
+        if sm_partition:
+            import torch
+            nsm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+            share = nsm // world
+            self.set("sm_first", rank * share)
+            self.set("sm_count", share)
+        mine = self.ipc_handle()
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        for q, (h, nbytes) in enumerate(allh):
+            if q != rank:
+                self.ipc_attach(q, h, nbytes)
+
     def attach_peer(self, peer_rank: int, peer: "Plan"):
         _check("mxp_chol_attach_peer_plan", lib().mxp_chol_attach_peer_plan(self._h, peer_rank, peer._h))
 

@@ -90,7 +90,16 @@ struct mxp_plan_s {
     std::vector<int> expected;
     bool list_uploaded = false;
     int reserved_sms = 1;
-    int tc_engine = 1;             // non-FP64 GEMM tasks on tcgen05 (0: DMMA with casts)
+    int tc_engine = 1;             // non-FP64 GEMM tasks: 0 DMMA with casts, 1 tcgen05 on operand
+                                   // images (register-staged when out of core), 2 tcgen05 register-staged
+    // operand images (tcgen05 engine, in core): see SchedArgs::img
+    std::vector<long long> img;    // [4T] byte offsets into the image arena, -1 = absent
+    std::vector<uint8_t> qtile;    // [T] tile has QUANT tasks
+    size_t shadow_bytes = 0;
+    long long img_key = -1;        // (tc_engine, pool) state the image plan was computed for
+    uint8_t* d_qtile = nullptr;
+    long long* d_img = nullptr;
+    uint8_t* d_shadow = nullptr;
     bool mxp = false;              // any tile below FP64
     uint8_t* d_prec = nullptr;
     unsigned long long* d_amax_x = nullptr;
@@ -194,7 +203,9 @@ int64_t nchunks(int64_t k, int64_t KC) {
 //                 (b) bulk GEMM chunks (n < k) of column k+1   [lookahead]
 //                 (c) TRSM row tasks of column k
 // POTRF(k) runs beside it (k_potrf_tile) once (a) has finished on tile (k,k).
+void plan_images(mxp_plan_s* p);
 void build_task_list(mxp_plan_s* p) {
+    plan_images(p);
     const int64_t Nt = p->Nt, nb = p->nb, KC = p->splitk_tiles, NB = blocks_per_tile(nb);
     p->items.clear();
     p->expected.assign(p->T, 0);
@@ -233,9 +244,87 @@ void build_task_list(mxp_plan_s* p) {
                 for (int64_t r = 0; r < nb / 64; ++r)
                     p->items.push_back(make_int4(ITEM_TRSM, (int)m, (int)k, (int)r));
         for (int64_t m = k + 1; m < Nt; ++m)
-            if (owned(m) && p->map[tile_index(Nt, m, k)] != MXP_FP64)
+            if (owned(m) && p->qtile[tile_index(Nt, m, k)])
                 for (int64_t r = 0; r < nb / 64; ++r)
                     p->items.push_back(make_int4(ITEM_QUANT, (int)m, (int)k, (int)r));
+    }
+}
+
+// Operand images (tcgen05 engine): tile t = (i, n) is an operand of the GEMMs
+// of row i (outputs (i, k), n < k < i; A side) and of column i (outputs
+// (m, i), m > i; B side).  Each such output of precision c != FP64 reads
+// cast_c(L_t), i.e. the image e = max(c, p_t) (an operand stored at or below
+// c is used as stored).  One fp32 image per distinct e, plus the TF32
+// remainder for e = FP32.  Out of core (pool < T) the register-staged engine
+// is used instead (images would be sized by the whole lower triangle).
+int64_t pool_slots(const mxp_plan_s* p);
+void plan_images(mxp_plan_s* p) {
+    const long long key = (long long)p->tc_engine * 2 + (pool_slots(p) == p->T ? 1 : 0);
+    if (key == p->img_key) return;
+    p->img_key = key;
+    const int64_t Nt = p->Nt, T = p->T;
+    p->img.assign(4 * T, -1);
+    p->qtile.assign(T, 0);
+    p->shadow_bytes = 0;
+    bool images = p->mxp && p->tc_engine == 1 && pool_slots(p) == T;
+    const long long img_bytes = (long long)sizeof(float) * p->nb * p->nb;
+    if (images) {  // the images must fit beside the pool in this device's free memory
+        long long need = 0;
+        for (int64_t t = 0; t < T; ++t) need += p->map[t] == MXP_FP32 ? 2 : (p->map[t] != MXP_FP64 ? 1 : 0);
+        size_t fr = 0, tot = 0;
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (cudaSetDevice(p->device) == cudaSuccess && cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+            const double pool = (double)sizeof(double) * p->nb * p->nb * T;
+            // lower bound of the image bytes (each non-FP64 tile at least its own image)
+            if (pool + (double)need * img_bytes > 0.9 * ((double)fr + (double)p->ws_bytes)) images = false;
+        }
+        cudaGetLastError();
+        cudaSetDevice(cur);
+    }
+    for (int64_t n = 0; n < Nt; ++n)
+        for (int64_t i = n + 1; i < Nt; ++i) {
+            const int64_t t = tile_index(Nt, i, n);
+            const int pt = p->map[t];
+            bool need[4] = {false, false, false, false};
+            if (images) {
+                for (int64_t k = n + 1; k < i; ++k) {
+                    const int c = p->map[tile_index(Nt, i, k)];
+                    if (c != MXP_FP64) need[std::max(c, pt)] = true;
+                }
+                for (int64_t m = i + 1; m < Nt; ++m) {
+                    const int c = p->map[tile_index(Nt, m, i)];
+                    if (c != MXP_FP64) need[std::max(c, pt)] = true;
+                }
+            }
+            bool any = false;
+            for (int e = 1; e <= 3; ++e)
+                if (need[e]) {
+                    any = true;
+                    p->img[4 * t + e - 1] = (long long)p->shadow_bytes;
+                    p->shadow_bytes += img_bytes;
+                    if (e == MXP_FP32) {
+                        p->img[4 * t + 3] = (long long)p->shadow_bytes;
+                        p->shadow_bytes += img_bytes;
+                    }
+                }
+            p->qtile[t] = (pt != MXP_FP64 || any) ? 1 : 0;
+        }
+    if (images) {  // full size known now: re-check, else use the register-staged engine
+        size_t fr = 0, tot = 0;
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (cudaSetDevice(p->device) == cudaSuccess && cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+            const double pool = (double)sizeof(double) * p->nb * p->nb * T;
+            if (pool + (double)p->shadow_bytes > 0.9 * ((double)fr + (double)p->ws_bytes)) {
+                p->img.assign(4 * T, -1);
+                p->shadow_bytes = 0;
+                for (int64_t t = 0; t < T; ++t) p->qtile[t] = p->map[t] != MXP_FP64 ? 1 : 0;
+                for (int64_t k = 0; k < p->Nt; ++k) p->qtile[tile_index(p->Nt, k, k)] = 0;
+            }
+        }
+        cudaGetLastError();
+        cudaSetDevice(cur);
     }
 }
 
@@ -251,8 +340,7 @@ size_t list_bytes(const mxp_plan_s* p) {
         cnt += nchunks(k, p->splitk_tiles) * per;
     }
     cnt += (Nt * (Nt - 1) / 2) * (nb / 64);
-    for (int64_t k = 0; k < Nt; ++k)
-        for (int64_t m = k + 1; m < Nt; ++m) cnt += (p->map[tile_index(Nt, m, k)] != MXP_FP64) * (nb / 64);
+    for (int64_t t = 0; t < p->T; ++t) cnt += p->qtile[t] * (nb / 64);
     cnt += p->T;   // PREP tasks (host-streaming mode)
     cnt += Nt;     // POTRF claims
     return sizeof(int4) * (size_t)cnt;
@@ -318,10 +406,12 @@ bool plan_slots(mxp_plan_s* p, int64_t C) {
 }
 
 struct Layout {
-    size_t slot, prev, epoch, flags, flags_bytes, expected, items, wbuf, stats, prec, amax_x, amax_s, args, pool, total;
+    size_t slot, prev, epoch, flags, flags_bytes, expected, items, wbuf, stats, prec, amax_x, amax_s, args, qtile, img,
+        shadow, pool, total;
 };
 
 Layout layout(const mxp_plan_s* p) {
+    plan_images(const_cast<mxp_plan_s*>(p));  // (cached; depends on map, engine and pool size)
     Layout L{};
     size_t off = 256 + align_up(sizeof(double) * (p->Nt + 2), 256);  // info, logdet parts
     L.slot = off;
@@ -349,6 +439,12 @@ Layout layout(const mxp_plan_s* p) {
     off += align_up(sizeof(double) * (size_t)p->T, 256);
     L.args = off;
     off += align_up(sizeof(SchedArgs), 256);
+    L.qtile = off;
+    off += align_up((size_t)p->T, 256);
+    L.img = off;
+    off += align_up(sizeof(long long) * 4 * (size_t)p->T, 256);
+    L.shadow = off;
+    off += align_up(p->shadow_bytes, 1024);
     L.pool = off;
     off += sizeof(double) * (size_t)pool_slots(p) * p->nb * p->nb;
     L.total = off;
@@ -390,6 +486,9 @@ void bind_workspace(mxp_plan_s* p) {
     p->d_prec = (uint8_t*)(p->ws + L.prec);
     p->d_amax_s = (double*)(p->ws + L.amax_s);
     p->d_args = (SchedArgs*)(p->ws + L.args);
+    p->d_qtile = (uint8_t*)(p->ws + L.qtile);
+    p->d_img = (long long*)(p->ws + L.img);
+    p->d_shadow = (uint8_t*)(p->ws + L.shadow);
     p->d_amax_x = (unsigned long long*)(p->ws + L.flags + align_up(sizeof(int) * flag_ints(p), 8));
     p->pool = (double*)(p->ws + L.pool);
 }
@@ -528,6 +627,12 @@ void push_tiles(mxp_plan_s* p, const SchedArgs& a) {
                 if (p->mxp)
                     CK(cudaMemcpyAsync(peer_addr(p, q, p->d_amax_s + t), p->d_amax_s + t, sizeof(double),
                                        cudaMemcpyDeviceToDevice, p->sPush));
+                for (int e = 0; e < 4 && p->shadow_bytes > 0; ++e)  // the tile's operand images
+                    if (p->img[4 * t + e] >= 0) {
+                        const uint8_t* im = p->d_shadow + p->img[4 * t + e];
+                        CK(cudaMemcpyAsync(peer_addr(p, q, im), im, sizeof(float) * nb * nb,
+                                           cudaMemcpyDeviceToDevice, p->sPush));
+                    }
                 CK(cudaMemcpyAsync(peer_addr(p, q, a.ready + t), p->d_epoch, sizeof(int), cudaMemcpyDeviceToDevice,
                                    p->sPush));
             }
@@ -606,6 +711,8 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
         CK(cudaMemcpyAsync(p->d_items, p->items.data(), sizeof(int4) * p->items.size(), cudaMemcpyHostToDevice, s0));
         CK(cudaMemcpyAsync(p->d_expected, p->expected.data(), sizeof(int) * T, cudaMemcpyHostToDevice, s0));
         CK(cudaMemcpyAsync(p->d_prec, p->map.data(), (size_t)T, cudaMemcpyHostToDevice, s0));
+        CK(cudaMemcpyAsync(p->d_qtile, p->qtile.data(), (size_t)T, cudaMemcpyHostToDevice, s0));
+        CK(cudaMemcpyAsync(p->d_img, p->img.data(), sizeof(long long) * 4 * T, cudaMemcpyHostToDevice, s0));
         CK(cudaStreamSynchronize(s0));
         p->list_uploaded = true;
     }
@@ -654,6 +761,9 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
         a.gen_nugget = gen->nugget;
     }
     a.prec = p->mxp ? p->d_prec : nullptr;
+    a.qtile = p->d_qtile;
+    a.img = (p->mxp && p->shadow_bytes > 0) ? p->d_img : nullptr;
+    a.shadow = p->d_shadow;
     a.tc_engine = p->tc_engine;
     a.amax_x = p->d_amax_x;
     a.amax_s = p->d_amax_s;
@@ -686,10 +796,16 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     a.sm_lo = p->sm_count > 0 ? p->sm_first : 0;
     a.sm_hi = p->sm_count > 0 ? std::min(nsm, p->sm_first + p->sm_count) : nsm;
     int occ = sched_ctas_per_sm();
+    // algorithmic flops of this rank's tasks: row m of L costs (m^2 + m) nb^3
+    // in GEMM/SYRK/TRSM (sum over all rows: n^3/3 - Nt nb^3/3) + nb^3/3 POTRF
     const double nb3 = (double)p->nb * p->nb * p->nb;
-    const double total = (double)Nt * Nt * Nt * nb3 / 3.0;
+    double chain_flops = 0.0, potrf_flops = 0.0;
+    for (int64_t m = p->rank; m < Nt; m += p->nranks) {
+        chain_flops += ((double)m * m + (double)m) * nb3;
+        potrf_flops += nb3 / 3.0;
+    }
     {
-        Prof pr(p, p->sU, MXP_KCLASS_CHAIN, total - (double)Nt * nb3 / 3.0);
+        Prof pr(p, p->sU, MXP_KCLASS_CHAIN, chain_flops);
         p->h_args = a;
         CK(cudaMemcpyAsync(p->d_args, &p->h_args, sizeof(SchedArgs), cudaMemcpyHostToDevice, p->sU));
         launch_sched(a, p->d_args, p->mxp, occ * nsm, p->sU);
@@ -697,7 +813,7 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
         dbg(p, p->sU, "sched");
     }
     {
-        Prof pr(p, p->sP, MXP_KCLASS_POTRF, (double)Nt * nb3 / 3.0, Nt);
+        Prof pr(p, p->sP, MXP_KCLASS_POTRF, potrf_flops, (Nt - p->rank + p->nranks - 1) / p->nranks);
         if (p->debug_sync != 2 && p->debug_sync != 3) {  // 3: every POTRF by the scheduler fallback
             for (int64_t k = p->rank; k < Nt; k += p->nranks) {  // diagonal tiles this rank owns
                 launch_potrf_tile(a, k, p->sP);
@@ -713,6 +829,7 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
         const int64_t nb = p->nb, n = p->n;
         for (int64_t k = 0; k < Nt; ++k)
             for (int64_t m = k; m < Nt; ++m) {
+                if (m % p->nranks != p->rank) continue;  // peers stream their own rows
                 const int64_t t = tile_index(Nt, m, k);
                 const int64_t rr = std::min(nb, n - m * nb), cr = std::min(nb, n - k * nb);
                 double* dst = p->pool + (size_t)p->slot_plan[t] * nb * nb;
@@ -737,6 +854,7 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
         // diagonal tiles go to a pinned stage and only their lower triangle is merged
         for (int64_t k = 0; k < Nt; ++k)
             for (int64_t m = k; m < Nt; ++m) {
+                if (m % p->nranks != p->rank) continue;
                 const int64_t t = tile_index(Nt, m, k);
                 const int64_t rr = std::min(nb, n - m * nb), cr = std::min(nb, n - k * nb);
                 if (g_wait32((CUstream)p->sD2H, (CUdeviceptr)(a.ready + t), (cuuint32_t)p->epoch,
@@ -908,13 +1026,14 @@ int mxp_chol_plan_set(mxp_plan_t p, mxp_attr_t key, int64_t v) {
         p->sm_count = (int)v;
         return MXP_OK;
     case MXP_ATTR_TC_ENGINE:
-        if (p->ws && !p->ws_owned) return MXP_ESTATE;  // changes the task list size
+        if (v < 0 || v > 2) return -3;
+        if (p->ws && !p->ws_owned) return MXP_ESTATE;  // changes the task list / image sizes
         if (p->ws_owned) {
             cudaFree(p->ws);
             p->ws = nullptr;
             p->ws_owned = false;
         }
-        p->tc_engine = v ? 1 : 0;
+        p->tc_engine = (int)v;
         p->list_uploaded = false;
         return MXP_OK;
     default: return -2;
@@ -1076,8 +1195,11 @@ int mxp_chol_factor(mxp_plan_t p, double* A_host, int64_t lda, int64_t* info) {
     // Host-resident path (Alg. 2): tiles stream host->device on a copy
     // stream in schedule order while the static schedule runs; each finished
     // tile streams back as soon as it is final (lower triangle only).
-    if (p->nranks > 1) {
-        g_last_error = "host-resident input with several ranks: not in this build (use the device or generated path)";
+    // Several ranks: each rank reads and writes back only the tile rows it
+    // owns (m mod nranks == rank); ranks sharing one host matrix (e.g. a
+    // shared-memory mapping) together produce all of L.  In-core only.
+    if (p->nranks > 1 && pool_slots(p) < p->T) {
+        g_last_error = "out-of-core streaming with several ranks: not in this build";
         return MXP_ENOTSUP;
     }
     p->have_result = false;
@@ -1128,6 +1250,7 @@ int mxp_chol_factor(mxp_plan_t p, double* A_host, int64_t lda, int64_t* info) {
         CK(cudaMemsetAsync(p->d_info, 0, sizeof(int64_t), s0));
         prof_reset(p);
         factor_incore_f64(p, s0, true, A_host, lda);
+        finish_pushes(p, s0);  // several ranks: drain / await the tile exchange
         // the schedule (U) and the POTRFs (P) end first; on failure the later
         // Ready flags never flip, so release the D2H stream explicitly
         CK(cudaStreamSynchronize(p->sU));
@@ -1141,6 +1264,7 @@ int mxp_chol_factor(mxp_plan_t p, double* A_host, int64_t lda, int64_t* info) {
             int* col_ready = p->d_flags + 2 + 6 * p->T + p->T * blocks_per_tile(p->nb) + p->Nt;
             CK(cudaMemsetAsync(col_ready, 0x7f, sizeof(int) * p->Nt, p->sAux));
             CK(cudaStreamSynchronize(p->sAux));
+            p->ready_dirty = true;
         }
         CK(cudaStreamSynchronize(p->sD2H));
         CK(cudaStreamSynchronize(p->sH2D));
@@ -1156,6 +1280,7 @@ int mxp_chol_factor(mxp_plan_t p, double* A_host, int64_t lda, int64_t* info) {
             for (unsigned w = 0; w < nth; ++w)
                 th.emplace_back([&, w] {
                     for (int64_t k = w; k < Nt; k += nth) {
+                        if (k % p->nranks != p->rank) continue;
                         const int64_t cr = std::min(nb, n - k * nb);
                         const double* S = p->h_stage + (size_t)k * nb * nb;
                         for (int64_t c = 0; c < cr; ++c)

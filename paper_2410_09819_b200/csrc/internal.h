@@ -59,6 +59,14 @@ struct SchedArgs {
     int rank, nranks;
     int sm_lo, sm_hi;          // SM partition of this rank's scheduler (co-located ranks)
     int64_t* peer_dinfo[MAX_RANKS];  // peers' info words (a failed pivot stops every rank)
+    // MxP operand images (tcgen05 engine, in core): per lower tile 4 byte
+    // offsets into `shadow` (-1 = absent): [0..2] = fp32 image of cast_e(L)
+    // for e = FP32, FP16, FP8; [3] = the TF32 remainder (lo) of the FP32 image.
+    // Each image is nb/128 row blocks x nb/16 K-chunks of 8 KB, every chunk in
+    // the tcgen05 shared-memory layout (tc_tf32.cuh).
+    const uint8_t* qtile;      // [T] 1 = tile has QUANT tasks (stored below FP64 or has images)
+    const long long* img;      // [4T] (nullptr: no images; register-staged engine)
+    uint8_t* shadow;
     int reserved_sms;          // SMs (smid < this) left to the POTRF kernels
     unsigned long long* stats; // optional diagnostics (MXP_ATTR_PROFILE): see STAT_*
 };

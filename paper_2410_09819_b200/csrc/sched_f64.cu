@@ -286,7 +286,7 @@ __device__ __forceinline__ bool task_trsm(const SchedArgs& a, int64_t m, int64_t
     __syncthreads();
     if (threadIdx.x == 0) {
         int old = atom_add_release(a.trsm_done + t, 1);
-        const bool fp64 = !a.prec || a.prec[t] == P_FP64;
+        const bool fp64 = !a.prec || !a.qtile[t];  // no QUANT task follows
         if (old + 1 == (int)(nb / 64) && fp64) {
             // FP64 tile: stored values are the TRSM result; amax_s drives later down-casts
             a.amax_s[t] = amax_of(a.amax_x + t);
@@ -375,6 +375,72 @@ __device__ __noinline__ bool task_gemm_tc(const SchedArgs& a, int64_t m, int64_t
     return true;
 }
 
+// tcgen05 GEMM task on operand images: the same contraction as task_gemm_tc,
+// operands bulk-copied from the per-tile fp32 images of cast_c(L) (written
+// once by the QUANT task of each operand tile), image e = max(c, p_operand)
+// (an operand stored at or below c is used as stored).
+template <bool THREE>
+__device__ __noinline__ bool task_gemm_img(const SchedArgs& a, int64_t m, int64_t k, int64_t b, int64_t c,
+                                           int cprec, uint8_t* smem, uint32_t tmem, int* s_flag) {
+    const int64_t Nt = a.Nt, nb = a.nb, S = nb / 128;
+    const int64_t bi = b % S, bj = b / S;
+    const int64_t t = tile_index(Nt, m, k);
+    int64_t n0, n1;
+    chunk_range(k, c, a.KC, n0, n1);
+    int* chunk_flag = a.blk_chunk + t * a.NB + b;
+    uint64_t tw0 = 0;
+    if (threadIdx.x == 0) {
+        if (a.stats) tw0 = globaltimer();
+        bool ok = wait_input(a, t, k);
+        for (int64_t n = n0; n < n1 && ok; ++n)
+            ok = wait_flag(a.ready + tile_index(Nt, m, n), a.epoch, a, k) &&
+                 wait_flag(a.ready + tile_index(Nt, k, n), a.epoch, a, k);
+        if (ok) ok = wait_flag(chunk_flag, (int)c, a, k);
+        *s_flag = ok;
+        if (a.stats) {
+            uint64_t tw1 = globaltimer();
+            atomicAdd(a.stats + STAT_GEMM_WAIT, tw1 - tw0);
+            tw0 = tw1;
+        }
+    }
+    __syncthreads();
+    if (!*s_flag) return false;
+    const int64_t kper = nb / tc::KS;
+    const int nsteps = (int)((n1 - n0) * kper);
+    const int64_t aoff = bi * kper * tc::SUB_BYTES, boff = bj * kper * tc::SUB_BYTES;
+    int64_t cur_n = n0 - 1, kc = kper;
+    const uint8_t *ahi = nullptr, *alo = nullptr, *bhi = nullptr, *blo = nullptr;
+    auto src = [&](int) {
+        if (kc == kper) {
+            kc = 0;
+            ++cur_n;
+            const int64_t ta = tile_index(Nt, m, cur_n), tb = tile_index(Nt, k, cur_n);
+            const int ea = a.prec[ta] > cprec ? a.prec[ta] : cprec;
+            const int eb = a.prec[tb] > cprec ? a.prec[tb] : cprec;
+            ahi = a.shadow + a.img[4 * ta + ea - 1] + aoff;
+            bhi = a.shadow + a.img[4 * tb + eb - 1] + boff;
+            alo = (THREE && ea == P_FP32) ? a.shadow + a.img[4 * ta + 3] + aoff : nullptr;
+            blo = (THREE && eb == P_FP32) ? a.shadow + a.img[4 * tb + 3] + boff : nullptr;
+        }
+        const int64_t o = kc * tc::SUB_BYTES;
+        ++kc;
+        return tc::ImgStep{ahi + o, alo ? alo + o : nullptr, bhi + o, blo ? blo + o : nullptr};
+    };
+    double* Ct = tile_ptr(a.pool, a.slot, Nt, nb, m, k) + bi * 128 + bj * 128 * nb;
+    tc::block_gemm_img<THREE>(Ct, nb, src, nsteps, smem, tmem);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        st_release(chunk_flag, (int)c + 1);
+        atom_add_release(a.gemm_done + t, 1);
+        if (a.stats) {
+            atomicAdd(a.stats + STAT_GEMM_BUSY, globaltimer() - tw0);
+            atomicAdd(a.stats + STAT_GEMM_N, 1ull);
+        }
+    }
+    return true;
+}
+
 // --------------------------------------------------------------- QUANT task
 // L_mk = deq(q_p(X)) on rows [64r, 64r+64) once every TRSM row task of the
 // tile has contributed to its amax (quantize once per task, after TRSM; O4).
@@ -386,16 +452,66 @@ __device__ __noinline__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k
     if (!*s_flag) return false;
     const int p = a.prec[t];
     const double amax = amax_of(a.amax_x + t);
-    const double sc = tile_scale(p, amax);
+    const double sc = tile_scale(p, amax), isc = 1.0 / sc;
+    const double amax_st = quantize_value(p, amax, sc, isc);  // q is monotone: max|q(x)| = q(max|x|)
     double* X = tile_ptr(a.pool, a.slot, Nt, nb, m, k) + r * 64;
-    for (int64_t idx = threadIdx.x; idx < 64 * nb; idx += blockDim.x) {
-        double* q = X + (idx & 63) + (idx >> 6) * nb;
-        __stcg(q, quantize_value(p, __ldcg(q), sc));
+    // operand images of this tile (rows [64r, 64r+64)): fp32 values of
+    // cast_e(L) = deq(q_e(L)) with the stored amax (identity when e <= p),
+    // FP32 image split into TF32 hi + lo (3xTF32)
+    uint8_t* im[4] = {nullptr, nullptr, nullptr, nullptr};
+    Cast ce[3];
+    bool any = false;
+    if (a.img) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const long long o = a.img[4 * t + e];
+            if (o >= 0) im[e] = a.shadow + o, any = true;
+        }
+#pragma unroll
+        for (int e = 0; e < 3; ++e) ce[e] = make_cast(p, e + 1, amax_st);
+    }
+    if (p != P_FP64 || any) {
+        const int64_t kper = nb / tc::KS;
+        for (int64_t idx = threadIdx.x; idx < 16 * nb; idx += blockDim.x) {
+            const int q4 = (int)(idx & 15), col = (int)(idx >> 4);
+            double* q = X + 4 * q4 + (int64_t)col * nb;
+            double2 v01 = __ldcg(reinterpret_cast<const double2*>(q));
+            double2 v23 = __ldcg(reinterpret_cast<const double2*>(q + 2));
+            double x[4] = {v01.x, v01.y, v23.x, v23.y};
+            if (p != P_FP64) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) x[i] = quantize_value(p, x[i], sc, isc);
+                __stcg(reinterpret_cast<double2*>(q), make_double2(x[0], x[1]));
+                __stcg(reinterpret_cast<double2*>(q + 2), make_double2(x[2], x[3]));
+            }
+            if (!any) continue;
+            const int row = (int)(r * 64) + 4 * q4;
+            const int64_t chunk = (int64_t)(row >> 7) * kper + (col >> 4);
+            const uint32_t off = tc::sw_offset(row & 127, col & 15);
+#pragma unroll
+            for (int e = 0; e < 3; ++e) {
+                if (!im[e]) continue;
+                float f[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) f[i] = (float)apply_cast(ce[e], x[i]);
+                uint8_t* dst = im[e] + chunk * tc::SUB_BYTES + off;
+                if (e == 0) {  // FP32: hi = RNE_tf32(v), lo = RNE_tf32(v - hi)
+                    float h[4], l[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) h[i] = tc::rne_tf32(f[i]), l[i] = tc::rne_tf32(f[i] - h[i]);
+                    __stcg(reinterpret_cast<float4*>(dst), make_float4(h[0], h[1], h[2], h[3]));
+                    __stcg(reinterpret_cast<float4*>(im[3] + chunk * tc::SUB_BYTES + off),
+                           make_float4(l[0], l[1], l[2], l[3]));
+                } else {
+                    __stcg(reinterpret_cast<float4*>(dst), make_float4(f[0], f[1], f[2], f[3]));
+                }
+            }
+        }
     }
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
-        a.amax_s[t] = quantize_value(p, amax, sc);  // q is monotone: max|q(x)| = q(max|x|)
+        a.amax_s[t] = amax_st;
         __threadfence();
         int old = atom_add_release(a.quant_done + t, 1);
         if (old + 1 == (int)(nb / 64)) {
@@ -738,6 +854,10 @@ __global__ void __launch_bounds__(CC::NT, 3) k_sched(const SchedArgs a_param, co
                     task_gemm<false>(a, m, k, it.w >> 16, it.w & 0xFFFF, smem, &s_flag);
                 else if (!a.tc_engine)
                     task_gemm_cast(*ap, m, k, it.w >> 16, it.w & 0xFFFF, smem, &s_flag);
+                else if (a.img && cp == P_FP32)
+                    task_gemm_img<true>(*ap, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_b, tmem, &s_flag);
+                else if (a.img)
+                    task_gemm_img<false>(*ap, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_b, tmem, &s_flag);
                 else if (cp == P_FP32)
                     task_gemm_tc<true>(*ap, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_b, mbar, tmem, &s_flag);
                 else

@@ -130,5 +130,129 @@ __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int nsteps, i
     }
 }
 
+// ---------------------------------------------------------------------------
+// Operand-image variant: the operands arrive as pre-built fp32 images of
+// cast_c(L) in exactly the shared-memory layout above (8 KB per 128 x 16
+// chunk), written once per tile by the QUANT task (see sched_f64.cu), so the
+// main loop is bulk copies (TMA engine, cp.async.bulk + mbarrier tx counts)
+// feeding tcgen05.mma -- no per-element work on the SMs.
+//
+// Stage = 32 KB = 4 chunks: THREE: A_hi | A_lo | B_hi | B_lo of one K = 16
+// step (lo chunks absent -> that product is skipped: the operand is exact in
+// TF32); else A(s) | A(s+1) | B(s) | B(s+1) (K = 32 per stage).  Two stages;
+// one elected thread issues copies and MMAs; all threads run the epilogue.
+struct ImgStep {
+    const uint8_t* ahi;
+    const uint8_t* alo;  // nullptr: A exact in TF32
+    const uint8_t* bhi;
+    const uint8_t* blo;
+};
+constexpr int IMG_STAGE = 4 * SUB_BYTES;                     // 32 KB
+constexpr int IMG_SMEM_BYTES = 1024 + 2 * IMG_STAGE + 64;    // + alignment slack + 5 mbarriers
+
+template <bool THREE, class Src>
+__device__ void block_gemm_img(double* C, int64_t ldc, const Src& src, int nsteps, uint8_t* smem, uint32_t tmem) {
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + 2 * IMG_STAGE);
+    uint64_t* done = full + 2;
+    uint64_t* fin = full + 4;  // one-shot: every MMA of the block has completed
+    const int nst = THREE ? nsteps : (nsteps + 1) / 2;  // stages to run
+    if (threadIdx.x == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        mbar_init(&done[0], 1);
+        mbar_init(&done[1], 1);
+        mbar_init(fin, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // stage contents: which of the 4 chunks hold data (bit i = chunk i)
+        auto issue = [&](int st, int stage) -> uint32_t {
+            uint8_t* B0 = base + stage * IMG_STAGE;
+            const uint8_t* srcs[4];
+            if (THREE) {
+                const ImgStep c = src(st);
+                srcs[0] = c.ahi, srcs[1] = c.alo, srcs[2] = c.bhi, srcs[3] = c.blo;
+            } else {
+                const ImgStep c0 = src(2 * st);
+                srcs[0] = c0.ahi, srcs[2] = c0.bhi;
+                if (2 * st + 1 < nsteps) {
+                    const ImgStep c1 = src(2 * st + 1);
+                    srcs[1] = c1.ahi, srcs[3] = c1.bhi;
+                } else {
+                    srcs[1] = srcs[3] = nullptr;
+                }
+            }
+            uint32_t mask = 0, bytes = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (srcs[i]) mask |= 1u << i, bytes += SUB_BYTES;
+            mbar_expect_tx(&full[stage], bytes);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (srcs[i]) bulk_g2s(B0 + i * SUB_BYTES, srcs[i], SUB_BYTES, &full[stage]);
+            return mask;
+        };
+        uint32_t masks[2];
+        masks[0] = issue(0, 0);
+        if (nst > 1) masks[1] = issue(1, 1);
+        for (int st = 0; st < nst; ++st) {
+            const int stage = st & 1;
+            mbar_wait(&full[stage], (st >> 1) & 1);
+            fence_after();
+            const uint32_t b0 = smem_u32(base + stage * IMG_STAGE);
+            const uint32_t m = masks[stage];
+#pragma unroll
+            for (int kg = 0; kg < KS / 8; ++kg) {
+                const uint32_t ko = kg * KSTEP_BYTES;
+                if (THREE) {
+                    const uint32_t acc0 = (st > 0 || kg > 0) ? 1u : 0u;
+                    mma_tf32(tmem, make_desc(b0 + ko), make_desc(b0 + 2 * SUB_BYTES + ko), acc0);
+                    if (m & 8u) mma_tf32(tmem, make_desc(b0 + ko), make_desc(b0 + 3 * SUB_BYTES + ko), 1u);
+                    if (m & 2u) mma_tf32(tmem, make_desc(b0 + SUB_BYTES + ko), make_desc(b0 + 2 * SUB_BYTES + ko), 1u);
+                } else {
+                    const uint32_t acc0 = (st > 0 || kg > 0) ? 1u : 0u;
+                    mma_tf32(tmem, make_desc(b0 + ko), make_desc(b0 + 2 * SUB_BYTES + ko), acc0);
+                    if (m & 2u)
+                        mma_tf32(tmem, make_desc(b0 + SUB_BYTES + ko), make_desc(b0 + 3 * SUB_BYTES + ko), 1u);
+                }
+            }
+            commit(&done[stage]);
+            if (st + 2 < nst) {
+                mbar_wait(&done[stage], (st >> 1) & 1);  // this stage's MMAs have read their operands
+                masks[stage] = issue(st + 2, stage);
+            }
+        }
+        commit(fin);  // tracks every earlier tcgen05 op of this thread
+    }
+    __syncwarp();
+    // (a one-shot barrier: the per-stage ones may be several phases ahead of
+    // a thread that starts waiting early, and parity waits would alias)
+    mbar_wait(fin, 0);
+    fence_after();
+    const int warp = threadIdx.x >> 5, row = threadIdx.x;
+    const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+    for (int c0 = 0; c0 < N; c0 += 32) {
+        float v[32];
+        tmem_ld32(tl + c0, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            double* p = C + row + (int64_t)(c0 + i) * ldc;
+            __stcg(p, __ldcg(p) - (double)v[i]);
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        mbar_inval(&full[0]);
+        mbar_inval(&full[1]);
+        mbar_inval(&done[0]);
+        mbar_inval(&done[1]);
+        mbar_inval(fin);
+    }
+}
+
 }  // namespace tc
 }  // namespace mxp

@@ -107,6 +107,29 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// mbarrier transaction count for bulk copies (tx bytes), then arrive
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes)
+                 : "memory");
+}
+// TMA-engine bulk copy global -> this CTA's shared memory, completing on mbar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+        : "memory");
+}
+
+// round-to-nearest-even to TF32 (10 explicit mantissa bits); the result is
+// exact as a tensor-core TF32 operand
+__device__ __forceinline__ float rne_tf32(float x) {
+    uint32_t b = __float_as_uint(x);
+    if ((b & 0x7F800000u) == 0x7F800000u) return x;  // inf / nan
+    b += 0x0FFFu + ((b >> 13) & 1u);
+    return __uint_as_float(b & 0xFFFFE000u);
+}
+
 // 3xTF32 split: x = hi + lo with hi = x rounded to tf32 (10 explicit bits)
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
     uint32_t b = __float_as_uint(x);

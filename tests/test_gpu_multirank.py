@@ -95,3 +95,56 @@ def test_ranks_not_pd():
     As = [torch.tensor(np.ascontiguousarray(A.T), device="cuda").T for _ in range(2)]
     res = _run(plans, lambda r, pl: pl.factor_device(As[r], stream_from_torch=False))
     assert res == [701, 701]
+    # the same rank plans recover on the next (good) matrix
+    A2 = w.spd_from_l0(L0)
+    As = [torch.tensor(np.ascontiguousarray(A2.T), device="cuda").T for _ in range(2)]
+    res = _run(plans, lambda r, pl: pl.factor_device(As[r], stream_from_torch=False))
+    torch.cuda.synchronize()
+    assert res == [0, 0]
+    for r in range(2):
+        assert np.array_equal(np.tril(As[r].cpu().numpy()), L0)
+
+
+def test_host_path_ranks_stream_their_rows():
+    """Host streaming with two ranks: each rank reads and writes back only its
+    own tile rows; together (row m from rank m mod P) they return the
+    single-rank factor bit for bit, and the upper triangle is untouched."""
+    import torch
+
+    from gpu_util import gpu_factor
+    n, nb, P = 2000, 256, 2
+    A = w.plgsy(n, seed=23)
+    L1, info, ld1, _ = gpu_factor(A, nb, host=True)
+    assert info == 0
+    plans = _ranks(n, nb, P)
+    Hs = [torch.tensor(np.asfortranarray(A)).T.contiguous().T for _ in range(P)]
+    res = _run(plans, lambda r, pl: (pl.factor(Hs[r], stream_from_torch=False), pl.logdet()))
+    L = np.zeros_like(A)
+    for r in range(P):
+        assert res[r][0] == 0 and res[r][1] == ld1
+        H = Hs[r].numpy()
+        iu = np.triu_indices(n, 1)
+        assert np.array_equal(H[iu], A[iu])
+        for m_ in range(r, -(-n // nb), P):
+            rows = slice(m_ * nb, min(n, (m_ + 1) * nb))
+            L[rows, :] = np.tril(H)[rows, :]
+    assert np.array_equal(L, L1)
+
+
+def test_ranks_repeat_factorizations():
+    """Epoch-valued Ready words and the start barrier: back-to-back
+    factorizations on the same rank plans stay bitwise equal."""
+    import torch
+
+    from gpu_util import gpu_factor
+    n, nb, P = 1536, 256, 2
+    A = w.plgsy(n, seed=29)
+    L1, _, _, _ = gpu_factor(A, nb)
+    plans = _ranks(n, nb, P)
+    for it in range(3):
+        As = [torch.tensor(np.ascontiguousarray(A.T), device="cuda").T for _ in range(P)]
+        res = _run(plans, lambda r, pl: pl.factor_device(As[r], stream_from_torch=False))
+        torch.cuda.synchronize()
+        assert res == [0] * P
+        for r in range(P):
+            assert np.array_equal(np.tril(As[r].cpu().numpy()), L1), (it, r)

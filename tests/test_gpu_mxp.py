@@ -21,12 +21,14 @@ def _matern(n, a=0.02627):
     return w.matern_cov(xy, 1.0, a)
 
 
-@pytest.mark.parametrize("tc", [1, 0])
+@pytest.mark.parametrize("tc", [1, 2, 0])
 @pytest.mark.parametrize("eps", [1e-5, 1e-8])
 @pytest.mark.parametrize("n,nb", [(2048, 128), (4096, 256), (1900, 256)])
 def test_mxp_matern_against_oracle(n, nb, eps, tc):
-    """tc=1: tiles below FP64 on tcgen05 (3xTF32 / 1xTF32, fp32 accumulation);
-    tc=0: the same casts on FP64 DMMA (fp64 accumulation, like the oracle)."""
+    """tc=1: tiles below FP64 on tcgen05 fed by per-tile operand images
+    (3xTF32 / 1xTF32, fp32 accumulation); tc=2: tcgen05 with operands
+    converted in registers; tc=0: the same casts on FP64 DMMA (fp64
+    accumulation, like the oracle)."""
     S = _matern(n)
     pmap = oracle.plan(S, nb, eps)
     assert np.any(pmap != oracle.FP64)
