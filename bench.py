@@ -403,7 +403,10 @@ def run_ours(args):
                 assert inf == 0, inf
                 ts.append(allreduce(e0.elapsed_time(e1) / 1e3, "max"))
             ld_ = pl.logdet()
+            run.ws_gb = pl.workspace_size() / 1e9
+            run.img_gb = pl.get("image_bytes") / 1e9
             pl.close()
+            del pl
             torch.cuda.empty_cache()
             return min(ts[1:] if len(ts) > 1 else ts), ld_
 
@@ -418,6 +421,7 @@ def run_ours(args):
             llm = -0.5 * nm * math.log(2 * math.pi) - 0.5 * ldm
             mxp["maps"][f"{eps:g}"] = {
                 "tflops": flops_m / tm / 1e12, "ms": tm * 1e3, "speedup_vs_fp64": t64 / tm,
+                "workspace_gb": round(run.ws_gb, 2), "operand_images_gb": round(run.img_gb, 2),
                 "tile_fractions_fp64_fp32_fp16_fp8": [round(float(np.mean(pmap == c)), 4) for c in range(4)],
                 "loglik_y0_rel_err": abs(llm - ll64) / abs(ll64), "logdet_abs_diff": abs(ldm - ld64),
                 "kl_eq3": ll64 - llm}

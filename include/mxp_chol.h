@@ -85,7 +85,8 @@ typedef enum mxp_attr {
     MXP_ATTR_H2D_BYTES = 101,     /* (get only) host->device bytes moved by the last factorization */
     MXP_ATTR_D2H_BYTES = 102,     /* (get only) device->host bytes moved by the last factorization */
     MXP_ATTR_POOL_SLOTS = 103,    /* (get only) tile slots in the device pool */
-    MXP_ATTR_NT = 104             /* (get only) Nt = ceil(n/nb) */
+    MXP_ATTR_NT = 104,            /* (get only) Nt = ceil(n/nb) */
+    MXP_ATTR_IMAGE_BYTES = 105    /* (get only) bytes of tcgen05 operand images in the workspace (0: none) */
 } mxp_attr_t;
 
 /*

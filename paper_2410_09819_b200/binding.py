@@ -16,7 +16,7 @@ ATTR = {
     "device": 0, "stream": 1, "hbm_bytes_cap": 2, "splitk_tiles": 3, "lookahead": 4,
     "debug_sync": 5, "profile": 6, "tc_engine": 7, "rank": 8, "nranks": 9, "sm_first": 10,
     "sm_count": 11, "gpu_launches": 100, "h2d_bytes": 101, "d2h_bytes": 102,
-    "pool_slots": 103, "nt": 104,
+    "pool_slots": 103, "nt": 104, "image_bytes": 105,
 }
 
 # every symbol include/mxp_chol.h declares (tests check the library exports them)
@@ -150,6 +150,7 @@ class Plan:
         if getattr(self, "_h", None) and self._h.value:
             lib().mxp_chol_plan_destroy(self._h)
             self._h = ctypes.c_void_p()
+        self._ws = self._ws_keep = None  # release a torch-provided workspace with the plan
 
     def set(self, key: str, value: int):
         _check(f"mxp_chol_plan_set({key})", lib().mxp_chol_plan_set(self._h, ATTR[key], int(value)))

@@ -1079,6 +1079,7 @@ int mxp_chol_plan_get(mxp_plan_t p, mxp_attr_t key, int64_t* v) {
     case MXP_ATTR_D2H_BYTES: *v = p->d2h; return MXP_OK;
     case MXP_ATTR_POOL_SLOTS: *v = pool_slots(p); return MXP_OK;
     case MXP_ATTR_NT: *v = p->Nt; return MXP_OK;
+    case MXP_ATTR_IMAGE_BYTES: plan_images(p); *v = (int64_t)p->shadow_bytes; return MXP_OK;
     default: return -2;
     }
 }
