@@ -298,7 +298,9 @@ class Plan:
                for k in range(nt)]
         return {"gemm_busy_ms": v[0] / 1e6, "gemm_wait_ms": v[1] / 1e6, "trsm_busy_ms": v[2] / 1e6,
                 "trsm_wait_ms": v[3] / 1e6, "gemm_tasks": v[4], "trsm_tasks": v[5], "span_ms": span,
-                "ctas": v[8], "potrf_timeline_ms": pot}
+                "ctas": v[8], "potrf_phase_ms": {"update": v[9] / 1e6, "chol": v[10] / 1e6, "inverse": v[11] / 1e6,
+                                                  "trsm": v[12] / 1e6},
+                "potrf_timeline_ms": pot}
 
     def logdet(self) -> float:
         v = ctypes.c_double()

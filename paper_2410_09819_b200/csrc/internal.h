@@ -74,6 +74,9 @@ struct SchedArgs {
 enum {
     STAT_GEMM_BUSY = 0, STAT_GEMM_WAIT = 1, STAT_TRSM_BUSY = 2, STAT_TRSM_WAIT = 3,
     STAT_GEMM_N = 4, STAT_TRSM_N = 5, STAT_T0 = 6, STAT_TEND = 7, STAT_CTAS = 8,
+    // POTRF phases (ns summed over columns): block-column update, unblocked
+    // factor, W_J inverse (+ write-back), in-tile TRSM
+    STAT_PF_UPD = 9, STAT_PF_CHOL = 10, STAT_PF_INV = 11, STAT_PF_TRSM = 12,
     STAT_POTRF = 16  // + 3k: kernel start, wait done, end
 };
 int sched_ctas_per_sm();

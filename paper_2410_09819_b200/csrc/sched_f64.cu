@@ -606,7 +606,10 @@ __device__ void store_acc(double (&acc)[C::MI][C::NI][2], double* Ct, int64_t ld
 }
 }  // namespace
 
-// Factor the diagonal tile (the claim for column k is already held).
+// Factor the diagonal tile (the claim for column k is already held),
+// left-looking over its 128-column blocks J: update block column J with the
+// finished columns (one GEMM of K = 128 J per block), factor D_JJ unblocked,
+// form W_J = L_JJ^-1, then D[I,J] = D[I,J] W_J^T for I > J.
 // NT = 256: the dedicated kernel (W_J in shared memory, 128x128 DMMA blocks);
 // NT = 128: the scheduler-CTA fallback (77 KB budget: W_J through global
 // memory, 64x128 DMMA blocks in two row halves).  Returns false on a non-PD
@@ -623,8 +626,37 @@ __device__ bool potrf_tile_body(const SchedArgs& a, int64_t k, double* smem, int
     double* P = smem + (NT == 256 ? 0 : 128);
     double* R = P + PK;      // packed W_J, row-major lower (NT = 256 only)
     using G = typename std::conditional<NT == 256, PC, CC>::type;
+    uint64_t tp = (a.stats && t == 0) ? globaltimer() : 0;
+    auto phase = [&](int slot) {  // diagnostics: time since the last mark into stats[slot]
+        if (a.stats && t == 0) {
+            const uint64_t now = globaltimer();
+            atomicAdd(a.stats + slot, now - tp);
+            tp = now;
+        }
+    };
     for (int J = 0; J < S; ++J) {
         double* DJJ = D + (int64_t)J * 128 * (1 + nb);
+        // ---- left-looking update of block column J (one long-K GEMM per
+        //      block instead of J short trailing updates):
+        //      D[I,J] -= D[I,0:J] D[J,0:J]^T for I >= J
+        if (J > 0) {
+            for (int I = J; I < S; ++I)
+                for (int h = 0; h < 128 / G::BM; ++h) {
+                    double acc[G::MI][G::NI][2];
+                    zero_acc<G>(acc);
+                    const double* Ab = D + (int64_t)I * 128 + h * G::BM;
+                    const double* Bb = D + (int64_t)J * 128;
+                    auto src = [&](int it, const double*& pa, const double*& pb) {
+                        pa = Ab + (int64_t)it * BK * nb;
+                        pb = Bb + (int64_t)it * BK * nb;
+                    };
+                    gemm_mainloop<G>(acc, src, nb, nb, J * 128 / BK, smem);
+                    store_acc<G>(acc, D + (int64_t)I * 128 + h * G::BM + (int64_t)J * 128 * nb, nb, true);
+                    __threadfence_block();
+                    __syncthreads();
+                }
+        }
+        phase(STAT_PF_UPD);
         double* W = Wk + J * (128 * 128);
         for (int idx = t; idx < 128 * 128; idx += NT) {
             int c = idx >> 7, r = idx & 127;
@@ -632,12 +664,31 @@ __device__ bool potrf_tile_body(const SchedArgs& a, int64_t k, double* smem, int
         }
         if (t == 0) *s_flag = 0;
         __syncthreads();
-        // ---- unblocked right-looking Cholesky (kij); thread = (row, column parity)
-        const int i = t & 127, par = NT == 256 ? (t >> 7) : 0, step = NT == 256 ? 2 : 1;
+        // ---- unblocked left-looking (column) Cholesky of the packed block:
+        //      thread i computes L[i,j] = (D[i,j] - sum_{q<j} L[i,q] L[j,q]) / L[j,j]
+        //      (S:144 up to summation order); 2 barriers per column.
+        //      pidx_c(x, q) = off(q) + x with off(q+1) = off(q) + 127 - q.
         for (int j = 0; j < 128; ++j) {
-            if (t == 0) {
-                double d = P[pidx_c(j, j)];
-                if (!(d > 0.0)) {
+            double sv = 0.0;
+            if (t >= j && t < 128) {
+                double s0 = P[pidx_c(t, j)], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                int off = 0, q = 0;
+                for (; q + 3 < j; q += 4) {
+                    const int o1 = off + 127 - q, o2 = o1 + 126 - q, o3 = o2 + 125 - q;
+                    s0 -= P[off + t] * P[off + j];
+                    s1 -= P[o1 + t] * P[o1 + j];
+                    s2 -= P[o2 + t] * P[o2 + j];
+                    s3 -= P[o3 + t] * P[o3 + j];
+                    off = o3 + 124 - q;
+                }
+                for (; q < j; ++q) {
+                    s0 -= P[off + t] * P[off + j];
+                    off += 127 - q;
+                }
+                sv = (s0 + s1) + (s2 + s3);
+            }
+            if (t == j) {
+                if (!(sv > 0.0)) {
                     *s_flag = 1;
                     const int64_t info = k * nb + (int64_t)J * 128 + j + 1;
                     *(volatile int64_t*)a.dinfo = info;
@@ -645,45 +696,61 @@ __device__ bool potrf_tile_body(const SchedArgs& a, int64_t k, double* smem, int
                         if (a.peer_dinfo[q]) *(volatile int64_t*)a.peer_dinfo[q] = info;
                     __threadfence_system();
                 } else {
-                    P[pidx_c(j, j)] = sqrt(d);
+                    P[pidx_c(j, j)] = sqrt(sv);
                 }
             }
             __syncthreads();
             if (*s_flag) return false;
-            if (t > j && t < 128) P[pidx_c(t, j)] = P[pidx_c(t, j)] / P[pidx_c(j, j)];
-            __syncthreads();
-            if (i > j && t < 128 * step) {
-                const double lij = P[pidx_c(i, j)];
-                int c0 = j + 1;
-                if (step == 2 && (c0 & 1) != par) ++c0;
-                for (int c = c0; c <= i; c += step) P[pidx_c(i, c)] -= lij * P[pidx_c(c, j)];
-            }
+            if (t > j && t < 128) P[pidx_c(t, j)] = sv / P[pidx_c(j, j)];
             __syncthreads();
         }
-        // ---- W = L^-1 by forward substitution, one column per thread (t < 128)
-        if (t < 128) {
-            const int c = t;
-            for (int r = 0; r < 128; ++r) {
-                double s0 = (r == c) ? 1.0 : 0.0, s1 = 0.0;
-                int q = 0;
-                if (NT == 256) {
-                    for (; q + 1 < r; q += 2) {
-                        double w0 = (q >= c) ? R[pidx_r(q, c)] : 0.0;
-                        double w1 = (q + 1 >= c) ? R[pidx_r(q + 1, c)] : 0.0;
-                        s0 -= P[pidx_c(r, q)] * w0;
-                        s1 -= P[pidx_c(r, q + 1)] * w1;
-                    }
-                    if (q < r) s0 -= P[pidx_c(r, q)] * ((q >= c) ? R[pidx_r(q, c)] : 0.0);
-                    if (r >= c) R[pidx_r(r, c)] = (s0 + s1) / P[pidx_c(r, r)];
-                } else {
-                    for (q = c; q + 1 < r; q += 2) {  // own column of W, through L2
-                        s0 -= P[pidx_c(r, q)] * __ldcg(W + q + c * 128);
-                        s1 -= P[pidx_c(r, q + 1)] * __ldcg(W + q + 1 + c * 128);
-                    }
-                    if (q < r && q >= c) s0 -= P[pidx_c(r, q)] * __ldcg(W + q + c * 128);
-                    __stcg(W + r + c * 128, r >= c ? (s0 + s1) / P[pidx_c(r, r)] : 0.0);
+        phase(STAT_PF_CHOL);
+        // ---- W = L^-1 row by row: W[r,c] = (delta_rc - sum_{q<r} L[r,q] W[q,c]) / L[r,r]
+        //      (thread = column c, independent of the others; L[r,q] is a
+        //      broadcast, W[q,c] consecutive in c).
+        //      Dedicated kernel: W row-major packed in smem (R); fallback: row-major
+        //      in the global W block, transposed in place afterwards.
+        for (int r = 0; r < 128; ++r) {
+            if (t <= r) {
+                const int c = t;
+                double s0 = (r == c) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                int off = 0, q = 0;
+                auto wqc = [&](int qq) -> double {
+                    if (c > qq) return 0.0;
+                    if (NT == 256) return R[pidx_r(qq, c)];
+                    return __ldcg(W + qq * 128 + c);
+                };
+                for (; q + 3 < r; q += 4) {
+                    const int o1 = off + 127 - q, o2 = o1 + 126 - q, o3 = o2 + 125 - q;
+                    s0 -= P[off + r] * wqc(q);
+                    s1 -= P[o1 + r] * wqc(q + 1);
+                    s2 -= P[o2 + r] * wqc(q + 2);
+                    s3 -= P[o3 + r] * wqc(q + 3);
+                    off = o3 + 124 - q;
+                }
+                for (; q < r; ++q) {
+                    s0 -= P[off + r] * wqc(q);
+                    off += 127 - q;
+                }
+                const double v = ((s0 + s1) + (s2 + s3)) / P[pidx_c(r, r)];
+                if (NT == 256) R[pidx_r(r, c)] = v;
+                else __stcg(W + r * 128 + c, v);
+            } else if (NT != 256 && t < 128) {
+                __stcg(W + r * 128 + t, 0.0);  // strictly upper part of row r
+            }
+            // (no barrier: column c of W is read and written by thread c only)
+        }
+        __syncthreads();
+        if (NT != 256) {  // row-major -> column-major in place
+            for (int idx = t; idx < 128 * 128; idx += NT) {
+                const int r = idx >> 7, c = idx & 127;
+                if (r < c) {
+                    const double x = __ldcg(W + r * 128 + c), y = __ldcg(W + c * 128 + r);
+                    __stcg(W + r * 128 + c, y);
+                    __stcg(W + c * 128 + r, x);
                 }
             }
+            __threadfence_block();
         }
         __syncthreads();
         // ---- write L_JJ (zero upper) [and W_J, col-major, zero upper]
@@ -694,6 +761,7 @@ __device__ bool potrf_tile_body(const SchedArgs& a, int64_t k, double* smem, int
         }
         __threadfence_block();
         __syncthreads();
+        phase(STAT_PF_INV);
         // ---- TRSM of the blocks below: D[I,J] = D[I,J] W^T (the mainloop
         //      consumes all of D[I,J] before the epilogue overwrites it)
         for (int I = J + 1; I < S; ++I)
@@ -710,23 +778,7 @@ __device__ bool potrf_tile_body(const SchedArgs& a, int64_t k, double* smem, int
                 __threadfence_block();
                 __syncthreads();
             }
-        // ---- trailing update inside the tile
-        for (int Jp = J + 1; Jp < S; ++Jp)
-            for (int I = Jp; I < S; ++I)
-                for (int h = 0; h < 128 / G::BM; ++h) {
-                    double acc[G::MI][G::NI][2];
-                    zero_acc<G>(acc);
-                    const double* Ab = D + (int64_t)I * 128 + h * G::BM + (int64_t)J * 128 * nb;
-                    const double* Bb = D + (int64_t)Jp * 128 + (int64_t)J * 128 * nb;
-                    auto src = [&](int it, const double*& pa, const double*& pb) {
-                        pa = Ab + (int64_t)it * BK * nb;
-                        pb = Bb + (int64_t)it * BK * nb;
-                    };
-                    gemm_mainloop<G>(acc, src, nb, nb, 128 / BK, smem);
-                    store_acc<G>(acc, D + (int64_t)I * 128 + h * G::BM + (int64_t)Jp * 128 * nb, nb, true);
-                    __threadfence_block();
-                    __syncthreads();
-                }
+        phase(STAT_PF_TRSM);
     }
     return true;
 }

@@ -211,11 +211,16 @@ __device__ void block_gemm_img(double* C, int64_t ldc, const Src& src, int nstep
                     mma_tf32(tmem, make_desc(b0 + ko), make_desc(b0 + 2 * SUB_BYTES + ko), acc0);
                     if (m & 8u) mma_tf32(tmem, make_desc(b0 + ko), make_desc(b0 + 3 * SUB_BYTES + ko), 1u);
                     if (m & 2u) mma_tf32(tmem, make_desc(b0 + SUB_BYTES + ko), make_desc(b0 + 2 * SUB_BYTES + ko), 1u);
-                } else {
+                } else {  // K step 2st first, then 2st + 1 (the register-staged engine's order)
                     const uint32_t acc0 = (st > 0 || kg > 0) ? 1u : 0u;
                     mma_tf32(tmem, make_desc(b0 + ko), make_desc(b0 + 2 * SUB_BYTES + ko), acc0);
-                    if (m & 2u)
-                        mma_tf32(tmem, make_desc(b0 + SUB_BYTES + ko), make_desc(b0 + 3 * SUB_BYTES + ko), 1u);
+                }
+            }
+            if (!THREE && (m & 2u)) {
+#pragma unroll
+                for (int kg = 0; kg < KS / 8; ++kg) {
+                    const uint32_t ko = kg * KSTEP_BYTES;
+                    mma_tf32(tmem, make_desc(b0 + SUB_BYTES + ko), make_desc(b0 + 3 * SUB_BYTES + ko), 1u);
                 }
             }
             commit(&done[stage]);

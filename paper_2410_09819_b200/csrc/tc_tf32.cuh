@@ -130,13 +130,11 @@ __device__ __forceinline__ float rne_tf32(float x) {
     return __uint_as_float(b & 0xFFFFE000u);
 }
 
-// 3xTF32 split: x = hi + lo with hi = x rounded to tf32 (10 explicit bits)
+// 3xTF32 split: x = hi + lo, hi = RNE_tf32(x), lo = RNE_tf32(x - hi) (both
+// exact TF32 operands; the same split the operand images store)
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-    uint32_t b = __float_as_uint(x);
-    uint32_t h = (b + 0x1000u) & 0xFFFFE000u;  // round half up on the magnitude
-    hi = __uint_as_float(h);
-    if (!isfinite(hi)) hi = __uint_as_float(b & 0xFFFFE000u);
-    lo = x - hi;
+    hi = rne_tf32(x);
+    lo = rne_tf32(x - hi);
 }
 
 }  // namespace tc
