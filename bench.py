@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--no-mxp", action="store_true")
     ap.add_argument("--mxp-n", type=int, default=131072)
     ap.add_argument("--mxp-eps", type=float, nargs="*", default=[1e-8, 1e-5])
+    ap.add_argument("--no-ooc", action="store_true")
+    ap.add_argument("--ooc-n", type=int, default=98304)
+    ap.add_argument("--ooc-frac", type=float, default=0.65)
     return ap.parse_args()
 
 
@@ -381,7 +384,10 @@ def run_ours(args):
         import numpy as np
 
         import workloads as w
+        import gc
+        gc.collect()
         torch.cuda.empty_cache()
+        free_gb = torch.cuda.mem_get_info()[0] / 1e9
         nm, nbm, theta = args.mxp_n, args.nb, (1.0, 0.02627, 0.5)
         xy = w.matern_locations(nm, seed=1)
         xyd = torch.as_tensor(xy, device=dev).contiguous()
@@ -407,6 +413,7 @@ def run_ours(args):
             run.img_gb = pl.get("image_bytes") / 1e9
             pl.close()
             del pl
+            gc.collect()
             torch.cuda.empty_cache()
             return min(ts[1:] if len(ts) > 1 else ts), ld_
 
@@ -414,7 +421,8 @@ def run_ours(args):
         ll64 = -0.5 * nm * math.log(2 * math.pi) - 0.5 * ld64
         mxp = {"workload": f"C3: Matern nu=0.5 theta=(1, 0.02627, 0.5) (weak), n={nm}, nb={nbm}, Morton-sorted "
                            f"uniform locations (seed 1), tiles generated on the device inside the schedule",
-               "fp64": {"tflops": flops_m / t64 / 1e12, "ms": t64 * 1e3, "logdet": ld64}, "maps": {}}
+               "fp64": {"tflops": flops_m / t64 / 1e12, "ms": t64 * 1e3, "logdet": ld64}, "maps": {},
+               "device_free_gb_at_start": round(free_gb, 1)}
         for eps in args.mxp_eps:
             pmap, _ = m.precision_map_matern_device(xyd, nbm, eps, theta[0], theta[1])
             tm, ldm = run(pmap, 1 + max(1, args.steps // 3))
@@ -427,6 +435,67 @@ def run_ours(args):
                 "kl_eq3": ll64 - llm}
         mxp["note"] = ("value/units: TFLOP/s = (n^3/3)/t, t = factorization incl. fused generation; loglik at "
                        "y=0 vs the FP64 run of the same pipeline (G16); 1 warm-up + timed reps, best")
+
+    # Out of core (a5/a9; C4's mode at a size this box's host RAM holds): the
+    # host matrix streamed through a pool capped at ooc_frac of the lower
+    # triangle (dead-tile slot recycling) vs the same host-streaming call
+    # with every tile resident; plgsy FP64, nb as C2.
+    ooc = None
+    if not args.no_ooc and ws == 1:
+        import gc
+        no, nbo = args.ooc_n, args.nb
+        nto = -(-no // nbo)
+        lower = nto * (nto + 1) // 2 * nbo * nbo * 8
+        gc.collect()
+        torch.cuda.empty_cache()
+        Ah = torch.empty((no, no), dtype=torch.float64).pin_memory()
+
+        def fresh():
+            Ad = torch.empty((no, no), dtype=torch.float64, device=dev).T
+            m.generate_plgsy_device(Ad, seed=args.seed, stream=stream.cuda_stream)
+            Ah.copy_(Ad.T)
+            del Ad
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+
+        def run_ooc(cap):
+            ts, hb, db, slots = [], 0, 0, 0
+            for i in range(2):  # first call: warm-up (plan workspace, pinned stage)
+                fresh()
+                pl = m.Plan(no, nbo)
+                pl.set("device", dev_index)
+                if cap:
+                    pl.set("hbm_bytes_cap", cap)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                inf = pl.factor(Ah.T)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                assert inf == 0, inf
+                ts.append(e0.elapsed_time(e1) / 1e3)
+                hb, db, slots = pl.get("h2d_bytes"), pl.get("d2h_bytes"), pl.get("pool_slots")
+                pl.close()
+                del pl
+                gc.collect()
+                torch.cuda.empty_cache()
+            return ts[-1], hb, db, slots
+
+        t_in, hb_in, db_in, s_in = run_ooc(0)
+        cap = int(args.ooc_frac * lower)
+        t_oc, hb_oc, db_oc, s_oc = run_ooc(cap)
+        fl = no ** 3 / 3
+        ooc = {"workload": f"plgsy n={no} nb={nbo} FP64 from pinned host memory (mxp_chol_factor)",
+               "lower_triangle_gb": round(lower / 1e9, 2),
+               "in_core": {"tflops": fl / t_in / 1e12, "ms": t_in * 1e3, "pool_slots": s_in,
+                           "h2d_bytes": hb_in, "d2h_bytes": db_in},
+               "out_of_core": {"tflops": fl / t_oc / 1e12, "ms": t_oc * 1e3, "pool_slots": s_oc,
+                               "hbm_cap_gb": round(cap / 1e9, 2), "h2d_bytes": hb_oc, "d2h_bytes": db_oc},
+               "ooc_over_in_core": t_in / t_oc,
+               "note": "C4 (n=262144, 276 GB lower triangle) exceeds this box's 196 GB host RAM; the same "
+                       "streaming/recycling path is timed with the pool capped below the lower triangle"}
+        del Ah
+        gc.collect()
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -449,6 +518,7 @@ def run_ours(args):
             "gpu_launches": launches, "clocks": ck,
             "baselines": {"cusolver_potrf": cusolver},
             "mxp_c3": mxp,
+            "ooc": ooc,
             "sched": sched,
             "check": {"backward_error_probe": probe, "logdet": logdet},
             "kernels": kstats,

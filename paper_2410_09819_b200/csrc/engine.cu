@@ -277,7 +277,7 @@ void plan_images(mxp_plan_s* p) {
         if (cudaSetDevice(p->device) == cudaSuccess && cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
             const double pool = (double)sizeof(double) * p->nb * p->nb * T;
             // lower bound of the image bytes (each non-FP64 tile at least its own image)
-            if (pool + (double)need * img_bytes > 0.9 * ((double)fr + (double)p->ws_bytes)) images = false;
+            if (pool + (double)need * img_bytes > (double)fr + (double)p->ws_bytes - 2e9) images = false;
         }
         cudaGetLastError();
         cudaSetDevice(cur);
@@ -316,7 +316,7 @@ void plan_images(mxp_plan_s* p) {
         cudaGetDevice(&cur);
         if (cudaSetDevice(p->device) == cudaSuccess && cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
             const double pool = (double)sizeof(double) * p->nb * p->nb * T;
-            if (pool + (double)p->shadow_bytes > 0.9 * ((double)fr + (double)p->ws_bytes)) {
+            if (pool + (double)p->shadow_bytes > (double)fr + (double)p->ws_bytes - 2e9) {  // 2 GB headroom
                 p->img.assign(4 * T, -1);
                 p->shadow_bytes = 0;
                 for (int64_t t = 0; t < T; ++t) p->qtile[t] = p->map[t] != MXP_FP64 ? 1 : 0;
@@ -822,11 +822,62 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
         }
         CK(cudaGetLastError());
     }
-    if (host_mode && !gen) {
+    // The copy streams park on stream memory waits, and a stream's command
+    // queue is finite: an enqueue into a full queue blocks the calling host
+    // thread.  So each stream that can park is fed by its own host thread --
+    // a blocked H2D enqueue (waiting for a slot to die) must never keep the D2H
+    // writes or the peer pushes that make it die from being enqueued.
+    std::vector<std::thread> feeders;
+    std::vector<std::string> feeder_err;
+    std::mutex feeder_mu;
+    auto feed = [&](auto body) {
+        feeders.emplace_back([&, body] {
+            try {
+                if (cudaSetDevice(p->device) != cudaSuccess) throw CudaError{cudaErrorInvalidDevice};
+                body();
+            } catch (const CudaError& e) {
+                std::lock_guard<std::mutex> g(feeder_mu);
+                feeder_err.push_back(g_last_error.empty() ? cudaGetErrorString(e.e) : g_last_error);
+            }
+        });
+    };
+    auto join_all = [&] {
+        for (auto& th : feeders) th.join();
+        feeders.clear();
+    };
+    int64_t d2h_bytes = 0;  // (outlives the feeders: they are joined on every path)
+    if (p->nranks > 1) feed([&] { push_tiles(p, a); });
+    if (host_mode && !gen) try {
         // H2D in schedule (column) order; the GPU front-end publishes loaded[t]
         CK(cudaStreamWaitEvent(p->sH2D, p->ev_start, 0));
         CK(cudaStreamWaitEvent(p->sD2H, p->ev_start, 0));
         const int64_t nb = p->nb, n = p->n;
+        feed([&, nb, n] {
+            // D2H of each finished tile as soon as Ready(t) flips (lower triangle only);
+            // diagonal tiles go to a pinned stage and only their lower triangle is merged
+            for (int64_t k = 0; k < Nt; ++k)
+                for (int64_t m = k; m < Nt; ++m) {
+                    if (m % p->nranks != p->rank) continue;
+                    const int64_t t = tile_index(Nt, m, k);
+                    const int64_t rr = std::min(nb, n - m * nb), cr = std::min(nb, n - k * nb);
+                    if (g_wait32((CUstream)p->sD2H, (CUdeviceptr)(a.ready + t), (cuuint32_t)p->epoch,
+                                 CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+                        throw CudaError{cudaErrorUnknown};
+                    const double* src = p->pool + (size_t)p->slot_plan[t] * nb * nb;
+                    if (m != k) {
+                        CK(cudaMemcpy2DAsync(A_host + (size_t)k * nb * lda + (size_t)m * nb, sizeof(double) * lda, src,
+                                             sizeof(double) * nb, sizeof(double) * rr, cr, cudaMemcpyDeviceToHost, p->sD2H));
+                        d2h_bytes += (int64_t)(sizeof(double) * rr * cr);
+                    } else {
+                        CK(cudaMemcpyAsync(p->h_stage + (size_t)k * nb * nb, src, sizeof(double) * nb * nb,
+                                           cudaMemcpyDeviceToHost, p->sD2H));
+                        d2h_bytes += (int64_t)(sizeof(double) * nb * nb);
+                    }
+                    if (g_write32((CUstream)p->sD2H, (CUdeviceptr)(d2h_done + t), 1, CU_STREAM_WRITE_VALUE_DEFAULT) !=
+                        CUDA_SUCCESS)
+                        throw CudaError{cudaErrorUnknown};
+                }
+        });
         for (int64_t k = 0; k < Nt; ++k)
             for (int64_t m = k; m < Nt; ++m) {
                 if (m % p->nranks != p->rank) continue;  // peers stream their own rows
@@ -850,32 +901,17 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
                     throw CudaError{cudaErrorUnknown};
                 p->h2d += (int64_t)(sizeof(double) * rr * cr);
             }
-        // D2H of each finished tile as soon as Ready(t) flips (lower triangle only);
-        // diagonal tiles go to a pinned stage and only their lower triangle is merged
-        for (int64_t k = 0; k < Nt; ++k)
-            for (int64_t m = k; m < Nt; ++m) {
-                if (m % p->nranks != p->rank) continue;
-                const int64_t t = tile_index(Nt, m, k);
-                const int64_t rr = std::min(nb, n - m * nb), cr = std::min(nb, n - k * nb);
-                if (g_wait32((CUstream)p->sD2H, (CUdeviceptr)(a.ready + t), (cuuint32_t)p->epoch,
-                             CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
-                    throw CudaError{cudaErrorUnknown};
-                const double* src = p->pool + (size_t)p->slot_plan[t] * nb * nb;
-                if (m != k) {
-                    CK(cudaMemcpy2DAsync(A_host + (size_t)k * nb * lda + (size_t)m * nb, sizeof(double) * lda, src,
-                                         sizeof(double) * nb, sizeof(double) * rr, cr, cudaMemcpyDeviceToHost, p->sD2H));
-                    p->d2h += (int64_t)(sizeof(double) * rr * cr);
-                } else {
-                    CK(cudaMemcpyAsync(p->h_stage + (size_t)k * nb * nb, src, sizeof(double) * nb * nb,
-                                       cudaMemcpyDeviceToHost, p->sD2H));
-                    p->d2h += (int64_t)(sizeof(double) * nb * nb);
-                }
-                if (g_write32((CUstream)p->sD2H, (CUdeviceptr)(d2h_done + t), 1, CU_STREAM_WRITE_VALUE_DEFAULT) !=
-                    CUDA_SUCCESS)
-                    throw CudaError{cudaErrorUnknown};
-            }
+        join_all();
+        p->d2h += d2h_bytes;
+    } catch (...) {
+        join_all();
+        throw;
     }
-    if (p->nranks > 1) push_tiles(p, a);
+    join_all();
+    if (!feeder_err.empty()) {
+        g_last_error = "copy-stream feeder: " + feeder_err[0];
+        throw CudaError{cudaErrorUnknown};
+    }
     CK(cudaEventRecord(p->ev_done, p->sP));
     CK(cudaStreamWaitEvent(p->sU, p->ev_done, 0));
 }
