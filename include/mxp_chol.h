@@ -81,12 +81,25 @@ typedef enum mxp_attr {
                                      CUDA_DEVICE_MAX_CONNECTIONS >= 8 * nranks (set before CUDA starts) */
     MXP_ATTR_SM_FIRST = 10,       /* first SM of this plan's scheduler partition (ranks co-located on one GPU) */
     MXP_ATTR_SM_COUNT = 11,       /* SMs in the partition (0 = all) */
+    MXP_ATTR_FP64_ENGINE = 12,    /* GEMM/SYRK tasks of FP64 tiles:
+                                     0 (default) = FP64 tensor pipe (DMMA, mma.sync.m8n8k4.f64);
+                                     1 = Ozaki scheme I on the int8 tensor cores (tcgen05 kind::i8): every
+                                       off-diagonal tile is split once, exactly, into s int8 slices with a
+                                       power-of-two scale per row (7s - 1 bits), the s(s+1)/2 slice products
+                                       of weight >= 2^-7(s-1) are accumulated exactly in int32 TMEM, and the
+                                       levels are combined in fp64 after every tile of K (fp64 accumulation
+                                       across tiles).  In core, single rank; otherwise (or if the s bytes per
+                                       element of slice images do not fit in HBM) it behaves as 0 -- see
+                                       MXP_ATTR_FP64_ENGINE_USED.  Re-sizes the workspace. */
+    MXP_ATTR_OZ_SLICES = 13,      /* s for MXP_ATTR_FP64_ENGINE = 1, 1..8 (default 8: 55 bits per operand,
+                                     dropped products <= 2^-56 of the row maxima) */
     MXP_ATTR_GPU_LAUNCHES = 100,  /* (get only) kernels launched by the last factorization */
     MXP_ATTR_H2D_BYTES = 101,     /* (get only) host->device bytes moved by the last factorization */
     MXP_ATTR_D2H_BYTES = 102,     /* (get only) device->host bytes moved by the last factorization */
     MXP_ATTR_POOL_SLOTS = 103,    /* (get only) tile slots in the device pool */
     MXP_ATTR_NT = 104,            /* (get only) Nt = ceil(n/nb) */
-    MXP_ATTR_IMAGE_BYTES = 105    /* (get only) bytes of tcgen05 operand images in the workspace (0: none) */
+    MXP_ATTR_IMAGE_BYTES = 105,   /* (get only) bytes of tcgen05 operand images in the workspace (0: none) */
+    MXP_ATTR_FP64_ENGINE_USED = 106 /* (get only) FP64 engine the next factorization uses (0 DMMA, 1 Ozaki) */
 } mxp_attr_t;
 
 /*
@@ -180,6 +193,29 @@ int mxp_chol_tile_device_ptr(mxp_plan_t plan, int64_t i, int64_t j, double** ptr
  * Returns MXP_ESTATE if no factorization succeeded.
  */
 int mxp_chol_logdet(mxp_plan_t plan, double* logdet);
+
+/*
+ * mxp_chol_solve_lower -- forward substitution L z = y on the resident factor
+ * of the last successful factorization (the quadratic form of Eq. 1, P:172:
+ * y^T A^-1 y = ||z||^2).  y_dev: n doubles on the plan's
+ * device (read only); z_dev: n doubles (device, may be NULL); sumsq: ||z||^2
+ * on return (host, may be NULL).  For tiles stored below FP64 the solve uses
+ * their stored (dequantized) values.  Every lower tile is read once (HBM
+ * bound); sums run in a fixed order (bitwise reproducible).  Ordered on
+ * MXP_ATTR_STREAM; returns after the result is complete.  MXP_ESTATE if no
+ * factorization succeeded or the factor is not resident (out of core, several
+ * ranks).
+ */
+int mxp_chol_solve_lower(mxp_plan_t plan, const double* y_dev, double* z_dev, double* sumsq);
+
+/*
+ * mxp_chol_loglik -- Gaussian log-likelihood of Eq. 1,
+ *   l = -n/2 log(2 pi) - 1/2 log|A| - 1/2 y^T A^-1 y,
+ * with A the last factorized matrix (covariance) and y_dev n observations on
+ * the device (NULL: y = 0, the convention of the paper's Eq. 3 KL check).
+ * loglik: host double.  Errors as mxp_chol_solve_lower.
+ */
+int mxp_chol_loglik(mxp_plan_t plan, const double* y_dev, double* loglik);
 
 /*
  * mxp_precision_map_from_matrix_device -- the MxP planner: per-tile

@@ -15,8 +15,8 @@ _lock = threading.Lock()
 ATTR = {
     "device": 0, "stream": 1, "hbm_bytes_cap": 2, "splitk_tiles": 3, "lookahead": 4,
     "debug_sync": 5, "profile": 6, "tc_engine": 7, "rank": 8, "nranks": 9, "sm_first": 10,
-    "sm_count": 11, "gpu_launches": 100, "h2d_bytes": 101, "d2h_bytes": 102,
-    "pool_slots": 103, "nt": 104, "image_bytes": 105,
+    "sm_count": 11, "fp64_engine": 12, "oz_slices": 13, "gpu_launches": 100, "h2d_bytes": 101, "d2h_bytes": 102,
+    "pool_slots": 103, "nt": 104, "image_bytes": 105, "fp64_engine_used": 106,
 }
 
 # every symbol include/mxp_chol.h declares (tests check the library exports them)
@@ -26,7 +26,7 @@ EXPORTS = [
     "mxp_precision_map_from_matrix_device", "mxp_generate_plgsy_device", "mxp_generate_kms_device",
     "mxp_generate_matern_device", "mxp_chol_factor_matern", "mxp_precision_map_matern_device",
     "mxp_chol_get_factor_device", "mxp_chol_tile_device_ptr", "mxp_chol_ipc_handle", "mxp_chol_ipc_attach",
-    "mxp_chol_attach_peer_plan", "mxp_chol_describe",
+    "mxp_chol_attach_peer_plan", "mxp_chol_describe", "mxp_chol_solve_lower", "mxp_chol_loglik",
     "mxp_chol_plan_destroy", "mxp_host_alloc", "mxp_host_free", "mxp_strerror", "mxp_last_error",
     "mxp_chol_abi_version", "mxp_chol_kernel_stats", "mxp_chol_sched_diagnostics",
 ]
@@ -92,6 +92,8 @@ def lib():
         L.mxp_chol_describe.argtypes = [vp, i32, pi64]
         L.mxp_chol_tile_device_ptr.argtypes = [vp, i64, i64, ctypes.POINTER(vp)]
         L.mxp_chol_sched_diagnostics.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64), i64, pi64]
+        L.mxp_chol_solve_lower.argtypes = [vp, vp, vp, pd]
+        L.mxp_chol_loglik.argtypes = [vp, vp, pd]
         _lib = L
         return L
 
@@ -305,6 +307,29 @@ class Plan:
     def logdet(self) -> float:
         v = ctypes.c_double()
         _check("mxp_chol_logdet", lib().mxp_chol_logdet(self._h, ctypes.byref(v)))
+        return v.value
+
+    @staticmethod
+    def _dev_vec(y, n):
+        import torch
+        if not (isinstance(y, torch.Tensor) and y.is_cuda and y.dtype == torch.float64 and y.numel() == n
+                and y.is_contiguous()):
+            raise ValueError("y must be a contiguous float64 CUDA tensor of n elements")
+        return y.data_ptr()
+
+    def solve_lower(self, y, z=None) -> float:
+        """z = L^-1 y on the resident factor (device tensors); returns ||z||^2."""
+        q = ctypes.c_double()
+        zp = self._dev_vec(z, self.n) if z is not None else None
+        _check("mxp_chol_solve_lower",
+               lib().mxp_chol_solve_lower(self._h, self._dev_vec(y, self.n), zp, ctypes.byref(q)))
+        return q.value
+
+    def loglik(self, y=None) -> float:
+        """Eq. 1 log-likelihood of the last factorized covariance at y (device; None: y = 0)."""
+        v = ctypes.c_double()
+        yp = self._dev_vec(y, self.n) if y is not None else None
+        _check("mxp_chol_loglik", lib().mxp_chol_loglik(self._h, yp, ctypes.byref(v)))
         return v.value
 
 

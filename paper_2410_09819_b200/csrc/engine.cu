@@ -18,6 +18,7 @@
 
 #include "../../include/mxp_chol.h"
 #include "internal.h"
+#include "oz_i8.cuh"
 
 using namespace mxp;
 
@@ -100,6 +101,15 @@ struct mxp_plan_s {
     uint8_t* d_qtile = nullptr;
     long long* d_img = nullptr;
     uint8_t* d_shadow = nullptr;
+    // FP64 engine (MXP_ATTR_FP64_ENGINE): 0 DMMA, 1 Ozaki int8 on tcgen05 (in core);
+    // oz_on = the engine actually used by the current image plan
+    int fp64_engine = 0, oz_slices = 8;
+    bool oz_on = false;
+    std::vector<long long> oz_img;  // [T] byte offsets of the int8 slice images, -1 = none
+    long long* d_oz_img = nullptr;
+    double* d_solve = nullptr;      // forward-solve work vectors (r | z | scalars)
+    std::vector<int4> items2;       // GEMM list of k_tc (Ozaki mode)
+    cudaStream_t sT = 0;
     bool mxp = false;              // any tile below FP64
     uint8_t* d_prec = nullptr;
     unsigned long long* d_amax_x = nullptr;
@@ -184,11 +194,22 @@ bool block_needed(int64_t m, int64_t k, int64_t b, int64_t nb) {
 }
 
 // GEMM blocks of a tile: 64x128 DMMA blocks, or 128x128 tcgen05 blocks for
-// tiles computed below FP64 when the tensor-core engine is on.
+// tiles computed below FP64 when the tensor-core engine is on, or 128x64
+// int8-tensor-core blocks for FP64 tiles in the Ozaki mode.
 int64_t gemm_blocks(const mxp_plan_s* p, int64_t m, int64_t k) {
     const int64_t nb = p->nb;
     if (p->tc_engine && p->map[tile_index(p->Nt, m, k)] != MXP_FP64) return (nb / 128) * (nb / 128);
     return blocks_per_tile(nb);
+}
+// block b of tile (m,k) computed?  (strictly upper blocks of diagonal tiles are skipped)
+bool gemm_block_needed(const mxp_plan_s* p, int64_t m, int64_t k, int64_t b) {
+    const int64_t nb = p->nb;
+    if (m != k) return true;
+    if (p->oz_on) {  // 128x64 blocks: rows [128 bi, +128), cols [64 bj, +64)
+        const int64_t SR = nb / 128, bi = b % SR, bj = b / SR;
+        return (bi + 1) * 128 > bj * 64;
+    }
+    return block_needed(m, k, b, nb);
 }
 
 // chunks of column k: ceil((k-1)/KC) fixed-size chunks over [0, k-1), then {k-1}
@@ -208,6 +229,7 @@ void build_task_list(mxp_plan_s* p) {
     plan_images(p);
     const int64_t Nt = p->Nt, nb = p->nb, KC = p->splitk_tiles, NB = blocks_per_tile(nb);
     p->items.clear();
+    p->items2.clear();
     p->expected.assign(p->T, 0);
     auto owned = [&](int64_t m) { return m % p->nranks == p->rank; };
     auto gemm_col = [&](int64_t k, int64_t c0, int64_t c1) {
@@ -215,8 +237,10 @@ void build_task_list(mxp_plan_s* p) {
             for (int64_t m = k; m < Nt; ++m)
                 if (owned(m))
                 for (int64_t b = 0; b < gemm_blocks(p, m, k); ++b)
-                    if (block_needed(m, k, b, nb)) {
-                        p->items.push_back(make_int4(ITEM_GEMM, (int)m, (int)k, (int)((b << 16) | c)));
+                    if (gemm_block_needed(p, m, k, b)) {
+                        // Ozaki mode: all GEMMs on the tensor-core kernel's list
+                        (p->oz_on ? p->items2 : p->items)
+                            .push_back(make_int4(ITEM_GEMM, (int)m, (int)k, (int)((b << 16) | c)));
                         p->expected[tile_index(Nt, m, k)]++;
                     }
     };
@@ -259,11 +283,14 @@ void build_task_list(mxp_plan_s* p) {
 // is used instead (images would be sized by the whole lower triangle).
 int64_t pool_slots(const mxp_plan_s* p);
 void plan_images(mxp_plan_s* p) {
-    const long long key = (long long)p->tc_engine * 2 + (pool_slots(p) == p->T ? 1 : 0);
+    const long long key = ((((long long)p->oz_slices * 2 + p->fp64_engine) * 9 + p->nranks) * 3 + p->tc_engine) * 2 +
+                          (pool_slots(p) == p->T ? 1 : 0);
     if (key == p->img_key) return;
     p->img_key = key;
     const int64_t Nt = p->Nt, T = p->T;
     p->img.assign(4 * T, -1);
+    p->oz_img.assign(T, -1);
+    p->oz_on = false;
     p->qtile.assign(T, 0);
     p->shadow_bytes = 0;
     bool images = p->mxp && p->tc_engine == 1 && pool_slots(p) == T;
@@ -310,7 +337,42 @@ void plan_images(mxp_plan_s* p) {
                 }
             p->qtile[t] = (pt != MXP_FP64 || any) ? 1 : 0;
         }
-    if (images) {  // full size known now: re-check, else use the register-staged engine
+    // Ozaki mode (in core; tiles below FP64 need the image engine): every
+    // off-diagonal tile is an operand of the FP64 SYRK of its row's diagonal
+    // tile, so each gets an int8 slice image (s bytes per element + row scales)
+    if (p->fp64_engine == 1 && pool_slots(p) == T && p->nranks == 1 && (!p->mxp || images)) {
+        const long long ob = oz::image_bytes(p->oz_slices, p->nb);
+        const size_t before = p->shadow_bytes;
+        for (int64_t n = 0; n < Nt; ++n)
+            for (int64_t i = n + 1; i < Nt; ++i) {
+                const int64_t t = tile_index(Nt, i, n);
+                p->oz_img[t] = (long long)p->shadow_bytes;
+                p->shadow_bytes += ob;
+                p->qtile[t] = 1;
+            }
+        p->oz_on = true;
+        size_t fr = 0, tot = 0;
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (cudaSetDevice(p->device) == cudaSuccess && cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+            const double pool = (double)sizeof(double) * p->nb * p->nb * T;
+            if (pool + (double)p->shadow_bytes > (double)fr + (double)p->ws_bytes - 2e9) {  // does not fit: DMMA
+                p->oz_img.assign(T, -1);
+                p->shadow_bytes = before;
+                p->oz_on = false;
+                for (int64_t t = 0; t < T; ++t) p->qtile[t] = 0;
+                for (int64_t t = 0; t < T; ++t)
+                    if (p->map[t] != MXP_FP64) p->qtile[t] = 1;
+                for (int64_t t = 0; t < T; ++t)
+                    for (int e = 0; e < 4; ++e)
+                        if (p->img[4 * t + e] >= 0) p->qtile[t] = 1;
+                for (int64_t k = 0; k < Nt; ++k) p->qtile[tile_index(Nt, k, k)] = 0;
+            }
+        }
+        cudaGetLastError();
+        cudaSetDevice(cur);
+    }
+    if (images && !p->oz_on) {  // full size known now: re-check, else use the register-staged engine
         size_t fr = 0, tot = 0;
         int cur = 0;
         cudaGetDevice(&cur);
@@ -332,7 +394,7 @@ size_t list_bytes(const mxp_plan_s* p) {
     // count without building: GEMM tasks + TRSM tasks
     const int64_t Nt = p->Nt, nb = p->nb, NB = blocks_per_tile(nb);
     int64_t diag_blocks = 0;
-    for (int64_t b = 0; b < NB; ++b) diag_blocks += block_needed(0, 0, b, nb);
+    for (int64_t b = 0; b < NB; ++b) diag_blocks += gemm_block_needed(p, 0, 0, b);
     int64_t cnt = 0;
     for (int64_t k = 1; k < Nt; ++k) {
         int64_t per = diag_blocks;
@@ -347,7 +409,8 @@ size_t list_bytes(const mxp_plan_s* p) {
 }
 
 size_t flag_ints(const mxp_plan_s* p) {
-    return (size_t)(2 + 7 * p->T + p->T * blocks_per_tile(p->nb) + 2 * p->Nt);
+    // + per-SM claim words of k_sched in the Ozaki mode (256) + counter2 (last)
+    return (size_t)(2 + 7 * p->T + p->T * blocks_per_tile(p->nb) + 2 * p->Nt + 256 + 1);
 }
 
 // Tile slots of the device pool: every lower tile in core; with
@@ -407,7 +470,7 @@ bool plan_slots(mxp_plan_s* p, int64_t C) {
 
 struct Layout {
     size_t slot, prev, epoch, flags, flags_bytes, expected, items, wbuf, stats, prec, amax_x, amax_s, args, qtile, img,
-        shadow, pool, total;
+        ozimg, solve, shadow, pool, total;
 };
 
 Layout layout(const mxp_plan_s* p) {
@@ -443,6 +506,10 @@ Layout layout(const mxp_plan_s* p) {
     off += align_up((size_t)p->T, 256);
     L.img = off;
     off += align_up(sizeof(long long) * 4 * (size_t)p->T, 256);
+    L.ozimg = off;
+    off += align_up(sizeof(long long) * (size_t)p->T, 256);
+    L.solve = off;  // forward solve: r, z (Nt*nb each) + scalars
+    off += align_up(sizeof(double) * (2 * (size_t)p->Nt * p->nb + 8), 256);
     L.shadow = off;
     off += align_up(p->shadow_bytes, 1024);
     L.pool = off;
@@ -488,6 +555,8 @@ void bind_workspace(mxp_plan_s* p) {
     p->d_args = (SchedArgs*)(p->ws + L.args);
     p->d_qtile = (uint8_t*)(p->ws + L.qtile);
     p->d_img = (long long*)(p->ws + L.img);
+    p->d_oz_img = (long long*)(p->ws + L.ozimg);
+    p->d_solve = (double*)(p->ws + L.solve);
     p->d_shadow = (uint8_t*)(p->ws + L.shadow);
     p->d_amax_x = (unsigned long long*)(p->ws + L.flags + align_up(sizeof(int) * flag_ints(p), 8));
     p->pool = (double*)(p->ws + L.pool);
@@ -503,6 +572,7 @@ void ensure_streams(mxp_plan_s* p) {
     CK(cudaStreamCreateWithFlags(&p->sD2H, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&p->sAux, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&p->sPush, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithPriority(&p->sT, cudaStreamNonBlocking, lo));
     p->ev_panel.resize(p->Nt);
     p->ev_bulk.resize(p->Nt);
     for (int64_t k = 0; k < p->Nt; ++k) {
@@ -709,6 +779,10 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     if (!p->list_uploaded) {
         build_task_list(p);
         CK(cudaMemcpyAsync(p->d_items, p->items.data(), sizeof(int4) * p->items.size(), cudaMemcpyHostToDevice, s0));
+        if (!p->items2.empty())
+            CK(cudaMemcpyAsync(p->d_items + p->items.size(), p->items2.data(), sizeof(int4) * p->items2.size(),
+                               cudaMemcpyHostToDevice, s0));
+        CK(cudaMemcpyAsync(p->d_oz_img, p->oz_img.data(), sizeof(long long) * T, cudaMemcpyHostToDevice, s0));
         CK(cudaMemcpyAsync(p->d_expected, p->expected.data(), sizeof(int) * T, cudaMemcpyHostToDevice, s0));
         CK(cudaMemcpyAsync(p->d_prec, p->map.data(), (size_t)T, cudaMemcpyHostToDevice, s0));
         CK(cudaMemcpyAsync(p->d_qtile, p->qtile.data(), (size_t)T, cudaMemcpyHostToDevice, s0));
@@ -732,6 +806,7 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     CK(cudaEventRecord(p->ev_start, s0));
     CK(cudaStreamWaitEvent(p->sU, p->ev_start, 0));
     CK(cudaStreamWaitEvent(p->sP, p->ev_start, 0));
+    if (p->oz_on) CK(cudaStreamWaitEvent(p->sT, p->ev_start, 0));
 
     SchedArgs a{};
     a.pool = p->pool;
@@ -760,9 +835,15 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
         a.gen_range = gen->range;
         a.gen_nugget = gen->nugget;
     }
-    a.prec = p->mxp ? p->d_prec : nullptr;
+    a.prec = (p->mxp || p->oz_on) ? p->d_prec : nullptr;
+    a.oz_img = p->oz_on ? p->d_oz_img : nullptr;
+    a.oz_slices = p->oz_slices;
+    a.items2 = p->d_items + p->items.size();
+    a.nitems2 = (int)p->items2.size();
+    a.counter2 = p->d_flags + flag_ints(p) - 1;
+    a.sm_claim = a.counter2 - 256;
     a.qtile = p->d_qtile;
-    a.img = (p->mxp && p->shadow_bytes > 0) ? p->d_img : nullptr;
+    a.img = (p->mxp && p->shadow_bytes > 0) ? p->d_img : nullptr;  // (null when no fp32 image exists)
     a.shadow = p->d_shadow;
     a.tc_engine = p->tc_engine;
     a.amax_x = p->d_amax_x;
@@ -804,13 +885,36 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
         chain_flops += ((double)m * m + (double)m) * nb3;
         potrf_flops += nb3 / 3.0;
     }
-    {
+    if (!p->oz_on) {
         Prof pr(p, p->sU, MXP_KCLASS_CHAIN, chain_flops);
         p->h_args = a;
         CK(cudaMemcpyAsync(p->d_args, &p->h_args, sizeof(SchedArgs), cudaMemcpyHostToDevice, p->sU));
         launch_sched(a, p->d_args, p->mxp, occ * nsm, p->sU);
         ++p->launches;
         dbg(p, p->sU, "sched");
+    } else {
+        // Ozaki mode: the GEMM kernel (one CTA per SM, all TMEM) on sT beside
+        // one k_sched CTA per SM (TRSM / QUANT / PREP / POTRF fallback) on sU
+        double trsm_flops = 0.0;
+        for (int64_t m = p->rank; m < Nt; m += p->nranks) trsm_flops += (double)m * nb3;
+        p->h_args = a;
+        CK(cudaMemcpyAsync(p->d_args, &p->h_args, sizeof(SchedArgs), cudaMemcpyHostToDevice, p->sU));
+        CK(cudaEventRecord(p->ev_join, p->sU));
+        CK(cudaStreamWaitEvent(p->sT, p->ev_join, 0));
+        {
+            Prof pr(p, p->sT, MXP_KCLASS_CHAIN, chain_flops - trsm_flops);
+            launch_tc(p->d_args, nsm, p->sT);
+            ++p->launches;
+        }
+        {
+            Prof pr(p, p->sU, MXP_KCLASS_TRSM, trsm_flops);
+            launch_sched(a, p->d_args, true, nsm, p->sU);
+            ++p->launches;
+        }
+        dbg(p, p->sT, "tc");
+        dbg(p, p->sU, "sched");
+        CK(cudaEventRecord(p->ev_join, p->sT));
+        CK(cudaStreamWaitEvent(p->sU, p->ev_join, 0));
     }
     {
         Prof pr(p, p->sP, MXP_KCLASS_POTRF, potrf_flops, (Nt - p->rank + p->nranks - 1) / p->nranks);
@@ -1061,6 +1165,20 @@ int mxp_chol_plan_set(mxp_plan_t p, mxp_attr_t key, int64_t v) {
         if (v < 0) return -3;
         p->sm_count = (int)v;
         return MXP_OK;
+    case MXP_ATTR_FP64_ENGINE:
+    case MXP_ATTR_OZ_SLICES:
+        if (key == MXP_ATTR_FP64_ENGINE && (v < 0 || v > 1)) return -3;
+        if (key == MXP_ATTR_OZ_SLICES && (v < 1 || v > oz::MAX_S)) return -3;
+        if (p->ws && !p->ws_owned) return MXP_ESTATE;  // changes the task list / image sizes
+        if (p->ws_owned) {
+            cudaFree(p->ws);
+            p->ws = nullptr;
+            p->ws_owned = false;
+        }
+        if (key == MXP_ATTR_FP64_ENGINE) p->fp64_engine = (int)v;
+        else p->oz_slices = (int)v;
+        p->list_uploaded = false;
+        return MXP_OK;
     case MXP_ATTR_TC_ENGINE:
         if (v < 0 || v > 2) return -3;
         if (p->ws && !p->ws_owned) return MXP_ESTATE;  // changes the task list / image sizes
@@ -1106,6 +1224,9 @@ int mxp_chol_plan_get(mxp_plan_t p, mxp_attr_t key, int64_t* v) {
     case MXP_ATTR_DEBUG_SYNC: *v = p->debug_sync; return MXP_OK;
     case MXP_ATTR_PROFILE: *v = p->profile; return MXP_OK;
     case MXP_ATTR_TC_ENGINE: *v = p->tc_engine; return MXP_OK;
+    case MXP_ATTR_FP64_ENGINE: *v = p->fp64_engine; return MXP_OK;
+    case MXP_ATTR_OZ_SLICES: *v = p->oz_slices; return MXP_OK;
+    case MXP_ATTR_FP64_ENGINE_USED: plan_images(p); *v = p->oz_on ? 1 : 0; return MXP_OK;
     case MXP_ATTR_RANK: *v = p->rank; return MXP_OK;
     case MXP_ATTR_NRANKS: *v = p->nranks; return MXP_OK;
     case MXP_ATTR_SM_FIRST: *v = p->sm_first; return MXP_OK;
@@ -1534,6 +1655,7 @@ int mxp_chol_describe(mxp_plan_t p, int streaming, int64_t* counts) {
     p->list_uploaded = false;
     for (int i = 0; i < 6; ++i) counts[i] = 0;
     for (const int4& it : p->items) counts[it.x]++;
+    for (const int4& it : p->items2) counts[it.x]++;
     for (int64_t k = 0; k < p->Nt; ++k)
         for (int64_t m = k; m < p->Nt; ++m)
             if (m % p->nranks == p->rank) counts[5]++;
@@ -1642,6 +1764,52 @@ int mxp_chol_get_factor_device(mxp_plan_t p, double* L_dev, int64_t ldl) {
         return status_from_exception(e);
     }
     cudaSetDevice(cur);
+    return MXP_OK;
+}
+
+int mxp_chol_solve_lower(mxp_plan_t p, const double* y_dev, double* z_dev, double* sumsq) {
+    if (!p) return -1;
+    if (!y_dev) return -2;
+    if (!p->have_result) return MXP_ESTATE;
+    if (!p->pool || p->slot_plan.empty() || pool_slots(p) < p->T || p->nranks > 1) return MXP_ESTATE;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    try {
+        CK(cudaSetDevice(p->device));
+        const int64_t N = p->Nt * p->nb;
+        double* r = p->d_solve;
+        double* z = r + N;
+        double* sc = z + N;
+        cudaStream_t s = p->user_stream;
+        CK(cudaMemsetAsync(r, 0, sizeof(double) * N, s));
+        CK(cudaMemcpyAsync(r, y_dev, sizeof(double) * p->n, cudaMemcpyDeviceToDevice, s));
+        launch_forward_solve(p->pool, p->d_slot, p->d_wbuf, p->Nt, p->nb, r, z, s);
+        launch_sumsq(z, p->n, sc, s);
+        CK(cudaGetLastError());
+        if (z_dev) CK(cudaMemcpyAsync(z_dev, z, sizeof(double) * p->n, cudaMemcpyDeviceToDevice, s));
+        double h = 0.0;
+        CK(cudaMemcpyAsync(&h, sc, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (sumsq) *sumsq = h;
+    } catch (const CudaError& e) {
+        cudaSetDevice(cur);
+        return status_from_exception(e);
+    }
+    cudaSetDevice(cur);
+    return MXP_OK;
+}
+
+int mxp_chol_loglik(mxp_plan_t p, const double* y_dev, double* loglik) {
+    if (!p) return -1;
+    if (!loglik) return -3;
+    if (!p->have_result) return MXP_ESTATE;
+    double q = 0.0;
+    if (y_dev) {
+        const int st = mxp_chol_solve_lower(p, y_dev, nullptr, &q);
+        if (st != MXP_OK) return st;
+    }
+    // Eq. 1: l = -n/2 log(2 pi) - 1/2 log|Sigma| - 1/2 y^T Sigma^-1 y
+    *loglik = -0.5 * (double)p->n * 1.8378770664093454836 - 0.5 * p->logdet - 0.5 * q;
     return MXP_OK;
 }
 

@@ -68,6 +68,17 @@ struct SchedArgs {
     const long long* img;      // [4T] (nullptr: no images; register-staged engine)
     uint8_t* shadow;
     int reserved_sms;          // SMs (smid < this) left to the POTRF kernels
+    // FP64 tiles on the int8 tensor cores (Ozaki scheme, oz_i8.cuh; MXP_ATTR_FP64_ENGINE = 1):
+    // every GEMM task goes to a second list run by the tensor-core kernel k_tc
+    // (one CTA per SM, all of its TMEM); k_sched keeps TRSM / QUANT / PREP / POTRF.
+    const long long* oz_img;   // [T] byte offset of the tile's int8 slice image in `shadow` (-1: none);
+                               //     nullptr: the Ozaki engine is off
+    int oz_slices;             // s (slices per operand, 1..8)
+    const int4* items2;        // the GEMM task list of k_tc
+    int nitems2;
+    int* counter2;             // its ticket
+    int* sm_claim;             // [256] k_sched CTAs per SM in the Ozaki mode (extras leave at once,
+                               //       keeping room for the k_tc CTA of every SM)
     unsigned long long* stats; // optional diagnostics (MXP_ATTR_PROFILE): see STAT_*
 };
 // diagnostics layout (ns from %globaltimer, summed over CTAs)
@@ -85,7 +96,16 @@ void launch_input_quantize(double* pool, const int32_t* slot, const uint8_t* pre
                            unsigned long long* amax_x, double* amax_s, cudaStream_t s, int rank = 0,
                            int nranks = 1);
 void launch_sched(const SchedArgs& a, const SchedArgs* a_dev, bool mxp, int grid, cudaStream_t s);  // a_dev: device copy of a
+// tensor-core GEMM kernel of the Ozaki mode (one CTA per SM, beside k_sched)
+void launch_tc(const SchedArgs* a_dev, int grid, cudaStream_t s);
+int tc_ctas_per_sm();
 void launch_potrf_tile(const SchedArgs& a, int64_t k, cudaStream_t s);
+
+// ---- forward solve / log-likelihood (solve.cu) -----------
+// z = L^-1 r on the resident factor (r, z: Nt*nb, padded with zeros; r is consumed)
+void launch_forward_solve(const double* pool, const int32_t* slot, const double* wbuf, int64_t Nt, int64_t nb,
+                          double* r, double* z, cudaStream_t s);
+void launch_sumsq(const double* z, int64_t n, double* out, cudaStream_t s);
 
 // ---- layout / utility kernels --------------------------------------------
 // lda matrix <-> pool tiles (padding: zeros, 1 on the padded diagonal)

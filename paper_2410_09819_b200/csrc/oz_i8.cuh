@@ -1,0 +1,271 @@
+// oz_i8.cuh -- FP64 tile GEMM emulated on the int8 tensor cores (Ozaki scheme,
+// "scheme I": error-free splitting into integer slices), sm_100a tcgen05.
+//
+// B200's FP64 tensor pipe (DMMA, ~37 TF/s) is the bottleneck
+// of the FP64 tiles (all of C2, the FP64 share of the MxP maps), while its int8
+// tensor cores run ~60x faster.  An FP64 operand tile X (rows r, K = tile
+// columns) is split row by row, exactly, into s int8 slices:
+//
+//   E_r = exponent with max_c |X_rc| < 2^E_r          (frexp of the row max)
+//   y = X_rc 2^-E_r in (-1, 1);  d_1 = rint(64 y), rem = 64 y - d_1,
+//   d_t = rint(128 rem), rem = 128 rem - d_t   (t = 2..s)   -- all exact in fp64
+//   X_rc = 2^(E_r - 6) sum_t d_t 2^(-7(t-1))  +  O(2^(E_r - 7s))
+//
+// with |d_t| <= 64.  A product of two tiles is then a sum of int8 GEMMs with
+// exact int32 accumulation; pairs of equal weight (t + u = c) share one TMEM
+// accumulator ("level" c), and pairs below the s-th level are dropped
+// (t + u <= s + 1: s(s+1)/2 int8 GEMMs):
+//
+//   (A B^T)_rj ~= sA_r sB_j sum_{c=2}^{s+1} 2^(-7(c-2)) ACC_c[r][j],
+//   ACC_c = sum_{t+u=c} D^A_t D^B_u^T,   sA_r = 2^(EA_r - 6),  sB_j = 2^(EB_j - 6).
+//
+// Each tile of K carries its own row scales, so the levels are drained (int32
+// -> fp64, scaled) after every tile of K into an fp64 register accumulator:
+// the accumulation across tiles is FP64, as in a DGEMM.  s = 8 gives 55 bits
+// per operand (vs 53 for FP64); the dropped pairs weigh <= 2^-56 relative to the
+// row maxima.  |ACC_c| <= 8 * 64^2 * nb < 2^31 for nb <= 65536: no overflow.
+//
+// Block shape: 128 (M, rows of A) x 64 (N, rows of B).  s levels x 64 int32
+// columns live in TMEM (s <= 8 -> <= 512 columns: the whole TMEM of the SM;
+// one such CTA per SM).
+//
+// Operand image of a tile (written once by the tile's QUANT tasks): for slice
+// t (0-based), 128-row block rb, 32-column K chunk kc, a 4 KB chunk at
+//   ((t * (nb/128) + rb) * (nb/32) + kc) * 4096
+// holding 128 rows x 32 int8 in the canonical K-major SWIZZLE_32B layout
+// (8-row groups of 256 B, row r8 at r8*32, 16-byte half h at h ^ ((r8 >> 2) & 1));
+// after the s slices, nb doubles of row scales 2^(E_r - 6).  A B-operand
+// (64 rows) is one half of a chunk: rows [64h, 64h+64) = bytes [2048h, 2048h+2048).
+#pragma once
+#include <stdint.h>
+
+#include "tc_tf32.cuh"
+
+namespace mxp {
+namespace oz {
+
+constexpr int MAX_S = 8;
+constexpr int BM = 128, BN = 64, KB = 32;  // block rows / cols, K per stage (int8 elements = bytes)
+constexpr int CHUNK = BM * KB;             // 4096 B: one slice chunk of 128 rows x 32 K
+constexpr int CHUNK_B = BN * KB;           // 2048 B
+constexpr int STAGES = 3;
+constexpr int STAGE_BYTES = MAX_S * (CHUNK + CHUNK_B);  // 48 KB
+constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 128 + BN * 8;  // + align slack, mbarriers, B scales
+constexpr int TMEM_COLS = 512;
+
+__host__ __device__ constexpr int64_t image_bytes(int s, int64_t nb) {
+    return (((int64_t)s * nb * nb + 8 * nb) + 1023) / 1024 * 1024;
+}
+__host__ __device__ constexpr int64_t slice_stride(int64_t nb) { return nb * nb; }
+__host__ __device__ constexpr int64_t chunk_offset(int64_t nb, int t, int64_t rb, int64_t kc) {
+    return ((t * (nb / 128) + rb) * (nb / 32) + kc) * CHUNK;
+}
+// byte offset of element (row, k) inside a 128 x 32 chunk (row < 128, k < 32)
+__host__ __device__ __forceinline__ uint32_t sw32_offset(int row, int k) {
+    const int r8 = row & 7;
+    return (uint32_t)((row >> 3) * 256 + r8 * 32 + ((((k >> 4) ^ (r8 >> 2)) & 1) << 4) + (k & 15));
+}
+
+// smem descriptor: K-major, SWIZZLE_32B, 8-row groups 256 B apart (SBO), LBO unused (1)
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(256 >> 4) << 32;
+    d |= (uint64_t)1 << 46;  // version 1 (sm100)
+    d |= (uint64_t)6 << 61;  // SWIZZLE_32B
+    return d;
+}
+// instruction descriptor: D s32, A/B signed int8, both K-major, M = 128, N = 64
+constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// exact int32 -> fp64 on the FP64 pipe: 2^52 + 2^31 + x  minus the constant
+__device__ __forceinline__ double i2d(int x) {
+    return __hiloint2double(0x43300000, (int)((unsigned)x ^ 0x80000000u)) - 4503601774854144.0;
+}
+
+// ---------------------------------------------------------------- slicing
+// The s int8 digits of y = x * 2^-E in (-1, 1) (see the header comment).
+__device__ __forceinline__ void slice_digits(double y, int s, int (&d)[MAX_S]) {
+    double r = y * 64.0;
+#pragma unroll
+    for (int t = 0; t < MAX_S; ++t) {
+        if (t > 0) r *= 128.0;
+        const double q = rint(r);
+        d[t] = t < s ? (int)q : 0;
+        r -= q;
+    }
+}
+// 2^(E-6) for the row max m (E: m < 2^E, from frexp); m = 0 -> scale 1 (all digits 0)
+__device__ __forceinline__ double row_scale(double m, double& inv) {
+    if (!(m > 0.0) || !isfinite(m)) {
+        inv = 1.0;
+        return 1.0;
+    }
+    int e;
+    frexp(m, &e);  // m = f 2^e, f in [0.5, 1)  ->  |x| <= m < 2^e
+    inv = scalbn(1.0, -e);
+    return scalbn(1.0, e - 6);
+}
+
+// Slices of 16 consecutive columns [k0, k0 + 16) (k0 % 16 == 0) of row `row`
+// of a tile into its image (x: the 16 values; inv = 2^-E of the row).
+__device__ __forceinline__ void write_slices16(uint8_t* img, int64_t nb, int s, int row, int k0,
+                                               const double (&x)[16], double inv) {
+    uint32_t w[MAX_S][4];
+#pragma unroll
+    for (int t = 0; t < MAX_S; ++t) w[t][0] = w[t][1] = w[t][2] = w[t][3] = 0u;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        int d[MAX_S];
+        slice_digits(x[e] * inv, s, d);
+#pragma unroll
+        for (int t = 0; t < MAX_S; ++t) w[t][e >> 2] |= ((uint32_t)d[t] & 0xFFu) << (8 * (e & 3));
+    }
+    const int64_t rb = row >> 7, kc = k0 >> 5;
+    const uint32_t off = sw32_offset(row & 127, k0 & 31);
+#pragma unroll
+    for (int t = 0; t < MAX_S; ++t)
+        if (t < s)
+            __stcg(reinterpret_cast<uint4*>(img + chunk_offset(nb, t, rb, kc) + off),
+                   make_uint4(w[t][0], w[t][1], w[t][2], w[t][3]));
+}
+
+// ------------------------------------------------------------ block GEMM
+// One operand tile of the K walk: chunk (t = 0, kc = 0) of the A rows / B rows
+// of this block, the byte stride between slices, and the row scales.
+struct OzTile {
+    const uint8_t* a;   // A: image + chunk_offset(nb, 0, rbA, 0)
+    const uint8_t* b;   // B: image + chunk_offset(nb, 0, rbB, 0) + 2048 * half
+    const double* sa;   // 128 row scales of A's rows
+    const double* sb;   // 64 row scales of B's rows
+};
+
+// C(128 x 64, fp64, column-major ldc) -= sum over ntiles tiles of A_n B_n^T,
+// each tile of K = 32 * kt (kt = nb / 32) emulated with s slices.
+// smem: >= SMEM_BYTES dynamic shared memory; tmem: 512 allocated columns.
+// All 128 threads call; thread 0 issues the bulk copies and MMAs.
+template <class Src>
+__device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, int s, int kt, int64_t nb,
+                           uint8_t* smem, uint32_t tmem) {
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * STAGE_BYTES);
+    uint64_t* done = full + STAGES;
+    uint64_t* tbar = done + STAGES;
+    double* s_sb = reinterpret_cast<double*>(base + STAGES * STAGE_BYTES + 128);
+    const int tid = threadIdx.x;
+    const int G = ntiles * kt;  // K steps (32 each)
+    const int64_t sstride = slice_stride(nb);
+    if (tid == 0) {
+        for (int i = 0; i < STAGES; ++i) tc::mbar_init(full + i, 1), tc::mbar_init(done + i, 1);
+        tc::mbar_init(tbar, 1);
+        tc::fence_mbar_init();
+    }
+    __syncthreads();
+    // producer: copies of K step g into its stage
+    OzTile cur{};
+    int cur_i = -1;
+    auto issue = [&](int g) {
+        const int i = g / kt, kc = g - i * kt;
+        if (i != cur_i) cur = src(i), cur_i = i;
+        uint8_t* st = base + (g % STAGES) * STAGE_BYTES;
+        uint64_t* fb = full + (g % STAGES);
+        tc::mbar_expect_tx(fb, (uint32_t)(s * (CHUNK + CHUNK_B)));
+        for (int t = 0; t < s; ++t) {
+            tc::bulk_g2s(st + t * CHUNK, cur.a + t * sstride + (int64_t)kc * CHUNK, CHUNK, fb);
+            tc::bulk_g2s(st + MAX_S * CHUNK + t * CHUNK_B, cur.b + t * sstride + (int64_t)kc * CHUNK, CHUNK_B, fb);
+        }
+    };
+    if (tid == 0)
+        for (int g = 0; g < STAGES && g < G; ++g) issue(g);
+
+    double acc[BN];
+#pragma unroll
+    for (int j = 0; j < BN; ++j) acc[j] = 0.0;
+    const int warp = tid >> 5;
+    const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+
+    for (int i = 0; i < ntiles; ++i) {
+        if (tid == 0) {
+            for (int kc = 0; kc < kt; ++kc) {
+                const int g = i * kt + kc, stage = g % STAGES;
+                tc::mbar_wait(full + stage, (uint32_t)((g / STAGES) & 1));
+                tc::fence_after();
+                const uint32_t sa = tc::smem_u32(base + stage * STAGE_BYTES);
+                const uint32_t sb = sa + MAX_S * CHUNK;
+                for (int t = 0; t < s; ++t) {
+                    const uint64_t ad = make_desc(sa + t * CHUNK);
+                    for (int u = 0; u + t < s; ++u)  // level c = t + u (0-based) <= s - 1
+                        mma_i8(tmem + (uint32_t)((t + u) * BN), ad, make_desc(sb + u * CHUNK_B),
+                               (kc > 0 || t > 0) ? 1u : 0u);
+                }
+                tc::commit(done + stage);
+                // refill the previous step's stage once its MMAs have read it
+                // (this step's MMAs stay queued behind them meanwhile)
+                if (g >= 1 && g - 1 + STAGES < G) {
+                    const int pg = g - 1;
+                    tc::mbar_wait(done + (pg % STAGES), (uint32_t)((pg / STAGES) & 1));
+                    issue(pg + STAGES);
+                }
+            }
+            tc::commit(tbar);  // every MMA of tile i
+        }
+        __syncwarp();
+        // drain: ACC levels of tile i -> fp64, scaled by the row scales
+        if (tid < BN) s_sb[tid] = __ldcg(src(i).sb + tid);
+        const double sa_r = __ldcg(src(i).sa + tid);
+        tc::mbar_wait(tbar, (uint32_t)(i & 1));
+        tc::fence_after();
+        __syncthreads();  // s_sb visible
+#pragma unroll
+        for (int g4 = 0; g4 < BN / 16; ++g4) {
+            double v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = 0.0;
+            for (int c = s - 1; c >= 0; --c) {  // smallest weight first
+                int x[16];
+                tmem_ld16(tl + (uint32_t)(c * BN + g4 * 16), x);
+                tmem_wait_ld();
+                const double w = __longlong_as_double((long long)(1023 - 7 * c) << 52);  // 2^(-7c)
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = fma(i2d(x[j]), w, v[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[g4 * 16 + j] = fma(v[j] * sa_r, s_sb[g4 * 16 + j], acc[g4 * 16 + j]);
+        }
+        tc::fence_before();
+        __syncthreads();  // TMEM and s_sb free for tile i + 1
+    }
+#pragma unroll
+    for (int j = 0; j < BN; ++j) {
+        double* p = C + tid + (int64_t)j * ldc;
+        __stcg(p, __ldcg(p) - acc[j]);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int i = 0; i < STAGES; ++i) tc::mbar_inval(full + i), tc::mbar_inval(done + i);
+        tc::mbar_inval(tbar);
+    }
+}
+
+}  // namespace oz
+}  // namespace mxp

@@ -24,6 +24,7 @@
 #include "dmma_gemm.cuh"
 #include "quant.cuh"
 #include "tc_block.cuh"
+#include "oz_i8.cuh"
 
 namespace mxp {
 
@@ -441,16 +442,97 @@ __device__ __noinline__ bool task_gemm_img(const SchedArgs& a, int64_t m, int64_
     return true;
 }
 
+// FP64 GEMM task on the int8 tensor cores (Ozaki scheme, oz_i8.cuh; SURVEY
+// §8(f) N4): C(m,k)[128x64 block b] -= sum over the chunk of L(m,n) L(k,n)^T,
+// operands from the int8 slice images written by the QUANT tasks, levels
+// drained to fp64 after every tile of K.
+__device__ __noinline__ bool task_gemm_oz(const SchedArgs& a, int64_t m, int64_t k, int64_t b, int64_t c,
+                                          uint8_t* smem, uint32_t tmem, int* s_flag) {
+    const int64_t Nt = a.Nt, nb = a.nb, SR = nb / 128;
+    const int64_t bi = b % SR, bj = b / SR;  // 128-row block bi, 64-column block bj
+    const int64_t t = tile_index(Nt, m, k);
+    int64_t n0, n1;
+    chunk_range(k, c, a.KC, n0, n1);
+    int* chunk_flag = a.blk_chunk + t * a.NB + b;
+    uint64_t tw0 = 0;
+    if (threadIdx.x == 0) {
+        if (a.stats) tw0 = globaltimer();
+        bool ok = wait_input(a, t, k);
+        for (int64_t n = n0; n < n1 && ok; ++n)
+            ok = wait_flag(a.ready + tile_index(Nt, m, n), a.epoch, a, k) &&
+                 wait_flag(a.ready + tile_index(Nt, k, n), a.epoch, a, k);
+        if (ok) ok = wait_flag(chunk_flag, (int)c, a, k);
+        *s_flag = ok;
+        if (a.stats) {
+            uint64_t tw1 = globaltimer();
+            atomicAdd(a.stats + STAT_GEMM_WAIT, tw1 - tw0);
+            tw0 = tw1;
+        }
+    }
+    __syncthreads();
+    if (!*s_flag) return false;
+    const int s = a.oz_slices;
+    const int64_t sc_off = (int64_t)s * nb * nb;
+    auto src = [&](int i) {
+        const int64_t n = n0 + i;
+        const uint8_t* ia = a.shadow + a.oz_img[tile_index(Nt, m, n)];
+        const uint8_t* ib = a.shadow + a.oz_img[tile_index(Nt, k, n)];
+        oz::OzTile o;
+        o.a = ia + oz::chunk_offset(nb, 0, bi, 0);
+        o.b = ib + oz::chunk_offset(nb, 0, bj >> 1, 0) + 2048 * (bj & 1);
+        o.sa = reinterpret_cast<const double*>(ia + sc_off) + bi * 128;
+        o.sb = reinterpret_cast<const double*>(ib + sc_off) + bj * 64;
+        return o;
+    };
+    double* Ct = tile_ptr(a.pool, a.slot, Nt, nb, m, k) + bi * 128 + bj * 64 * nb;
+    oz::block_gemm(Ct, nb, src, (int)(n1 - n0), s, (int)(nb / 32), nb, smem, tmem);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        st_release(chunk_flag, (int)c + 1);
+        atom_add_release(a.gemm_done + t, 1);
+        if (a.stats) {
+            atomicAdd(a.stats + STAT_GEMM_BUSY, globaltimer() - tw0);
+            atomicAdd(a.stats + STAT_GEMM_N, 1ull);
+        }
+    }
+    return true;
+}
+
+// Int8 slice image of rows [64r, 64r+64) of a final tile (Ozaki operands):
+// per-row scale 2^(E-6) from the row max, then s digits per element.  Thread
+// (row = tid & 63, half = tid >> 6) covers half of the row's columns.
+__device__ void oz_slice_rows(const SchedArgs& a, const double* X, int64_t r, uint8_t* img, double* red) {
+    const int64_t nb = a.nb;
+    const int s = a.oz_slices;
+    const int tid = threadIdx.x, row = tid & 63, half = tid >> 6;
+    const int64_t c0 = half * (nb / 2), c1 = c0 + nb / 2;
+    double mx = 0.0;
+    for (int64_t cc = c0; cc < c1; ++cc) mx = fmax(mx, fabs(__ldcg(X + row + cc * nb)));
+    red[tid] = mx;
+    __syncthreads();
+    double inv;
+    const double sc = oz::row_scale(fmax(red[row], red[row + 64]), inv);
+    if (half == 0) reinterpret_cast<double*>(img + (int64_t)s * nb * nb)[r * 64 + row] = sc;
+    for (int64_t k0 = c0; k0 < c1; k0 += 16) {
+        double x[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) x[e] = __ldcg(X + row + (k0 + e) * nb);
+        oz::write_slices16(img, nb, s, (int)(r * 64 + row), (int)k0, x, inv);
+    }
+}
+
 // --------------------------------------------------------------- QUANT task
 // L_mk = deq(q_p(X)) on rows [64r, 64r+64) once every TRSM row task of the
 // tile has contributed to its amax (quantize once per task, after TRSM; O4).
-__device__ __noinline__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k, int64_t r, int* s_flag) {
+__device__ __noinline__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k, int64_t r, double* red,
+                                        int* s_flag) {
     const int64_t Nt = a.Nt, nb = a.nb;
     const int64_t t = tile_index(Nt, m, k);
     if (threadIdx.x == 0) *s_flag = wait_flag(a.trsm_done + t, (int)(nb / 64), a, k);
     __syncthreads();
     if (!*s_flag) return false;
-    const int p = a.prec[t];
+    const int p = a.prec ? a.prec[t] : P_FP64;
     const double amax = amax_of(a.amax_x + t);
     const double sc = tile_scale(p, amax), isc = 1.0 / sc;
     const double amax_st = quantize_value(p, amax, sc, isc);  // q is monotone: max|q(x)| = q(max|x|)
@@ -507,6 +589,11 @@ __device__ __noinline__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k
                 }
             }
         }
+    }
+    if (a.oz_img && a.oz_img[t] >= 0) {  // int8 slices of the stored values (FP64 GEMM operands)
+        __threadfence_block();
+        __syncthreads();
+        oz_slice_rows(a, X, r, a.shadow + a.oz_img[t], red);
     }
     __threadfence();
     __syncthreads();
@@ -856,13 +943,19 @@ __global__ void __launch_bounds__(CC::NT, 3) k_sched(const SchedArgs a_param, co
     static_assert(PAD * 8 >= 2 * sizeof(int), "scratch must fit in the padding");
     int& s_idx = *reinterpret_cast<int*>(smem + CC::BM);
     int& s_flag = *(reinterpret_cast<int*>(smem + CC::BM) + 1);
+    if (MXP && a.oz_img) {  // Ozaki mode: one k_sched CTA per SM (the k_tc CTA needs the rest of the SM)
+        if (threadIdx.x == 0) s_idx = atomicAdd(a.sm_claim + (id & 255), 1);
+        __syncthreads();
+        if (s_idx > 0) return;
+        __syncthreads();
+    }
     // tcgen05 state in the last 32 bytes (padding of the last B row of the DMMA
     // pipeline, never touched by it): two mbarriers + the TMEM base address.
     uint8_t* smem_b = reinterpret_cast<uint8_t*>(smem);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_b + CC::SMEM_BYTES - 32);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_b + CC::SMEM_BYTES - 16);
     uint32_t tmem = 0;
-    if (MXP && a.tc_engine) {  // MxP: this CTA owns 128 TMEM columns (3 CTAs x 128 <= 512 per SM)
+    if (MXP && a.tc_engine && !a.oz_img) {  // MxP: this CTA owns 128 TMEM columns (3 CTAs x 128 <= 512 per SM)
         if (threadIdx.x < 32) tc::tmem_alloc(tmem_slot, tc::TMEM_COLS);
         tc::fence_before();
         __syncthreads();
@@ -917,16 +1010,67 @@ __global__ void __launch_bounds__(CC::NT, 3) k_sched(const SchedArgs a_param, co
             } else if (it.x == ITEM_TRSM) {
                 task_trsm_ool(*ap, m, k, it.w, smem, &s_flag);
             } else {
-                task_quant(*ap, m, k, it.w, &s_flag);
+                task_quant(*ap, m, k, it.w, reinterpret_cast<double*>(smem) + 2048, &s_flag);
             }
         }
         __syncthreads();
     }
-    if (MXP && a.tc_engine) {
+    if (MXP && a.tc_engine && !a.oz_img) {
         tc::fence_before();
         __syncthreads();
         if (threadIdx.x < 32) tc::tmem_dealloc(tmem, tc::TMEM_COLS);
     }
+    if (a.stats && threadIdx.x == 0) atomicMax(a.stats + STAT_TEND, globaltimer());
+}
+
+// ------------------------------------------- tensor-core GEMM kernel (Ozaki mode)
+// MXP_ATTR_FP64_ENGINE = 1: every GEMM task of the schedule runs here -- FP64
+// outputs on the int8 tensor cores (task_gemm_oz), outputs below FP64 on the
+// tf32 operand-image engine -- one persistent CTA per SM owning all 512 TMEM
+// columns, co-resident with one k_sched CTA (TRSM / QUANT / PREP / POTRF
+// fallback) per SM.  Its list is the GEMM subsequence of the static schedule
+// (same order), so the ticket argument of k_sched carries over: every awaited
+// task precedes the waiting one in the global order, and each list is taken in
+// order by CTAs that are all resident.
+__global__ void __launch_bounds__(128, 1) k_tc(const SchedArgs* __restrict__ ap) {
+    const SchedArgs& a = *ap;
+    const int id = (int)smid();
+    if (id < a.sm_lo + a.reserved_sms || id >= a.sm_hi) return;
+    extern __shared__ __align__(1024) uint8_t smem_t[];
+    __shared__ int s_idx, s_flag;
+    __shared__ uint32_t tmem_slot;
+    if (threadIdx.x < 32) tc::tmem_alloc(&tmem_slot, oz::TMEM_COLS);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tmem_slot;
+    if (a.stats && threadIdx.x == 0) atomicMin(a.stats + STAT_T0, globaltimer());
+    while (true) {
+        if (threadIdx.x == 0) {
+            int i = atomicAdd(a.counter2, 1);
+            if (i >= a.nitems2) i = -1;
+            else if (skip_column(a, a.items2[i].z)) i = -2;
+            s_idx = i;
+        }
+        __syncthreads();
+        const int idx = s_idx;
+        __syncthreads();
+        if (idx == -1) break;
+        if (idx == -2) continue;
+        const int4 it = a.items2[idx];
+        const int64_t m = it.y, k = it.z;
+        const int cp = a.prec[tile_index(a.Nt, m, k)];
+        if (cp == P_FP64)
+            task_gemm_oz(a, m, k, it.w >> 16, it.w & 0xFFFF, smem_t, tmem, &s_flag);
+        else if (cp == P_FP32)
+            task_gemm_img<true>(a, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_t, tmem, &s_flag);
+        else
+            task_gemm_img<false>(a, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_t, tmem, &s_flag);
+        __syncthreads();
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) tc::tmem_dealloc(tmem, oz::TMEM_COLS);
     if (a.stats && threadIdx.x == 0) atomicMax(a.stats + STAT_TEND, globaltimer());
 }
 
@@ -1022,6 +1166,7 @@ void configure_sched() {
     cudaFuncSetAttribute(k_sched<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM_BYTES);
     cudaFuncSetAttribute(k_sched<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM_BYTES);
     cudaFuncSetAttribute(k_potrf_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF_SMEM);
+    cudaFuncSetAttribute(k_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, oz::SMEM_BYTES);
     done = true;
 }
 
@@ -1036,6 +1181,18 @@ void launch_sched(const SchedArgs& a, const SchedArgs* a_dev, bool mxp, int grid
     configure_sched();
     if (mxp) k_sched<true><<<grid, CC::NT, CC::SMEM_BYTES, s>>>(a, a_dev);
     else k_sched<false><<<grid, CC::NT, CC::SMEM_BYTES, s>>>(a, a_dev);
+}
+
+int tc_ctas_per_sm() {
+    int occ = 0;
+    configure_sched();
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tc, 128, oz::SMEM_BYTES);
+    return occ;
+}
+
+void launch_tc(const SchedArgs* a_dev, int grid, cudaStream_t s) {
+    configure_sched();
+    k_tc<<<grid, 128, oz::SMEM_BYTES, s>>>(a_dev);
 }
 
 void launch_potrf_tile(const SchedArgs& a, int64_t k, cudaStream_t s) {

@@ -1,0 +1,106 @@
+// solve.cu -- forward substitution L z = y on the resident tile factor and the
+// Gaussian log-likelihood (Eq. 1, the
+// quadratic form y^T Sigma^-1 y = ||z||^2 with L z = y).
+//
+// HBM-bound: every lower tile of L is read once (nb^2 * 8 bytes per tile,
+// n^2/2 * 8 bytes in all).  Tile column k: the diagonal solve
+// z_k = L_kk^-1 r_k (one CTA, blocked by 128 with the inverses W_J = L_JJ^-1
+// the POTRF left in wbuf), then r_m -= L_mk z_k for every m > k (one CTA per
+// 128-row block).  Every sum runs in a fixed order: the result is bitwise
+// reproducible.
+#include "internal.h"
+
+namespace mxp {
+namespace {
+
+// r[m*nb + rows] -= L(m,k)[rows, :] z_k  for m = k+1 .. Nt-1, 128-row blocks
+__global__ void __launch_bounds__(256) k_trsv_gemv(const double* __restrict__ pool, const int32_t* __restrict__ slot,
+                                                   int64_t Nt, int64_t nb, int64_t k, double* r,
+                                                   const double* __restrict__ z) {
+    extern __shared__ double sz[];  // z_k (nb) + 256 partial sums
+    double* part = sz + nb;
+    const int64_t RB = nb / 128;
+    const int64_t m = k + 1 + blockIdx.x / RB, rb = blockIdx.x % RB;
+    for (int64_t c = threadIdx.x; c < nb; c += blockDim.x) sz[c] = z[k * nb + c];
+    __syncthreads();
+    const int row = threadIdx.x & 127, h = threadIdx.x >> 7;
+    const double* L = pool + (int64_t)slot[tile_index(Nt, m, k)] * nb * nb + rb * 128 + row;
+    const int64_t c0 = h * (nb / 2), c1 = c0 + nb / 2;
+    double s0 = 0.0, s1 = 0.0;
+    for (int64_t c = c0; c < c1; c += 2) {
+        s0 = fma(__ldcs(L + c * nb), sz[c], s0);
+        s1 = fma(__ldcs(L + (c + 1) * nb), sz[c + 1], s1);
+    }
+    part[threadIdx.x] = s0 + s1;
+    __syncthreads();
+    if (h == 0) r[m * nb + rb * 128 + row] -= part[row] + part[row + 128];
+}
+
+// z_k = L_kk^-1 r_k: for J = 0..nb/128-1:  s = r_J - L[J, <J] z_<J;  z_J = W_J s
+__global__ void __launch_bounds__(256) k_trsv_diag(const double* __restrict__ pool, const int32_t* __restrict__ slot,
+                                                   const double* __restrict__ wbuf, int64_t Nt, int64_t nb,
+                                                   int64_t k, const double* __restrict__ r, double* z) {
+    extern __shared__ double sz[];  // z_k so far (nb) + s (128) + partials (256)
+    double* s = sz + nb;
+    double* part = s + 128;
+    const int row = threadIdx.x & 127, h = threadIdx.x >> 7;
+    const double* Lkk = pool + (int64_t)slot[tile_index(Nt, k, k)] * nb * nb;
+    const int64_t S = nb / 128;
+    for (int64_t J = 0; J < S; ++J) {
+        const double* LJ = Lkk + J * 128 + row;
+        const int64_t half = J * 64;  // columns [0, 128J) in two halves
+        double a0 = 0.0, a1 = 0.0;
+        for (int64_t c = h * half; c < (h + 1) * half; c += 2) {
+            a0 = fma(__ldcs(LJ + c * nb), sz[c], a0);
+            a1 = fma(__ldcs(LJ + (c + 1) * nb), sz[c + 1], a1);
+        }
+        part[threadIdx.x] = a0 + a1;
+        __syncthreads();
+        if (h == 0) s[row] = r[k * nb + J * 128 + row] - (part[row] + part[row + 128]);
+        __syncthreads();
+        const double* W = wbuf + (k * S + J) * (128 * 128);  // column-major, lower triangular
+        double b0 = 0.0;
+        const int kk0 = h == 0 ? 0 : (row + 1) / 2, kk1 = h == 0 ? (row + 1) / 2 : row + 1;
+        for (int kk = kk0; kk < kk1; ++kk) b0 = fma(W[row + kk * 128], s[kk], b0);
+        part[threadIdx.x] = b0;
+        __syncthreads();
+        if (h == 0) sz[J * 128 + row] = part[row] + part[row + 128];
+        __syncthreads();
+    }
+    for (int64_t c = threadIdx.x; c < nb; c += blockDim.x) z[k * nb + c] = sz[c];
+}
+
+// out = sum z_i^2 over i < n (fixed-order tree in one CTA)
+__global__ void __launch_bounds__(1024) k_sumsq(const double* __restrict__ z, int64_t n, double* out) {
+    __shared__ double red[1024];
+    double a = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a = fma(z[i], z[i], a);
+    red[threadIdx.x] = a;
+    __syncthreads();
+    for (int w = 512; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = red[0];
+}
+
+}  // namespace
+
+void launch_forward_solve(const double* pool, const int32_t* slot, const double* wbuf, int64_t Nt, int64_t nb,
+                          double* r, double* z, cudaStream_t s) {
+    const size_t sm_diag = sizeof(double) * (nb + 128 + 256), sm_gemv = sizeof(double) * (nb + 256);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_trsv_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_trsv_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        configured = true;
+    }
+    for (int64_t k = 0; k < Nt; ++k) {
+        k_trsv_diag<<<1, 256, sm_diag, s>>>(pool, slot, wbuf, Nt, nb, k, r, z);
+        if (k + 1 < Nt) k_trsv_gemv<<<(unsigned)((Nt - k - 1) * (nb / 128)), 256, sm_gemv, s>>>(pool, slot, Nt, nb, k, r, z);
+    }
+}
+
+void launch_sumsq(const double* z, int64_t n, double* out, cudaStream_t s) { k_sumsq<<<1, 1024, 0, s>>>(z, n, out); }
+
+}  // namespace mxp

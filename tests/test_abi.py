@@ -48,6 +48,8 @@ def test_library_is_sm100a(mxp):
     sass = os.popen(f"/usr/local/cuda/bin/cuobjdump -sass {mxp.lib_path()}").read()
     assert "DMMA.8x8x4" in sass  # FP64 tensor-pipe contraction in the chain kernels
     assert "LDGSTS" in sass     # cp.async operand staging
+    assert "UTCIMMA" in sass    # int8 tcgen05 MMA (Ozaki FP64 engine)
+    assert "UTCHMMA" in sass    # tf32 tcgen05 MMA (tiles below FP64)
 
 
 def test_argument_validation_without_gpu(mxp):

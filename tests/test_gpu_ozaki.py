@@ -1,0 +1,146 @@
+"""-m gpu parity of the FP64 tiles on the int8 tensor cores (Ozaki scheme I,
+MXP_ATTR_FP64_ENGINE = 1) vs the CPU oracle.
+
+The FP64 bar of BASELINE north_star applies unchanged: per-entry
+|L_gpu - L_oracle| <= 1e-10 ||L||_max, backward error <= 1e-13; bitwise on the
+integer-L0 inputs (small integers split exactly into slices and every product
+and sum is exact); MxP maps within G15 and as close as the tf32 engine."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as w
+from gpu_util import gpu_factor
+
+pytestmark = pytest.mark.gpu
+
+OZ = {"fp64_engine": 1}
+
+
+def _close(L, Lo, tol=1e-10):
+    err = np.max(np.abs(L - Lo))
+    assert err <= tol * np.max(np.abs(Lo)), err
+    return err
+
+
+def _check_used(plan):
+    assert plan.get("fp64_engine_used") == 1
+
+
+def test_ozaki_kms_closed_form():
+    n, nb, rho = 1024, 256, 0.5
+    A = w.kms(n, rho)
+    L, info, ld, plan = gpu_factor(A, nb, attrs=OZ)
+    _check_used(plan)
+    assert info == 0
+    Lo, _ = oracle.factor(A, nb)
+    _close(L, Lo)
+    closed = (n - 1) * math.log(1 - rho * rho)
+    assert abs(ld - closed) <= 1e-12 * abs(closed)
+    assert np.linalg.norm(A - L @ L.T) / np.linalg.norm(A) <= 1e-13
+
+
+@pytest.mark.parametrize("n,nb", [(2048, 256), (1536, 512), (1100, 128), (3072, 1024), (2900, 256)])
+def test_ozaki_plgsy_against_oracle(n, nb):
+    A = w.plgsy(n, seed=42)
+    L, info, ld, plan = gpu_factor(A, nb, attrs=OZ)
+    _check_used(plan)
+    assert info == 0
+    Lo, _ = oracle.factor(A, nb)
+    _close(L, Lo)
+    assert abs(ld - oracle.logdet(Lo)) <= 1e-12 * abs(ld)
+    assert np.linalg.norm(A - L @ L.T) / np.linalg.norm(A) <= 1e-13
+
+
+@pytest.mark.parametrize("rho", [0.9, 0.99])
+def test_ozaki_kms_ill_conditioned(rho):
+    n, nb = 2048, 256
+    A = w.kms(n, rho)
+    L, info, ld, _ = gpu_factor(A, nb, attrs=OZ)
+    Lo, _ = oracle.factor(A, nb)
+    assert info == 0
+    _close(L, Lo)
+    assert np.linalg.norm(A - L @ L.T) / np.linalg.norm(A) <= 1e-13
+
+
+def test_ozaki_matern_strong_correlation_fp64():
+    xy = w.matern_locations(2048, seed=1)
+    S = w.matern_cov(xy, 1.0, 0.210158)
+    L, info, ld, _ = gpu_factor(S, 256, attrs=OZ)
+    Lo, oinfo = oracle.factor(S, 256)
+    assert info == oinfo == 0
+    _close(L, Lo, 1e-9)  # the DMMA path's bar for this kappa ~ 1e5 input
+    assert abs(ld - oracle.logdet(Lo)) <= 1e-9 * abs(ld)
+    assert np.linalg.norm(S - L @ L.T) / np.linalg.norm(S) <= 1e-13
+
+
+@pytest.mark.parametrize("n,nb", [(1024, 128), (1024, 256), (2048, 512), (1000, 256)])
+def test_ozaki_integer_l0_bitwise(n, nb):
+    L0 = w.integer_l0(n, seed=n + nb)
+    A = w.spd_from_l0(L0)
+    L, info, ld, _ = gpu_factor(A, nb, attrs=OZ)
+    assert info == 0
+    assert np.array_equal(L, L0)
+
+
+@pytest.mark.parametrize("n,nb,j", [(1024, 256, 700), (1024, 128, 0), (1024, 256, 300)])
+def test_ozaki_not_pd_info(n, nb, j):
+    L0 = w.integer_l0(n, seed=5)
+    A = w.spd_from_l0(L0)
+    A[j, j] = -1.0 + np.sum(L0[j, :j] ** 2)
+    L, info, ld, _ = gpu_factor(A, nb, attrs=OZ)
+    _, oinfo = oracle.factor(A, nb)
+    assert info == oinfo == j + 1
+    kfail = j // nb
+    assert np.array_equal(L[:, : kfail * nb], L0[:, : kfail * nb])
+
+
+def test_ozaki_determinism_and_repeat():
+    A = w.plgsy(2048, seed=3)
+    L1, i1, ld1, plan = gpu_factor(A, 256, attrs=OZ)
+    L2, i2, ld2, _ = gpu_factor(A, 256, plan=plan)
+    assert i1 == i2 == 0
+    assert np.array_equal(L1, L2) and ld1 == ld2
+    L3, _, _, _ = gpu_factor(A, 256, attrs=dict(OZ, splitk_tiles=2))
+    _close(L3, L1, 1e-13)
+
+
+def test_ozaki_host_path_equals_device_path():
+    A = w.plgsy(2048, seed=9)
+    Ld, _, ldd, _ = gpu_factor(A, 256, attrs=OZ)
+    Lh, info, ldh, plan = gpu_factor(A, 256, attrs=OZ, host=True)
+    assert info == 0
+    assert np.array_equal(Ld, Lh) and ldd == ldh
+
+
+@pytest.mark.parametrize("s", [6, 7])
+def test_ozaki_fewer_slices_accuracy(s):
+    """s slices carry 7s-1 bits; the error scales accordingly (s=7: ~1e-14)."""
+    A = w.plgsy(2048, seed=42)
+    L, info, _, _ = gpu_factor(A, 256, attrs=dict(OZ, oz_slices=s))
+    assert info == 0
+    Lo, _ = oracle.factor(A, 256)
+    err = np.max(np.abs(L - Lo)) / np.max(np.abs(Lo))
+    assert err <= 2.0 ** (-7 * s + 10), err
+    assert np.linalg.norm(A - L @ L.T) / np.linalg.norm(A) <= 2.0 ** (-7 * s + 8)
+
+
+@pytest.mark.parametrize("eps", [1e-5, 1e-8])
+@pytest.mark.parametrize("n,nb", [(2048, 128), (1900, 256)])
+def test_ozaki_mxp_matern_against_oracle(n, nb, eps):
+    """MxP map with the FP64 tiles on the int8 tensor cores and the others on
+    the tf32 image engine (both in the k_tc kernel)."""
+    xy = w.matern_locations(n, seed=1)
+    S = w.matern_cov(xy, 1.0, 0.02627)
+    pmap = oracle.plan(S, nb, eps)
+    assert np.any(pmap != oracle.FP64)
+    L, info, ld, plan = gpu_factor(S, nb, pmap, attrs=OZ)
+    _check_used(plan)
+    Lo, oinfo = oracle.factor(S, nb, pmap)
+    assert info == oinfo == 0
+    err = np.max(np.abs(L - Lo))
+    assert err <= 1e-4 * np.max(np.abs(Lo)), err  # the tf32 engine's bar (fp32 accumulation)
+    Lt, _, ldt, _ = gpu_factor(S, nb, pmap, attrs={"tc_engine": 1})  # DMMA FP64 tiles, same images
+    assert abs(ld - ldt) <= 1e-9 * abs(ldt)
