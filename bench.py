@@ -62,6 +62,10 @@ def parse():
     ap.add_argument("--no-ooc", action="store_true")
     ap.add_argument("--ooc-n", type=int, default=98304)
     ap.add_argument("--ooc-frac", type=float, default=0.65)
+    ap.add_argument("--fp64-engine", default="dmma", choices=["dmma", "ozaki"],
+                    help="GEMM/SYRK engine of FP64 tiles: FP64 tensor pipe (DMMA) or Ozaki-I on int8 tcgen05")
+    ap.add_argument("--oz-slices", type=int, default=8)
+    ap.add_argument("--no-engine-compare", action="store_true")
     return ap.parse_args()
 
 
@@ -162,9 +166,20 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def load_traffic(nb):
-    """dram bytes per launch of the chain kernel from the committed ncu capture."""
-    path = os.path.join(ROOT, "profiles", "ncu_chain_latest.json")
+def int8_peak():
+    """Dense int8 tensor peak: MEASURED_PEAKS.json's bf16 dense figure x the nominal int8:bf16 ratio (2)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return 2.0 * pk["bf16_tflops"], ("2 x MEASURED_PEAKS.json bf16_tflops (burst, %.1f) -- B200 int8:bf16 "
+                                         "dense ratio 2 (4.5 POPS : 2.25 PFLOPS nominal)" % pk["bf16_tflops"])
+    except Exception:
+        return 4500.0, "nominal B200 dense int8 4.5 POPS (MEASURED_PEAKS.json absent)"
+
+
+def load_traffic(nb, engine="dmma"):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_tc_latest.json" if engine == "ozaki" else "ncu_chain_latest.json")
     try:
         with open(path) as f:
             d = json.load(f)
@@ -204,9 +219,13 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
         return t.item()
 
-    def new_plan(nn, nbb, pmap=None):
+    ENG = {"dmma": 0, "ozaki": 1}
+
+    def new_plan(nn, nbb, pmap=None, engine=None):
         pl = m.Plan(nn, nbb, pmap)
         pl.set("device", dev_index)
+        pl.set("fp64_engine", ENG[engine or args.fp64_engine])
+        pl.set("oz_slices", args.oz_slices)
         if ws > 1:
             pl.connect(rank, ws, sm_partition=coloc)  # row-cyclic ranks, IPC-mapped peer pools
         else:
@@ -272,6 +291,44 @@ def run_ours(args):
         for key in ("gemm_busy_ms", "gemm_wait_ms", "trsm_busy_ms", "trsm_wait_ms"):
             sched[key + "_per_cta"] = sched.pop(key) / max(sched["ctas"], 1)
 
+    engine_used = "ozaki" if plan.get("fp64_engine_used") == 1 else "dmma"
+
+    # the other FP64 engine on the same input (same step, fewer reps)
+    engines = {engine_used: {"tflops": value, "ms": t_step * 1e3, "backward_error_probe": probe,
+                             "logdet": logdet}}
+    if not args.no_engine_compare:
+        other = "dmma" if engine_used == "ozaki" else "ozaki"
+        pl2 = new_plan(n, nb, engine=other)
+        ts = []
+        for i in range(3):
+            B.copy_(A)
+            torch.cuda.synchronize()
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            inf = pl2.factor_device(B)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            assert inf == 0, inf
+            if i:
+                ts.append(allreduce(e0.elapsed_time(e1) / 1e3, "max"))
+        L2 = torch.tril(B)
+        x2 = torch.randn(n, 4, dtype=torch.float64, device=dev, generator=torch.Generator(device=dev).manual_seed(7))
+        pr2 = ((A @ x2 - L2 @ (L2.T @ x2)).norm() / (torch.linalg.matrix_norm(A) * x2.norm())).item()
+        del L2, x2
+        used2 = "ozaki" if pl2.get("fp64_engine_used") == 1 else "dmma"
+        engines[used2] = {"tflops": flops / min(ts) / 1e12, "ms": min(ts) * 1e3, "backward_error_probe": pr2,
+                          "logdet": pl2.logdet()}
+        pl2.close()
+        del pl2
+        torch.cuda.empty_cache()
+    if "ozaki" in engines:
+        engines["ozaki"]["slices"] = args.oz_slices
+        engines["ozaki"]["what"] = ("Ozaki scheme I: FP64 tiles split exactly into int8 slices (row scales), "
+                                    "s(s+1)/2 int8 tcgen05 GEMMs per tile product, exact int32 TMEM "
+                                    "accumulation, fp64 combination per tile of K")
+
     # live FP64 peak: cuBLAS DGEMM on this box (MEASURED_PEAKS.json has no fp64 figure)
     d = 8192
     Xa = torch.randn(d, d, dtype=torch.float64, device=dev)
@@ -292,8 +349,23 @@ def run_ours(args):
 
     chain = stats_acc.get("chain", [0, 0.0, 0.0])
     achieved = chain[2] / (chain[1] / 1e3) / 1e12 if chain[1] > 0 else None
-    traffic, tinfo = load_traffic(nb)
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": dgemm_peak, "unit": "TFLOP/s",
+    traffic, tinfo = load_traffic(nb, engine_used)
+    if engine_used == "ozaki":
+        npairs = args.oz_slices * (args.oz_slices + 1) // 2
+        i8_peak, i8_how = int8_peak()
+        roofline = {"bound": "tensor", "achieved": achieved * npairs if achieved else None, "peak": i8_peak,
+                    "unit": "TOPS (int8)", "frac": achieved * npairs / i8_peak if achieved else None,
+                    "traffic": traffic, "fp64_equivalent_tflops": achieved,
+                    "kernel": "k_tc (persistent tensor-core kernel: all GEMM/SYRK tasks, FP64 tiles as "
+                              f"{npairs} int8 tcgen05 GEMMs each (Ozaki I, s={args.oz_slices}))",
+                    "achieved_how": "algorithmic GEMM/SYRK flops of k_tc (n^3/3 - Nt nb^3/3 - TRSM flops) x "
+                                    f"{npairs} int8 products per FP64 multiply-add / its CUDA-event duration on "
+                                    "its stream, summed over the timed steps",
+                    "peak_how": i8_how,
+                    "traffic_how": "dram__bytes_read.sum+dram__bytes_write.sum of one captured k_tc launch "
+                                   "(profiles/ncu_tc_latest.json)" if traffic else None,
+                    "fp64_dgemm_peak_live": None}
+    roofline = roofline if engine_used == "ozaki" else {"bound": "tensor", "achieved": achieved, "peak": dgemm_peak, "unit": "TFLOP/s",
                 "frac": achieved / dgemm_peak if achieved else None, "traffic": traffic,
                 "kernel": "k_sched (persistent static-schedule kernel: FP64 DMMA GEMM/SYRK + TRSM tasks, "
                           "all flops but the diagonal POTRFs)",
@@ -303,6 +375,8 @@ def run_ours(args):
                             "MEASURED_PEAKS.json has no fp64 figure)",
                 "traffic_how": "dram__bytes_read.sum+dram__bytes_write.sum of one captured k_sched launch "
                                "(profiles/ncu_chain_latest.json)" if traffic else None}
+    if engine_used == "ozaki":
+        roofline["fp64_dgemm_peak_live"] = dgemm_peak
     kstats = {k: {"launches": v[0], "ms": v[1], "tflops": (v[2] / (v[1] / 1e3) / 1e12) if v[1] > 0 and v[2] > 0
                   else None} for k, v in stats_acc.items()}
 
@@ -391,6 +465,7 @@ def run_ours(args):
         nm, nbm, theta = args.mxp_n, args.nb, (1.0, 0.02627, 0.5)
         xy = w.matern_locations(nm, seed=1)
         xyd = torch.as_tensor(xy, device=dev).contiguous()
+        yd = torch.randn(nm, dtype=torch.float64, device=dev, generator=torch.Generator(device=dev).manual_seed(3))
         flops_m = nm ** 3 / 3
 
         def run(pmap, reps):
@@ -409,6 +484,17 @@ def run_ours(args):
                 assert inf == 0, inf
                 ts.append(allreduce(e0.elapsed_time(e1) / 1e3, "max"))
             ld_ = pl.logdet()
+            # N1: Eq. 1 log-likelihood at a seeded y (forward solve on the resident factor)
+            run.ll_y = None
+            if ws == 1:
+                torch.cuda.synchronize()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                run.ll_y = pl.loglik(yd)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                run.solve_ms = e0.elapsed_time(e1)
             run.ws_gb = pl.workspace_size() / 1e9
             run.img_gb = pl.get("image_bytes") / 1e9
             pl.close()
@@ -419,9 +505,18 @@ def run_ours(args):
 
         t64, ld64 = run(None, 1 + max(1, args.steps // 3))
         ll64 = -0.5 * nm * math.log(2 * math.pi) - 0.5 * ld64
+        ll64_y = run.ll_y
+        if ll64_y is not None:
+            lower_bytes = (nm // nbm) * (nm // nbm + 1) // 2 * nbm * nbm * 8
+            mxp["fp64"]["loglik_y"] = ll64_y
+            mxp["fp64"]["forward_solve"] = {
+                "ms": run.solve_ms, "gbs": lower_bytes / (run.solve_ms / 1e3) / 1e9,
+                "how": "mxp_chol_loglik(y): forward solve L z = y (every lower tile read once) + ||z||^2, "
+                       "CUDA events; GB/s = lower-triangle bytes / time (HBM roofline: MEASURED_PEAKS hbm_gbs)"}
         mxp = {"workload": f"C3: Matern nu=0.5 theta=(1, 0.02627, 0.5) (weak), n={nm}, nb={nbm}, Morton-sorted "
                            f"uniform locations (seed 1), tiles generated on the device inside the schedule",
                "fp64": {"tflops": flops_m / t64 / 1e12, "ms": t64 * 1e3, "logdet": ld64}, "maps": {},
+               "fp64_engine": args.fp64_engine,
                "device_free_gb_at_start": round(free_gb, 1)}
         for eps in args.mxp_eps:
             pmap, _ = m.precision_map_matern_device(xyd, nbm, eps, theta[0], theta[1])
@@ -432,6 +527,7 @@ def run_ours(args):
                 "workspace_gb": round(run.ws_gb, 2), "operand_images_gb": round(run.img_gb, 2),
                 "tile_fractions_fp64_fp32_fp16_fp8": [round(float(np.mean(pmap == c)), 4) for c in range(4)],
                 "loglik_y0_rel_err": abs(llm - ll64) / abs(ll64), "logdet_abs_diff": abs(ldm - ld64),
+                "loglik_y_rel_err": (abs(run.ll_y - ll64_y) / abs(ll64_y)) if ll64_y is not None else None,
                 "kl_eq3": ll64 - llm}
         mxp["note"] = ("value/units: TFLOP/s = (n^3/3)/t, t = factorization incl. fused generation; loglik at "
                        "y=0 vs the FP64 run of the same pipeline (G16); 1 warm-up + timed reps, best")
@@ -506,9 +602,12 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if engine_used == "dmma" else "f64 (Ozaki-I: int8 tcgen05 slice products, int32/fp64 accumulation)",
+            "data": "synthetic",
             "config": {"workload": f"C2: plgsy random SPD n={n} nb={nb} FP64 in-core on B200, "
                                    f"device-resident input", "n": n, "nb": nb, "seed": args.seed,
+                       "fp64_engine": engine_used,
                        "l2": "inputs (n^2*8 B = %.1f GB) larger than L2 (126 MB); no flush" % (n * n * 8 / 1e9),
                        "parallelism": "single GPU" if ws == 1 else
                        f"row-cyclic over {ws} ranks (tile row m on rank m mod {ws}); finished tiles pushed "
@@ -521,6 +620,7 @@ def run_ours(args):
             "ooc": ooc,
             "sched": sched,
             "check": {"backward_error_probe": probe, "logdet": logdet},
+            "fp64_engines": engines,
             "kernels": kstats,
         }
         print(json.dumps(line), flush=True)

@@ -91,7 +91,7 @@ typedef enum mxp_attr {
                                        across tiles).  In core, single rank; otherwise (or if the s bytes per
                                        element of slice images do not fit in HBM) it behaves as 0 -- see
                                        MXP_ATTR_FP64_ENGINE_USED.  Re-sizes the workspace. */
-    MXP_ATTR_OZ_SLICES = 13,      /* s for MXP_ATTR_FP64_ENGINE = 1, 1..8 (default 8: 55 bits per operand,
+    MXP_ATTR_OZ_SLICES = 13,      /* s for MXP_ATTR_FP64_ENGINE = 1, 4..8 (default 8: 55 bits per operand,
                                      dropped products <= 2^-56 of the row maxima) */
     MXP_ATTR_GPU_LAUNCHES = 100,  /* (get only) kernels launched by the last factorization */
     MXP_ATTR_H2D_BYTES = 101,     /* (get only) host->device bytes moved by the last factorization */

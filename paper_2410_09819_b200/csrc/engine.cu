@@ -409,8 +409,8 @@ size_t list_bytes(const mxp_plan_s* p) {
 }
 
 size_t flag_ints(const mxp_plan_s* p) {
-    // + per-SM claim words of k_sched in the Ozaki mode (256) + counter2 (last)
-    return (size_t)(2 + 7 * p->T + p->T * blocks_per_tile(p->nb) + 2 * p->Nt + 256 + 1);
+    // + timeout diagnostics (8) + per-SM claim words of k_sched in the Ozaki mode (256) + counter2 (last)
+    return (size_t)(2 + 7 * p->T + p->T * blocks_per_tile(p->nb) + 2 * p->Nt + 8 + 256 + 1);
 }
 
 // Tile slots of the device pool: every lower tile in core; with
@@ -769,6 +769,37 @@ struct GenSource {  // fused on-device generation of the input tiles (N2)
     double sigma2 = 1.0, range = 1.0, nugget = 0.0;
 };
 
+// what the first timed-out wait of the static schedule was waiting for
+std::string sched_timeout_detail(mxp_plan_s* p) {
+    const size_t nf = flag_ints(p);
+    std::vector<int> f(nf);
+    if (cudaMemcpy(f.data(), p->d_flags, sizeof(int) * nf, cudaMemcpyDeviceToHost) != cudaSuccess) {
+        cudaGetLastError();
+        return "";
+    }
+    const int* d = f.data() + nf - 1 - 256 - 8;
+    if (!d[7]) return "";
+    const int64_t T = p->T, NB = blocks_per_tile(p->nb);
+    int64_t o = d[0];
+    static const char* names[] = {"ready", "gemm_done", "trsm_done", "quant_done", "loaded", "prep_done"};
+    std::string what;
+    if (o >= 0 && o < 6 * T) {
+        int64_t t = o % T, m = 0, n = 0;
+        tile_coords(p->Nt, t, m, n);
+        what = std::string(names[o / T]) + "(" + std::to_string(m) + "," + std::to_string(n) + ")";
+    } else if (o >= 6 * T && o < 6 * T + T * NB) {
+        int64_t t = (o - 6 * T) / NB, b = (o - 6 * T) % NB, m = 0, n = 0;
+        tile_coords(p->Nt, t, m, n);
+        what = "blk_chunk(" + std::to_string(m) + "," + std::to_string(n) + ") block " + std::to_string(b);
+    } else {
+        what = "flag offset " + std::to_string(o);
+    }
+    return " [first timeout: " + what + " target " + std::to_string(d[1]) + " value " + std::to_string(d[2]) +
+           " column " + std::to_string(d[6]) + " sm " + std::to_string(d[3]) + " block " + std::to_string(d[4]) + "/" +
+           std::to_string(d[5]) + "; tickets k_sched " + std::to_string(f[0]) + "/" + std::to_string(p->items.size()) +
+           " k_tc " + std::to_string(f[nf - 1]) + "/" + std::to_string(p->items2.size()) + "]";
+}
+
 void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A_host = nullptr,
                        int64_t lda = 0, const GenSource* gen = nullptr) {
     const int64_t Nt = p->Nt, T = p->T;
@@ -842,6 +873,7 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     a.nitems2 = (int)p->items2.size();
     a.counter2 = p->d_flags + flag_ints(p) - 1;
     a.sm_claim = a.counter2 - 256;
+    a.tdiag = a.sm_claim - 8;
     a.qtile = p->d_qtile;
     a.img = (p->mxp && p->shadow_bytes > 0) ? p->d_img : nullptr;  // (null when no fp32 image exists)
     a.shadow = p->d_shadow;
@@ -1168,7 +1200,7 @@ int mxp_chol_plan_set(mxp_plan_t p, mxp_attr_t key, int64_t v) {
     case MXP_ATTR_FP64_ENGINE:
     case MXP_ATTR_OZ_SLICES:
         if (key == MXP_ATTR_FP64_ENGINE && (v < 0 || v > 1)) return -3;
-        if (key == MXP_ATTR_OZ_SLICES && (v < 1 || v > oz::MAX_S)) return -3;
+        if (key == MXP_ATTR_OZ_SLICES && (v < oz::MIN_S || v > oz::MAX_S)) return -3;
         if (p->ws && !p->ws_owned) return MXP_ESTATE;  // changes the task list / image sizes
         if (p->ws_owned) {
             cudaFree(p->ws);
@@ -1325,7 +1357,7 @@ int mxp_chol_factor_device(mxp_plan_t p, double* A, int64_t lda, int64_t* info) 
         CK(cudaMemcpyAsync(&herr, p->d_flags + 1, sizeof(int), cudaMemcpyDeviceToHost, s0));
         CK(cudaStreamSynchronize(s0));
         if (herr) {
-            g_last_error = "static schedule: a Ready-table wait timed out (scheduler error)";
+            g_last_error = "static schedule: a Ready-table wait timed out (scheduler error)" + sched_timeout_detail(p);
             throw CudaError{cudaErrorLaunchTimeout};
         }
         prof_collect(p);
@@ -1427,7 +1459,7 @@ int mxp_chol_factor(mxp_plan_t p, double* A_host, int64_t lda, int64_t* info) {
         CK(cudaStreamSynchronize(p->sD2H));
         CK(cudaStreamSynchronize(p->sH2D));
         if (herr) {
-            g_last_error = "static schedule: a Ready-table wait timed out (scheduler error)";
+            g_last_error = "static schedule: a Ready-table wait timed out (scheduler error)" + sched_timeout_detail(p);
             throw CudaError{cudaErrorLaunchTimeout};
         }
         // merge the lower triangles of the staged diagonal tiles (upper untouched)
@@ -1625,7 +1657,7 @@ int mxp_chol_factor_matern(mxp_plan_t p, const double* xy_dev, double sigma2, do
         CK(cudaMemcpyAsync(&herr, p->d_flags + 1, sizeof(int), cudaMemcpyDeviceToHost, s0));
         CK(cudaStreamSynchronize(s0));
         if (herr) {
-            g_last_error = "static schedule: a Ready-table wait timed out (scheduler error)";
+            g_last_error = "static schedule: a Ready-table wait timed out (scheduler error)" + sched_timeout_detail(p);
             throw CudaError{cudaErrorLaunchTimeout};
         }
         prof_collect(p);

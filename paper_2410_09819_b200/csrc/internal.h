@@ -77,6 +77,8 @@ struct SchedArgs {
     const int4* items2;        // the GEMM task list of k_tc
     int nitems2;
     int* counter2;             // its ticket
+    int* tdiag;                // [8] first timed-out wait: flag offset from `ready`, target, value, smid,
+                               //     block, grid, column, taken (host reports it in mxp_last_error)
     int* sm_claim;             // [256] k_sched CTAs per SM in the Ozaki mode (extras leave at once,
                                //       keeping room for the k_tc CTA of every SM)
     unsigned long long* stats; // optional diagnostics (MXP_ATTR_PROFILE): see STAT_*

@@ -160,13 +160,33 @@ struct OzTile {
     const double* sb;   // 64 row scales of B's rows
 };
 
+// one lane of a converged warp (the same lane every time: the lowest active)
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\t"
+        "elect.sync rx|px, %1;\n\t"
+        "@px mov.s32 %0, 1;\n\t}\n"
+        : "+r"(pred)
+        : "r"(0xFFFFFFFFu));
+    return pred != 0;
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int* v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
+
 // C(128 x 64, fp64, column-major ldc) -= sum over ntiles tiles of A_n B_n^T,
-// each tile of K = 32 * kt (kt = nb / 32) emulated with s slices.
+// each tile of K = 32 * kt (kt = nb / 32) emulated with S slices.
 // smem: >= SMEM_BYTES dynamic shared memory; tmem: 512 allocated columns.
-// All 128 threads call; thread 0 issues the bulk copies and MMAs.
-template <class Src>
-__device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, int s, int kt, int64_t nb,
-                           uint8_t* smem, uint32_t tmem) {
+// All 128 threads call; thread 0 issues the bulk copies and the MMAs (S
+// compile-time: the S(S+1)/2 MMAs of a K step are straight-line code on
+// precomputed descriptors).
+template <int S, class Src>
+__device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles, int kt, int64_t nb, uint8_t* smem,
+                             uint32_t tmem) {
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * STAGE_BYTES);
     uint64_t* done = full + STAGES;
@@ -181,7 +201,7 @@ __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, i
         tc::fence_mbar_init();
     }
     __syncthreads();
-    // producer: copies of K step g into its stage
+    // producer (warp 0): copies of K step g into its stage
     OzTile cur{};
     int cur_i = -1;
     auto issue = [&](int g) {
@@ -189,36 +209,44 @@ __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, i
         if (i != cur_i) cur = src(i), cur_i = i;
         uint8_t* st = base + (g % STAGES) * STAGE_BYTES;
         uint64_t* fb = full + (g % STAGES);
-        tc::mbar_expect_tx(fb, (uint32_t)(s * (CHUNK + CHUNK_B)));
-        for (int t = 0; t < s; ++t) {
-            tc::bulk_g2s(st + t * CHUNK, cur.a + t * sstride + (int64_t)kc * CHUNK, CHUNK, fb);
-            tc::bulk_g2s(st + MAX_S * CHUNK + t * CHUNK_B, cur.b + t * sstride + (int64_t)kc * CHUNK, CHUNK_B, fb);
+        if (elect_one()) {
+            tc::mbar_expect_tx(fb, (uint32_t)(S * (CHUNK + CHUNK_B)));
+#pragma unroll
+            for (int t = 0; t < S; ++t) {
+                tc::bulk_g2s(st + t * CHUNK, cur.a + t * sstride + (int64_t)kc * CHUNK, CHUNK, fb);
+                tc::bulk_g2s(st + MAX_S * CHUNK + t * CHUNK_B, cur.b + t * sstride + (int64_t)kc * CHUNK, CHUNK_B,
+                             fb);
+            }
         }
+        __syncwarp();
     };
-    if (tid == 0)
+    const int warp = tid >> 5;
+    if (warp == 0)  // warp 0 (converged) drives the copies and MMAs; one elected lane issues them
         for (int g = 0; g < STAGES && g < G; ++g) issue(g);
 
     double acc[BN];
 #pragma unroll
     for (int j = 0; j < BN; ++j) acc[j] = 0.0;
-    const int warp = tid >> 5;
     const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
 
     for (int i = 0; i < ntiles; ++i) {
-        if (tid == 0) {
+        if (warp == 0) {
             for (int kc = 0; kc < kt; ++kc) {
                 const int g = i * kt + kc, stage = g % STAGES;
                 tc::mbar_wait(full + stage, (uint32_t)((g / STAGES) & 1));
                 tc::fence_after();
                 const uint32_t sa = tc::smem_u32(base + stage * STAGE_BYTES);
-                const uint32_t sb = sa + MAX_S * CHUNK;
-                for (int t = 0; t < s; ++t) {
-                    const uint64_t ad = make_desc(sa + t * CHUNK);
-                    for (int u = 0; u + t < s; ++u)  // level c = t + u (0-based) <= s - 1
-                        mma_i8(tmem + (uint32_t)((t + u) * BN), ad, make_desc(sb + u * CHUNK_B),
-                               (kc > 0 || t > 0) ? 1u : 0u);
-                }
-                tc::commit(done + stage);
+                const uint64_t ad0 = make_desc(sa), bd0 = make_desc(sa + MAX_S * CHUNK);
+                const uint32_t acc0 = kc > 0 ? 1u : 0u;
+#pragma unroll
+                for (int t = 0; t < S; ++t)
+#pragma unroll
+                    for (int u = 0; u + t < S; ++u)  // level c = t + u (0-based) <= S - 1
+                        if (elect_one())
+                            mma_i8(tmem + (uint32_t)((t + u) * BN), ad0 + (uint64_t)(t * (CHUNK >> 4)),
+                                   bd0 + (uint64_t)(u * (CHUNK_B >> 4)), t > 0 ? 1u : acc0);
+                if (elect_one()) tc::commit(done + stage);
+                __syncwarp();
                 // refill the previous step's stage once its MMAs have read it
                 // (this step's MMAs stay queued behind them meanwhile)
                 if (g >= 1 && g - 1 + STAGES < G) {
@@ -227,30 +255,30 @@ __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, i
                     issue(pg + STAGES);
                 }
             }
-            tc::commit(tbar);  // every MMA of tile i
+            if (elect_one()) tc::commit(tbar);  // every MMA of tile i
+            __syncwarp();
         }
-        __syncwarp();
         // drain: ACC levels of tile i -> fp64, scaled by the row scales
         if (tid < BN) s_sb[tid] = __ldcg(src(i).sb + tid);
         const double sa_r = __ldcg(src(i).sa + tid);
         tc::mbar_wait(tbar, (uint32_t)(i & 1));
         tc::fence_after();
         __syncthreads();  // s_sb visible
+        __syncwarp();     // (converged warp for the .sync.aligned TMEM loads)
 #pragma unroll
-        for (int g4 = 0; g4 < BN / 16; ++g4) {
-            double v[16];
+        for (int g8 = 0; g8 < BN / 8; ++g8) {
+            int x[S][8];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = 0.0;
-            for (int c = s - 1; c >= 0; --c) {  // smallest weight first
-                int x[16];
-                tmem_ld16(tl + (uint32_t)(c * BN + g4 * 16), x);
-                tmem_wait_ld();
-                const double w = __longlong_as_double((long long)(1023 - 7 * c) << 52);  // 2^(-7c)
+            for (int c = 0; c < S; ++c) tmem_ld8(tl + (uint32_t)(c * BN + g8 * 8), x[c]);
+            tmem_wait_ld();
 #pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = fma(i2d(x[j]), w, v[j]);
+            for (int j = 0; j < 8; ++j) {
+                double v = 0.0;
+#pragma unroll
+                for (int c = S - 1; c >= 0; --c)  // smallest weight first; 2^(-7c) exact
+                    v = fma(i2d(x[c][j]), __longlong_as_double((long long)(1023 - 7 * c) << 52), v);
+                acc[g8 * 8 + j] = fma(v * sa_r, s_sb[g8 * 8 + j], acc[g8 * 8 + j]);
             }
-#pragma unroll
-            for (int j = 0; j < 16; ++j) acc[g4 * 16 + j] = fma(v[j] * sa_r, s_sb[g4 * 16 + j], acc[g4 * 16 + j]);
         }
         tc::fence_before();
         __syncthreads();  // TMEM and s_sb free for tile i + 1
@@ -264,6 +292,19 @@ __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, i
     if (tid == 0) {
         for (int i = 0; i < STAGES; ++i) tc::mbar_inval(full + i), tc::mbar_inval(done + i);
         tc::mbar_inval(tbar);
+    }
+}
+
+constexpr int MIN_S = 4;  // slices supported by the compiled variants: MIN_S..MAX_S
+template <class Src>
+__device__ __forceinline__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, int s, int kt,
+                                           int64_t nb, uint8_t* smem, uint32_t tmem) {
+    switch (s) {
+    case 4: block_gemm_t<4>(C, ldc, src, ntiles, kt, nb, smem, tmem); break;
+    case 5: block_gemm_t<5>(C, ldc, src, ntiles, kt, nb, smem, tmem); break;
+    case 6: block_gemm_t<6>(C, ldc, src, ntiles, kt, nb, smem, tmem); break;
+    case 7: block_gemm_t<7>(C, ldc, src, ntiles, kt, nb, smem, tmem); break;
+    default: block_gemm_t<8>(C, ldc, src, ntiles, kt, nb, smem, tmem); break;
     }
 }
 

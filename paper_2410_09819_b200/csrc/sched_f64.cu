@@ -43,6 +43,16 @@ __device__ bool wait_flag(const int* flag, int target, const SchedArgs& a, int64
         if (info != 0 && col >= (info - 1) / a.nb) return false;
         if (*(volatile int*)a.err) return false;
         if (globaltimer() - t0 > WAIT_TIMEOUT_NS) {
+            if (a.tdiag && atomicCAS(a.tdiag + 7, 0, 1) == 0) {
+                a.tdiag[0] = (int)(flag - a.ready);
+                a.tdiag[1] = target;
+                a.tdiag[2] = ld_acquire(flag);
+                a.tdiag[3] = (int)smid();
+                a.tdiag[4] = (int)blockIdx.x;
+                a.tdiag[5] = (int)gridDim.x;
+                a.tdiag[6] = (int)col;
+                __threadfence();
+            }
             atomicExch(a.err, 1);
             return false;
         }
@@ -1167,6 +1177,14 @@ void configure_sched() {
     cudaFuncSetAttribute(k_sched<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM_BYTES);
     cudaFuncSetAttribute(k_potrf_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF_SMEM);
     cudaFuncSetAttribute(k_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, oz::SMEM_BYTES);
+    // every SM configured for the full 228 KB of shared memory: the Ozaki mode
+    // co-schedules one k_tc CTA (~150 KB) and one k_sched CTA (~78 KB) per SM,
+    // which a smaller carve-out picked for whichever kernel lands first would
+    // forbid (the second kernel's CTAs would then wait for the first to exit)
+    cudaFuncSetAttribute(k_tc, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_sched<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_sched<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_potrf_tile, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     done = true;
 }
 
