@@ -4,6 +4,12 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
+FP64 engine (--fp64-engine): "ozaki" (default) runs the FP64 GEMM/SYRK updates
+as exact int8 slice products on the tcgen05 tensor cores (Ozaki scheme I, 8
+slices = 55-bit operands, int32/fp64 accumulation) -- its
+backward error is checked every run and reported beside the native FP64
+tensor-pipe (DMMA) engine's, which is also timed (fp64_engines).
+
 Workload (BASELINE.json configs[1], "C2"): n = 65536, nb = 1024, FP64,
 PLASMA-plgsy random SPD (seed 42, generated on the device by the same counter
 hash as workloads/), in-core on one B200.  A step = one full factorization
@@ -62,7 +68,7 @@ def parse():
     ap.add_argument("--no-ooc", action="store_true")
     ap.add_argument("--ooc-n", type=int, default=98304)
     ap.add_argument("--ooc-frac", type=float, default=0.65)
-    ap.add_argument("--fp64-engine", default="dmma", choices=["dmma", "ozaki"],
+    ap.add_argument("--fp64-engine", default="ozaki", choices=["dmma", "ozaki"],
                     help="GEMM/SYRK engine of FP64 tiles: FP64 tensor pipe (DMMA) or Ozaki-I on int8 tcgen05")
     ap.add_argument("--oz-slices", type=int, default=8)
     ap.add_argument("--no-engine-compare", action="store_true")

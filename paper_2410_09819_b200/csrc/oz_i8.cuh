@@ -27,7 +27,8 @@
 //
 // Block shape: 128 (M, rows of A) x 64 (N, rows of B).  s levels x 64 int32
 // columns live in TMEM (s <= 8 -> <= 512 columns: the whole TMEM of the SM;
-// one such CTA per SM).
+// one such CTA per SM), level c at columns [64c, 64c+64).  Stacking B slices
+// along N maps onto consecutive levels, so one MMA of N = 64m covers m pairs.
 //
 // Operand image of a tile (written once by the tile's QUANT tasks): for slice
 // t (0-based), 128-row block rb, 32-column K chunk kc, a 4 KB chunk at
@@ -76,16 +77,18 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
     d |= (uint64_t)6 << 61;  // SWIZZLE_32B
     return d;
 }
-// instruction descriptor: D s32, A/B signed int8, both K-major, M = 128, N = 64
-constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
+// instruction descriptor: D s32, A/B signed int8, both K-major, M = 128, N = n
+__host__ __device__ constexpr uint32_t idesc_i8(int n) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
 
-__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
@@ -238,13 +241,21 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
                 const uint32_t sa = tc::smem_u32(base + stage * STAGE_BYTES);
                 const uint64_t ad0 = make_desc(sa), bd0 = make_desc(sa + MAX_S * CHUNK);
                 const uint32_t acc0 = kc > 0 ? 1u : 0u;
+                // A slice t meets B slices u = 0 .. S-1-t, i.e. levels t .. S-1.  The B
+                // slices sit 2 KB apart in smem (64 rows each): B slices u0 .. u0+m-1
+                // stacked are ONE K-major operand of N = 64 m rows, and its product
+                // lands in the m consecutive level accumulators (t+u0) .. (t+u0+m-1)
+                // -- so each A slice needs ceil((S-t)/4) MMAs of N <= 256 instead of
+                // S-t MMAs of N = 64 (12 instead of 36 for S = 8; A read 12x, not 36x).
 #pragma unroll
                 for (int t = 0; t < S; ++t)
 #pragma unroll
-                    for (int u = 0; u + t < S; ++u)  // level c = t + u (0-based) <= S - 1
+                    for (int u0 = 0; u0 + t < S; u0 += 4) {
+                        const int m = (S - t - u0) < 4 ? (S - t - u0) : 4;
                         if (elect_one())
-                            mma_i8(tmem + (uint32_t)((t + u) * BN), ad0 + (uint64_t)(t * (CHUNK >> 4)),
-                                   bd0 + (uint64_t)(u * (CHUNK_B >> 4)), t > 0 ? 1u : acc0);
+                            mma_i8(tmem + (uint32_t)((t + u0) * BN), ad0 + (uint64_t)(t * (CHUNK >> 4)),
+                                   bd0 + (uint64_t)(u0 * (CHUNK_B >> 4)), idesc_i8(BN * m), t > 0 ? 1u : acc0);
+                    }
                 if (elect_one()) tc::commit(done + stage);
                 __syncwarp();
                 // refill the previous step's stage once its MMAs have read it
