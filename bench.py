@@ -511,6 +511,11 @@ def run_ours(args):
 
         t64, ld64 = run(None, 1 + max(1, args.steps // 3))
         ll64 = -0.5 * nm * math.log(2 * math.pi) - 0.5 * ld64
+        mxp = {"workload": f"C3: Matern nu=0.5 theta=(1, 0.02627, 0.5) (weak), n={nm}, nb={nbm}, Morton-sorted "
+                           f"uniform locations (seed 1), tiles generated on the device inside the schedule",
+               "fp64": {"tflops": flops_m / t64 / 1e12, "ms": t64 * 1e3, "logdet": ld64}, "maps": {},
+               "fp64_engine": args.fp64_engine,
+               "device_free_gb_at_start": round(free_gb, 1)}
         ll64_y = run.ll_y
         if ll64_y is not None:
             lower_bytes = (nm // nbm) * (nm // nbm + 1) // 2 * nbm * nbm * 8
@@ -519,11 +524,6 @@ def run_ours(args):
                 "ms": run.solve_ms, "gbs": lower_bytes / (run.solve_ms / 1e3) / 1e9,
                 "how": "mxp_chol_loglik(y): forward solve L z = y (every lower tile read once) + ||z||^2, "
                        "CUDA events; GB/s = lower-triangle bytes / time (HBM roofline: MEASURED_PEAKS hbm_gbs)"}
-        mxp = {"workload": f"C3: Matern nu=0.5 theta=(1, 0.02627, 0.5) (weak), n={nm}, nb={nbm}, Morton-sorted "
-                           f"uniform locations (seed 1), tiles generated on the device inside the schedule",
-               "fp64": {"tflops": flops_m / t64 / 1e12, "ms": t64 * 1e3, "logdet": ld64}, "maps": {},
-               "fp64_engine": args.fp64_engine,
-               "device_free_gb_at_start": round(free_gb, 1)}
         for eps in args.mxp_eps:
             pmap, _ = m.precision_map_matern_device(xyd, nbm, eps, theta[0], theta[1])
             tm, ldm = run(pmap, 1 + max(1, args.steps // 3))

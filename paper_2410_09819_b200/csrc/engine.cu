@@ -231,6 +231,15 @@ void build_task_list(mxp_plan_s* p) {
     p->items.clear();
     p->items2.clear();
     p->expected.assign(p->T, 0);
+    // Ozaki mode: k_tc walks the whole list (items2), k_sched its non-GEMM part (items)
+    auto push = [&](const int4& it) {
+        if (p->oz_on) {
+            p->items2.push_back(it);
+            if (it.x != ITEM_GEMM) p->items.push_back(it);
+        } else {
+            p->items.push_back(it);
+        }
+    };
     auto owned = [&](int64_t m) { return m % p->nranks == p->rank; };
     auto gemm_col = [&](int64_t k, int64_t c0, int64_t c1) {
         for (int64_t c = c0; c < c1; ++c)
@@ -238,15 +247,13 @@ void build_task_list(mxp_plan_s* p) {
                 if (owned(m))
                 for (int64_t b = 0; b < gemm_blocks(p, m, k); ++b)
                     if (gemm_block_needed(p, m, k, b)) {
-                        // Ozaki mode: all GEMMs on the tensor-core kernel's list
-                        (p->oz_on ? p->items2 : p->items)
-                            .push_back(make_int4(ITEM_GEMM, (int)m, (int)k, (int)((b << 16) | c)));
+                        push(make_int4(ITEM_GEMM, (int)m, (int)k, (int)((b << 16) | c)));
                         p->expected[tile_index(Nt, m, k)]++;
                     }
     };
     auto prep_col = [&](int64_t k) {
         for (int64_t m = k; m < Nt; ++m)
-            if (owned(m)) p->items.push_back(make_int4(ITEM_PREP, (int)m, (int)k, 0));
+            if (owned(m)) push(make_int4(ITEM_PREP, (int)m, (int)k, 0));
     };
     if (p->host_mode) prep_col(0);
     for (int64_t k = 0; k < Nt; ++k) {
@@ -257,7 +264,7 @@ void build_task_list(mxp_plan_s* p) {
         }
         // POTRF(k): normally claimed by the dedicated kernel; listed so the
         // schedule can also complete on its own (fallback, see sched_f64.cu)
-        if (owned(k)) p->items.push_back(make_int4(ITEM_POTRF, (int)k, (int)k, 0));
+        if (owned(k)) push(make_int4(ITEM_POTRF, (int)k, (int)k, 0));
         if (k + 1 < Nt) {
             int64_t nb1 = nchunks(k + 1, KC) - 1;  // bulk chunks of column k+1
             gemm_col(k + 1, 0, nb1);
@@ -266,11 +273,11 @@ void build_task_list(mxp_plan_s* p) {
         for (int64_t m = k + 1; m < Nt; ++m)
             if (owned(m))
                 for (int64_t r = 0; r < nb / 64; ++r)
-                    p->items.push_back(make_int4(ITEM_TRSM, (int)m, (int)k, (int)r));
+                    push(make_int4(ITEM_TRSM, (int)m, (int)k, (int)r));
         for (int64_t m = k + 1; m < Nt; ++m)
             if (owned(m) && p->qtile[tile_index(Nt, m, k)])
                 for (int64_t r = 0; r < nb / 64; ++r)
-                    p->items.push_back(make_int4(ITEM_QUANT, (int)m, (int)k, (int)r));
+                    push(make_int4(ITEM_QUANT, (int)m, (int)k, (int)r));
     }
 }
 
@@ -405,12 +412,15 @@ size_t list_bytes(const mxp_plan_s* p) {
     for (int64_t t = 0; t < p->T; ++t) cnt += p->qtile[t] * (nb / 64);
     cnt += p->T;   // PREP tasks (host-streaming mode)
     cnt += Nt;     // POTRF claims
+    if (p->oz_on) cnt *= 2;  // the whole list for k_tc + its non-GEMM part for k_sched (upper bound)
     return sizeof(int4) * (size_t)cnt;
 }
 
 size_t flag_ints(const mxp_plan_s* p) {
-    // + timeout diagnostics (8) + per-SM claim words of k_sched in the Ozaki mode (256) + counter2 (last)
-    return (size_t)(2 + 7 * p->T + p->T * blocks_per_tile(p->nb) + 2 * p->Nt + 8 + 256 + 1);
+    // + Ozaki-mode task claims (TRSM, QUANT: T * nb/64 each; PREP: T) + timeout diagnostics (8)
+    // + per-SM claim words of k_sched in the Ozaki mode (256) + counter2 (last)
+    return (size_t)(2 + 7 * p->T + p->T * blocks_per_tile(p->nb) + 2 * p->Nt + (2 * p->T * (p->nb / 64) + p->T) +
+                    8 + 256 + 1);
 }
 
 // Tile slots of the device pool: every lower tile in core; with
@@ -874,6 +884,7 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     a.counter2 = p->d_flags + flag_ints(p) - 1;
     a.sm_claim = a.counter2 - 256;
     a.tdiag = a.sm_claim - 8;
+    a.task_claim = a.tdiag - (2 * T * (p->nb / 64) + T);
     a.qtile = p->d_qtile;
     a.img = (p->mxp && p->shadow_bytes > 0) ? p->d_img : nullptr;  // (null when no fp32 image exists)
     a.shadow = p->d_shadow;

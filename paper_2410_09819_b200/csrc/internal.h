@@ -74,9 +74,10 @@ struct SchedArgs {
     const long long* oz_img;   // [T] byte offset of the tile's int8 slice image in `shadow` (-1: none);
                                //     nullptr: the Ozaki engine is off
     int oz_slices;             // s (slices per operand, 1..8)
-    const int4* items2;        // the GEMM task list of k_tc
-    int nitems2;
-    int* counter2;             // its ticket
+    const int4* items2;        // k_tc's list: the WHOLE static list (k_tc alone can finish the
+    int nitems2;               //   schedule, e.g. when a profiler serializes the kernels); k_sched
+    int* counter2;             //   takes the non-GEMM subsequence (items); both claim non-GEMM tasks
+    int* task_claim;           //   by CAS here: TRSM [T*R] | QUANT [T*R] | PREP [T]  (R = nb/64)
     int* tdiag;                // [8] first timed-out wait: flag offset from `ready`, target, value, smid,
                                //     block, grid, column, taken (host reports it in mxp_last_error)
     int* sm_claim;             // [256] k_sched CTAs per SM in the Ozaki mode (extras leave at once,

@@ -931,6 +931,17 @@ __device__ __noinline__ void task_potrf_fallback(const SchedArgs& a, int64_t k, 
     if (potrf_tile_body<CC::NT>(a, k, smem, s_flag)) publish_potrf(a, k, smem + CC::LDA_S + CC::BM);
 }
 
+// Ozaki mode: a non-GEMM task is listed for both kernels and run by whichever
+// claims it first (POTRF has its own claim word, shared with k_potrf_tile).
+__device__ __forceinline__ bool claim_task(const SchedArgs& a, const int4& it) {
+    if (!a.oz_img || it.x == ITEM_GEMM || it.x == ITEM_POTRF) return true;
+    const int64_t R = a.nb / 64, T = a.Nt * (a.Nt + 1) / 2, t = tile_index(a.Nt, it.y, it.z);
+    int* c = it.x == ITEM_TRSM ? a.task_claim + t * R + it.w
+           : it.x == ITEM_QUANT ? a.task_claim + T * R + t * R + it.w
+                                : a.task_claim + 2 * T * R + t;
+    return atomicCAS(c, 0, 1) == 0;
+}
+
 // ------------------------------------------------------ the static schedule
 // The arguments live in global memory (copied once per factorization) so the
 // out-of-line task functions can take them by reference without a local copy.
@@ -992,6 +1003,13 @@ __global__ void __launch_bounds__(CC::NT, 3) k_sched(const SchedArgs a_param, co
         if (idx == -2) continue;
         const int4 it = a.items[idx];
         const int64_t m = it.y, k = it.z;
+        if (MXP && a.oz_img) {  // Ozaki mode: k_tc may have run it already
+            if (threadIdx.x == 0) s_flag = claim_task(*ap, it);
+            __syncthreads();
+            const bool mine = s_flag;
+            __syncthreads();
+            if (!mine) continue;
+        }
         // out-of-line tasks take the global copy of the arguments (*ap): a
         // reference to the by-value kernel parameter would force a local copy
         if (it.x == ITEM_POTRF) {
@@ -1037,11 +1055,13 @@ __global__ void __launch_bounds__(CC::NT, 3) k_sched(const SchedArgs a_param, co
 // MXP_ATTR_FP64_ENGINE = 1: every GEMM task of the schedule runs here -- FP64
 // outputs on the int8 tensor cores (task_gemm_oz), outputs below FP64 on the
 // tf32 operand-image engine -- one persistent CTA per SM owning all 512 TMEM
-// columns, co-resident with one k_sched CTA (TRSM / QUANT / PREP / POTRF
-// fallback) per SM.  Its list is the GEMM subsequence of the static schedule
-// (same order), so the ticket argument of k_sched carries over: every awaited
-// task precedes the waiting one in the global order, and each list is taken in
-// order by CTAs that are all resident.
+// columns, co-resident with one k_sched CTA per SM that takes the non-GEMM
+// subsequence (TRSM / QUANT / PREP / POTRF fallback).  k_tc walks the WHOLE
+// list in order and runs a non-GEMM task itself when k_sched has not claimed
+// it yet: so k_tc alone is a complete static schedule (the ticket argument of
+// k_sched holds for it), and k_sched only takes work off it -- a task claimed
+// by k_sched depends on earlier tasks only, which k_tc or k_sched finish.
+// (Profilers that serialize kernels run k_tc alone: still correct.)
 __global__ void __launch_bounds__(128, 1) k_tc(const SchedArgs* __restrict__ ap) {
     const SchedArgs& a = *ap;
     const int id = (int)smid();
@@ -1069,13 +1089,27 @@ __global__ void __launch_bounds__(128, 1) k_tc(const SchedArgs* __restrict__ ap)
         if (idx == -2) continue;
         const int4 it = a.items2[idx];
         const int64_t m = it.y, k = it.z;
-        const int cp = a.prec[tile_index(a.Nt, m, k)];
-        if (cp == P_FP64)
-            task_gemm_oz(a, m, k, it.w >> 16, it.w & 0xFFFF, smem_t, tmem, &s_flag);
-        else if (cp == P_FP32)
-            task_gemm_img<true>(a, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_t, tmem, &s_flag);
-        else
-            task_gemm_img<false>(a, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_t, tmem, &s_flag);
+        double* smem_d = reinterpret_cast<double*>(smem_t);
+        if (it.x == ITEM_GEMM) {
+            const int cp = a.prec[tile_index(a.Nt, m, k)];
+            if (cp == P_FP64)
+                task_gemm_oz(a, m, k, it.w >> 16, it.w & 0xFFFF, smem_t, tmem, &s_flag);
+            else if (cp == P_FP32)
+                task_gemm_img<true>(a, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_t, tmem, &s_flag);
+            else
+                task_gemm_img<false>(a, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_t, tmem, &s_flag);
+        } else {
+            if (threadIdx.x == 0) s_flag = claim_task(a, it);
+            __syncthreads();
+            const bool mine = s_flag;
+            __syncthreads();
+            if (mine) {
+                if (it.x == ITEM_POTRF) task_potrf_fallback(a, k, smem_d, &s_flag);
+                else if (it.x == ITEM_PREP) task_prep(a, m, k, smem_d + CC::LDA_S + CC::BM, &s_flag);
+                else if (it.x == ITEM_TRSM) task_trsm_ool(a, m, k, it.w, smem_d, &s_flag);
+                else task_quant(a, m, k, it.w, smem_d + 2048, &s_flag);
+            }
+        }
         __syncthreads();
     }
     tc::fence_before();

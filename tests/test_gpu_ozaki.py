@@ -144,3 +144,14 @@ def test_ozaki_mxp_matern_against_oracle(n, nb, eps):
     assert err <= 1e-4 * np.max(np.abs(Lo)), err  # the tf32 engine's bar (fp32 accumulation)
     Lt, _, ldt, _ = gpu_factor(S, nb, pmap, attrs={"tc_engine": 1})  # DMMA FP64 tiles, same images
     assert abs(ld - ldt) <= 1e-9 * abs(ldt)
+
+
+def test_ozaki_tc_kernel_alone_completes_the_schedule():
+    """debug_sync=1 synchronizes after every launch, so k_tc runs before k_sched
+    and the POTRF kernels exist (as under a profiler that serializes kernels):
+    it must finish the whole static schedule by itself, with the same bits."""
+    A = w.plgsy(2048, seed=8)
+    L1, i1, ld1, _ = gpu_factor(A, 256, attrs=OZ)
+    L2, i2, ld2, _ = gpu_factor(A, 256, attrs=dict(OZ, debug_sync=1))
+    assert i1 == i2 == 0
+    assert np.array_equal(L1, L2) and ld1 == ld2
