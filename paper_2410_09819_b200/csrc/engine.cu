@@ -949,12 +949,12 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
             launch_tc(p->d_args, nsm, p->sT);
             ++p->launches;
         }
+        dbg(p, p->sT, "tc");  // (debug_sync = 1: k_tc then runs the whole schedule alone)
         {
             Prof pr(p, p->sU, MXP_KCLASS_TRSM, trsm_flops);
             launch_sched(a, p->d_args, true, nsm, p->sU);
             ++p->launches;
         }
-        dbg(p, p->sT, "tc");
         dbg(p, p->sU, "sched");
         CK(cudaEventRecord(p->ev_join, p->sT));
         CK(cudaStreamWaitEvent(p->sU, p->ev_join, 0));
