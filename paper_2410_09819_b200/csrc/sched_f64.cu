@@ -390,7 +390,7 @@ __device__ __noinline__ bool task_gemm_tc(const SchedArgs& a, int64_t m, int64_t
 // operands bulk-copied from the per-tile fp32 images of cast_c(L) (written
 // once by the QUANT task of each operand tile), image e = max(c, p_operand)
 // (an operand stored at or below c is used as stored).
-template <bool THREE>
+template <bool THREE, int NST>
 __device__ __noinline__ bool task_gemm_img(const SchedArgs& a, int64_t m, int64_t k, int64_t b, int64_t c,
                                            int cprec, uint8_t* smem, uint32_t tmem, int* s_flag) {
     const int64_t Nt = a.Nt, nb = a.nb, S = nb / 128;
@@ -438,7 +438,7 @@ __device__ __noinline__ bool task_gemm_img(const SchedArgs& a, int64_t m, int64_
         return tc::ImgStep{ahi + o, alo ? alo + o : nullptr, bhi + o, blo ? blo + o : nullptr};
     };
     double* Ct = tile_ptr(a.pool, a.slot, Nt, nb, m, k) + bi * 128 + bj * 128 * nb;
-    tc::block_gemm_img<THREE>(Ct, nb, src, nsteps, smem, tmem);
+    tc::block_gemm_img<THREE, NST>(Ct, nb, src, nsteps, smem, tmem);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1028,9 +1028,9 @@ __global__ void __launch_bounds__(CC::NT, 3) k_sched(const SchedArgs a_param, co
                 else if (!a.tc_engine)
                     task_gemm_cast(*ap, m, k, it.w >> 16, it.w & 0xFFFF, smem, &s_flag);
                 else if (a.img && cp == P_FP32)
-                    task_gemm_img<true>(*ap, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_b, tmem, &s_flag);
+                    task_gemm_img<true, 2>(*ap, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_b, tmem, &s_flag);
                 else if (a.img)
-                    task_gemm_img<false>(*ap, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_b, tmem, &s_flag);
+                    task_gemm_img<false, 2>(*ap, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_b, tmem, &s_flag);
                 else if (cp == P_FP32)
                     task_gemm_tc<true>(*ap, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_b, mbar, tmem, &s_flag);
                 else
@@ -1095,9 +1095,9 @@ __global__ void __launch_bounds__(128, 1) k_tc(const SchedArgs* __restrict__ ap)
             if (cp == P_FP64)
                 task_gemm_oz(a, m, k, it.w >> 16, it.w & 0xFFFF, smem_t, tmem, &s_flag);
             else if (cp == P_FP32)
-                task_gemm_img<true>(a, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_t, tmem, &s_flag);
+                task_gemm_img<true, 4>(a, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_t, tmem, &s_flag);
             else
-                task_gemm_img<false>(a, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_t, tmem, &s_flag);
+                task_gemm_img<false, 4>(a, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_t, tmem, &s_flag);
         } else {
             if (threadIdx.x == 0) s_flag = claim_task(a, it);
             __syncthreads();

@@ -26,12 +26,15 @@ __global__ void __launch_bounds__(256) k_trsv_gemv(const double* __restrict__ po
     const int row = threadIdx.x & 127, h = threadIdx.x >> 7;
     const double* L = pool + (int64_t)slot[tile_index(Nt, m, k)] * nb * nb + rb * 128 + row;
     const int64_t c0 = h * (nb / 2), c1 = c0 + nb / 2;
-    double s0 = 0.0, s1 = 0.0;
-    for (int64_t c = c0; c < c1; c += 2) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // 4 chains, 8 loads in flight per thread
+#pragma unroll 2
+    for (int64_t c = c0; c < c1; c += 4) {
         s0 = fma(__ldcs(L + c * nb), sz[c], s0);
         s1 = fma(__ldcs(L + (c + 1) * nb), sz[c + 1], s1);
+        s2 = fma(__ldcs(L + (c + 2) * nb), sz[c + 2], s2);
+        s3 = fma(__ldcs(L + (c + 3) * nb), sz[c + 3], s3);
     }
-    part[threadIdx.x] = s0 + s1;
+    part[threadIdx.x] = (s0 + s1) + (s2 + s3);
     __syncthreads();
     if (h == 0) r[m * nb + rb * 128 + row] -= part[row] + part[row + 128];
 }
@@ -49,12 +52,15 @@ __global__ void __launch_bounds__(256) k_trsv_diag(const double* __restrict__ po
     for (int64_t J = 0; J < S; ++J) {
         const double* LJ = Lkk + J * 128 + row;
         const int64_t half = J * 64;  // columns [0, 128J) in two halves
-        double a0 = 0.0, a1 = 0.0;
-        for (int64_t c = h * half; c < (h + 1) * half; c += 2) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll 2
+        for (int64_t c = h * half; c < (h + 1) * half; c += 4) {
             a0 = fma(__ldcs(LJ + c * nb), sz[c], a0);
             a1 = fma(__ldcs(LJ + (c + 1) * nb), sz[c + 1], a1);
+            a2 = fma(__ldcs(LJ + (c + 2) * nb), sz[c + 2], a2);
+            a3 = fma(__ldcs(LJ + (c + 3) * nb), sz[c + 3], a3);
         }
-        part[threadIdx.x] = a0 + a1;
+        part[threadIdx.x] = (a0 + a1) + (a2 + a3);
         __syncthreads();
         if (h == 0) s[row] = r[k * nb + J * 128 + row] - (part[row] + part[row + 128]);
         __syncthreads();
