@@ -174,6 +174,7 @@ mxp_plan_s::~mxp_plan_s() {
     if (sAux) cudaStreamDestroy(sAux);
     if (sPush) cudaStreamDestroy(sPush);
     if (sMain) cudaStreamDestroy(sMain);
+    if (sT) cudaStreamDestroy(sT);
     if (ev_join) cudaEventDestroy(ev_join);
     for (int q = 0; q < MAX_RANKS; ++q)
         if (peer_ipc[q] && peer_ws[q]) cudaIpcCloseMemHandle(peer_ws[q]);
@@ -582,7 +583,6 @@ void ensure_streams(mxp_plan_s* p) {
     CK(cudaStreamCreateWithFlags(&p->sD2H, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&p->sAux, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&p->sPush, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithPriority(&p->sT, cudaStreamNonBlocking, lo));
     p->ev_panel.resize(p->Nt);
     p->ev_bulk.resize(p->Nt);
     for (int64_t k = 0; k < p->Nt; ++k) {
@@ -847,7 +847,15 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     CK(cudaEventRecord(p->ev_start, s0));
     CK(cudaStreamWaitEvent(p->sU, p->ev_start, 0));
     CK(cudaStreamWaitEvent(p->sP, p->ev_start, 0));
-    if (p->oz_on) CK(cudaStreamWaitEvent(p->sT, p->ev_start, 0));
+    if (p->oz_on) {
+        if (!p->sT) {  // created only when used: every stream takes a hardware queue, and parked
+                       // streams (stream memory waits) must not share one with the others
+            int lo = 0, hi = 0;
+            CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            CK(cudaStreamCreateWithPriority(&p->sT, cudaStreamNonBlocking, lo));
+        }
+        CK(cudaStreamWaitEvent(p->sT, p->ev_start, 0));
+    }
 
     SchedArgs a{};
     a.pool = p->pool;

@@ -53,12 +53,7 @@ constexpr int STAGES = 3;
 constexpr int STAGE_BYTES = MAX_S * (CHUNK + CHUNK_B);  // 48 KB
 constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 128 + BN * 8;  // + align slack, mbarriers, B scales
 constexpr int TMEM_COLS = 512;
-constexpr int PF = 6;  // L2 prefetch distance, in K steps
 
-// L2 prefetch of a global range (TMA engine; no completion tracking)
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
 
 __host__ __device__ constexpr int64_t image_bytes(int s, int64_t nb) {
     return (((int64_t)s * nb * nb + 8 * nb) + 1023) / 1024 * 1024;
@@ -210,25 +205,10 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
         tc::fence_mbar_init();
     }
     __syncthreads();
-    // producer (warp 0): copies of K step g into its stage, and an L2 prefetch of
-    // step g + PF (the operand images stream from HBM: L2 holds ~70 % of them)
-    OzTile cur{}, pcur{};
-    int cur_i = -1, pcur_i = -1;
-    auto prefetch = [&](int g) {
-        if (g >= G) return;
-        const int i = g / kt, kc = g - i * kt;
-        if (i != pcur_i) pcur = src(i), pcur_i = i;
-        if (elect_one()) {
-#pragma unroll
-            for (int t = 0; t < S; ++t) {
-                bulk_prefetch_l2(pcur.a + t * sstride + (int64_t)kc * CHUNK, CHUNK);
-                bulk_prefetch_l2(pcur.b + t * sstride + (int64_t)kc * CHUNK, CHUNK_B);
-            }
-        }
-        __syncwarp();
-    };
+    // producer (warp 0): copies of K step g into its stage
+    OzTile cur{};
+    int cur_i = -1;
     auto issue = [&](int g) {
-        prefetch(g + PF);
         const int i = g / kt, kc = g - i * kt;
         if (i != cur_i) cur = src(i), cur_i = i;
         uint8_t* st = base + (g % STAGES) * STAGE_BYTES;
@@ -246,7 +226,7 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
     };
     const int warp = tid >> 5;
     if (warp == 0) {  // warp 0 (converged) drives the copies and MMAs; one elected lane issues them
-        for (int g = STAGES; g < STAGES + PF - 1 && g < G; ++g) prefetch(g);
+        __syncwarp();
         for (int g = 0; g < STAGES && g < G; ++g) issue(g);
     }
 
@@ -257,6 +237,7 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
 
     for (int i = 0; i < ntiles; ++i) {
         if (warp == 0) {
+            __syncwarp();
             for (int kc = 0; kc < kt; ++kc) {
                 const int g = i * kt + kc, stage = g % STAGES;
                 tc::mbar_wait(full + stage, (uint32_t)((g / STAGES) & 1));

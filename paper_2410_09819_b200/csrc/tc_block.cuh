@@ -185,6 +185,7 @@ __device__ void block_gemm_img(double* C, int64_t ldc, const Src& src, int nstep
     }
     __syncthreads();
     if ((threadIdx.x >> 5) == 0) {
+        __syncwarp();  // converged: elect.sync below needs all 32 lanes
         // stage contents: which of the 4 chunks hold data (bit i = chunk i)
         auto issue = [&](int st, int stage) -> uint32_t {
             uint8_t* B0 = base + stage * IMG_STAGE;
