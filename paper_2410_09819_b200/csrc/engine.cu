@@ -519,9 +519,8 @@ Layout layout(const mxp_plan_s* p) {
     off += align_up(sizeof(long long) * 4 * (size_t)p->T, 256);
     L.ozimg = off;
     off += align_up(sizeof(long long) * (size_t)p->T, 256);
-    L.solve = off;  // forward solve: r, z (Nt*nb each) + scalars + partial products and flags
-    off += align_up(sizeof(double) * (2 * (size_t)p->Nt * p->nb + 8), 256) +
-           align_up(forward_solve_work_bytes(p->Nt, p->nb), 256);
+    L.solve = off;  // forward solve: r, z (Nt*nb each) + scalars
+    off += align_up(sizeof(double) * (2 * (size_t)p->Nt * p->nb + 8), 256);
     L.shadow = off;
     off += align_up(p->shadow_bytes, 1024);
     L.pool = off;
@@ -1835,22 +1834,13 @@ int mxp_chol_solve_lower(mxp_plan_t p, const double* y_dev, double* z_dev, doubl
         cudaStream_t s = p->user_stream;
         CK(cudaMemsetAsync(r, 0, sizeof(double) * N, s));
         CK(cudaMemcpyAsync(r, y_dev, sizeof(double) * p->n, cudaMemcpyDeviceToDevice, s));
-        void* work = reinterpret_cast<char*>(p->d_solve) +
-                     align_up(sizeof(double) * (2 * (size_t)N + 8), 256);
-        if (launch_forward_solve(p->pool, p->d_slot, p->d_wbuf, p->Nt, p->nb, r, z, work, s) != 0)
-            throw CudaError{cudaGetLastError()};
+        launch_forward_solve(p->pool, p->d_slot, p->d_wbuf, p->Nt, p->nb, r, z, s);
         launch_sumsq(z, p->n, sc, s);
         CK(cudaGetLastError());
-        int serr = 0;
-        CK(cudaMemcpyAsync(&serr, forward_solve_err(work, p->Nt, p->nb), sizeof(int), cudaMemcpyDeviceToHost, s));
         if (z_dev) CK(cudaMemcpyAsync(z_dev, z, sizeof(double) * p->n, cudaMemcpyDeviceToDevice, s));
         double h = 0.0;
         CK(cudaMemcpyAsync(&h, sc, sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        if (serr) {
-            g_last_error = "forward solve: a dependency wait timed out";
-            throw CudaError{cudaErrorLaunchTimeout};
-        }
         if (sumsq) *sumsq = h;
     } catch (const CudaError& e) {
         cudaSetDevice(cur);

@@ -105,12 +105,9 @@ int tc_ctas_per_sm();
 void launch_potrf_tile(const SchedArgs& a, int64_t k, cudaStream_t s);
 
 // ---- forward solve / log-likelihood (solve.cu) -----------
-// z = L^-1 r on the resident factor (r, z: Nt*nb, padded with zeros); work: the
-// partial products and flags (forward_solve_work_bytes); returns 0 or -1 (launch failed)
-size_t forward_solve_work_bytes(int64_t Nt, int64_t nb);
-int launch_forward_solve(const double* pool, const int32_t* slot, const double* wbuf, int64_t Nt, int64_t nb,
-                         double* r, double* z, void* work, cudaStream_t s);
-const int* forward_solve_err(void* work, int64_t Nt, int64_t nb);  // device word: 1 = a wait timed out
+// z = L^-1 r on the resident factor (r, z: Nt*nb, padded with zeros; r is consumed)
+void launch_forward_solve(const double* pool, const int32_t* slot, const double* wbuf, int64_t Nt, int64_t nb,
+                          double* r, double* z, cudaStream_t s);
 void launch_sumsq(const double* z, int64_t n, double* out, cudaStream_t s);
 
 // ---- layout / utility kernels --------------------------------------------
