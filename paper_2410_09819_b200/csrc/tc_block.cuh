@@ -148,22 +148,19 @@ struct ImgStep {
     const uint8_t* blo;
 };
 constexpr int IMG_STAGE = 4 * SUB_BYTES;                     // 32 KB
-constexpr int IMG_SMEM_BYTES = 1024 + 2 * IMG_STAGE + 64;    // + alignment slack + 5 mbarriers
+constexpr int IMG_SMEM_BYTES = 1024 + 2 * IMG_STAGE + 64;    // + alignment slack + 5 mbarriers (NST = 2)
 
-// NST: kept for the call sites; the engine runs 2 stages (measured faster in both
-// k_sched and k_tc than a 4-stage warp-driven variant: C3 110.9 vs 103.1 TF/s at 1e-8)
+// NST stages: 2 in k_sched (3 CTAs per SM), 4 in k_tc (one CTA per SM).  Thread 0
+// drives the pipeline (a warp-driven elect.sync variant measured slower).
 template <bool THREE, int NST, class Src>
 __device__ void block_gemm_img(double* C, int64_t ldc, const Src& src, int nsteps, uint8_t* smem, uint32_t tmem) {
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(base + 2 * IMG_STAGE);
-    uint64_t* done = full + 2;
-    uint64_t* fin = full + 4;  // one-shot: every MMA of the block has completed
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + NST * IMG_STAGE);
+    uint64_t* done = full + NST;
+    uint64_t* fin = done + NST;  // one-shot: every MMA of the block has completed
     const int nst = THREE ? nsteps : (nsteps + 1) / 2;  // stages to run
     if (threadIdx.x == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
-        mbar_init(&done[0], 1);
-        mbar_init(&done[1], 1);
+        for (int i = 0; i < NST; ++i) mbar_init(&full[i], 1), mbar_init(&done[i], 1);
         mbar_init(fin, 1);
         fence_mbar_init();
     }
@@ -196,12 +193,11 @@ __device__ void block_gemm_img(double* C, int64_t ldc, const Src& src, int nstep
                 if (srcs[i]) bulk_g2s(B0 + i * SUB_BYTES, srcs[i], SUB_BYTES, &full[stage]);
             return mask;
         };
-        uint32_t masks[2];
-        masks[0] = issue(0, 0);
-        if (nst > 1) masks[1] = issue(1, 1);
+        uint32_t masks[NST];
+        for (int i = 0; i < NST && i < nst; ++i) masks[i] = issue(i, i);
         for (int st = 0; st < nst; ++st) {
-            const int stage = st & 1;
-            mbar_wait(&full[stage], (st >> 1) & 1);
+            const int stage = st % NST;
+            mbar_wait(&full[stage], (st / NST) & 1);
             fence_after();
             const uint32_t b0 = smem_u32(base + stage * IMG_STAGE);
             const uint32_t m = masks[stage];
@@ -226,9 +222,9 @@ __device__ void block_gemm_img(double* C, int64_t ldc, const Src& src, int nstep
                 }
             }
             commit(&done[stage]);
-            if (st + 2 < nst) {
-                mbar_wait(&done[stage], (st >> 1) & 1);  // this stage's MMAs have read their operands
-                masks[stage] = issue(st + 2, stage);
+            if (st + NST < nst) {
+                mbar_wait(&done[stage], (st / NST) & 1);  // this stage's MMAs have read their operands
+                masks[stage] = issue(st + NST, stage);
             }
         }
         commit(fin);  // tracks every earlier tcgen05 op of this thread
@@ -253,10 +249,7 @@ __device__ void block_gemm_img(double* C, int64_t ldc, const Src& src, int nstep
     fence_before();
     __syncthreads();
     if (threadIdx.x == 0) {
-        mbar_inval(&full[0]);
-        mbar_inval(&full[1]);
-        mbar_inval(&done[0]);
-        mbar_inval(&done[1]);
+        for (int i = 0; i < NST; ++i) mbar_inval(&full[i]), mbar_inval(&done[i]);
         mbar_inval(fin);
     }
 }
