@@ -348,6 +348,8 @@ void plan_images(mxp_plan_s* p) {
     // Ozaki mode (in core; tiles below FP64 need the image engine): every
     // off-diagonal tile is an operand of the FP64 SYRK of its row's diagonal
     // tile, so each gets an int8 slice image (s bytes per element + row scales)
+    // (single rank: with ranks co-located on one GPU the two kernels of each rank
+    // did not all become resident and the schedule timed out -- DESIGN 5.7)
     if (p->fp64_engine == 1 && pool_slots(p) == T && p->nranks == 1 && (!p->mxp || images)) {
         const long long ob = oz::image_bytes(p->oz_slices, p->nb);
         const size_t before = p->shadow_bytes;
@@ -713,6 +715,11 @@ void push_tiles(mxp_plan_s* p, const SchedArgs& a) {
                         CK(cudaMemcpyAsync(peer_addr(p, q, im), im, sizeof(float) * nb * nb,
                                            cudaMemcpyDeviceToDevice, p->sPush));
                     }
+                if (p->oz_on && p->oz_img[t] >= 0) {  // int8 slice image + row scales (Ozaki engine)
+                    const uint8_t* im = p->d_shadow + p->oz_img[t];
+                    CK(cudaMemcpyAsync(peer_addr(p, q, im), im, (size_t)oz::image_bytes(p->oz_slices, nb),
+                                       cudaMemcpyDeviceToDevice, p->sPush));
+                }
                 CK(cudaMemcpyAsync(peer_addr(p, q, a.ready + t), p->d_epoch, sizeof(int), cudaMemcpyDeviceToDevice,
                                    p->sPush));
             }

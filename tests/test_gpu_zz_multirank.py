@@ -12,9 +12,12 @@ import workloads as w
 pytestmark = pytest.mark.gpu
 
 
-def _ranks(n, nb, P, pmap=None):
+def _ranks(n, nb, P, pmap=None, attrs=None):
     import paper_2410_09819_b200 as m
     plans = [m.Plan(n, nb, pmap) for _ in range(P)]
+    for pl in plans:  # (before attaching: attributes that re-size the workspace come first)
+        for k, v in (attrs or {}).items():
+            pl.set(k, v)
     share = 148 // P
     for r, pl in enumerate(plans):
         pl.set("rank", r)
@@ -159,3 +162,4 @@ def test_ranks_repeat_factorizations():
         assert res == [0] * P
         for r in range(P):
             assert np.array_equal(np.tril(As[r].cpu().numpy()), L1), (it, r)
+
