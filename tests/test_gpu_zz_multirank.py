@@ -81,18 +81,10 @@ def test_generated_mxp_two_ranks():
     assert p1.factor_matern(xy, 1.0, 0.02627) == 0
     L1 = p1.get_factor().cpu().numpy()
     plans = _ranks(n, nb, 2, pmap)
-    fn = lambda r, pl: (pl.factor_matern(xy, 1.0, 0.02627, stream_from_torch=False), pl.logdet())  # noqa: E731
-    try:
-        res = _run(plans, fn)
-    except AssertionError as e:
-        # KNOWN ISSUE: with two ranks co-located on one GPU this
-        # generated-MxP case intermittently (~1 in 3 runs, also before the Ozaki
-        # work) stalls a cross-rank Ready push until the 20 s scheduler timeout.
-        # The ranks recover on the same plans (epoch-valued Ready words); one
-        # retry, reported, and the bitwise checks below still apply.
-        import warnings
-        warnings.warn(f"co-located 2-rank generated MxP: retry after {e}")
-        res = _run(plans, fn)
+    # KNOWN ISSUE: with two ranks co-located on one GPU this
+    # generated-MxP case intermittently (~1 run in 3, also before the Ozaki work)
+    # stalls a cross-rank Ready push until the 20 s scheduler timeout.
+    res = _run(plans, lambda r, pl: (pl.factor_matern(xy, 1.0, 0.02627, stream_from_torch=False), pl.logdet()))
     for r in range(2):
         assert res[r][0] == 0
         assert res[r][1] == p1.logdet()
