@@ -75,6 +75,11 @@ def parse():
     return ap.parse_args()
 
 
+def progress(what):
+    """leg markers on stderr (the JSON line stays the only stdout line)"""
+    print(f"[bench] {time.strftime('%H:%M:%S')} done: {what}", file=sys.stderr, flush=True)
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -282,6 +287,7 @@ def run_ours(args):
     launches = int(allreduce(launches, "sum"))
     value = flops / t_step / 1e12  # one n x n factorization per step, over all ranks
 
+    progress("C2 timed")
     # correctness probe on the last factor: ||(A - L L^T) x|| / (||A||_F ||x||)
     L = torch.tril(B)
     g = torch.Generator(device=dev)
@@ -299,6 +305,7 @@ def run_ours(args):
 
     engine_used = "ozaki" if plan.get("fp64_engine_used") == 1 else "dmma"
 
+    progress("probe")
     # the other FP64 engine on the same input (same step, fewer reps)
     engines = {engine_used: {"tflops": value, "ms": t_step * 1e3, "backward_error_probe": probe,
                              "logdet": logdet}}
@@ -335,6 +342,7 @@ def run_ours(args):
                                     "s(s+1)/2 int8 tcgen05 GEMMs per tile product, exact int32 TMEM "
                                     "accumulation, fp64 combination per tile of K")
 
+    progress("engine compare")
     # live FP64 peak: cuBLAS DGEMM on this box (MEASURED_PEAKS.json has no fp64 figure)
     d = 8192
     Xa = torch.randn(d, d, dtype=torch.float64, device=dev)
@@ -386,6 +394,7 @@ def run_ours(args):
     kstats = {k: {"launches": v[0], "ms": v[1], "tflops": (v[2] / (v[1] / 1e3) / 1e12) if v[1] > 0 and v[2] > 0
                   else None} for k, v in stats_acc.items()}
 
+    progress("dgemm peak")
     # cuSOLVER potrf (cusolverDnXpotrf, fp64) on the same box (library baseline).
     # Its lower-triangle path dies with an illegal address at exactly n = 65536
     # (n^2 = 2^32; 65024 works), so it is timed lower at n - 512 (same family,
@@ -419,6 +428,7 @@ def run_ours(args):
     del plan
     torch.cuda.empty_cache()
 
+    progress("cusolver")
     # end-to-end through the host API: pinned host A, H2D + factor + D2H per
     # step.  Several ranks: each rank streams (and writes back) only the tile
     # rows it owns from its own pinned copy of A.
@@ -454,6 +464,7 @@ def run_ours(args):
     del A
     torch.cuda.empty_cache()
 
+    progress("e2e")
     # C3 (BASELINE configs[2]): Matern nu=0.5 weak correlation, 4-precision map,
     # n = 131072, generated tile by tile on the device inside the schedule;
     # log-likelihood at y = 0 (Eq. 3 convention, G16) vs the FP64 factorization
@@ -538,6 +549,7 @@ def run_ours(args):
         mxp["note"] = ("value/units: TFLOP/s = (n^3/3)/t, t = factorization incl. fused generation; loglik at "
                        "y=0 vs the FP64 run of the same pipeline (G16); 1 warm-up + timed reps, best")
 
+    progress("C3")
     # Out of core (a5/a9; C4's mode at a size this box's host RAM holds): the
     # host matrix streamed through a pool capped at ooc_frac of the lower
     # triangle (dead-tile slot recycling) vs the same host-streaming call
