@@ -11,10 +11,10 @@ with gcc and marshals numpy arrays through ctypes.
 
 Parity status: quantizers, norms, planner, the all-FP64
 factorization, log-det and forward solve are pinned by tests that do not
-re-use this code.  The mixed-precision factorization is **parity unpinned**
-beyond its exact special cases (banded integer L0, reduction to the FP64 map);
-its accuracy is pinned only through the log-likelihood against the FP64
-factor.
+re-use this code.  The mixed-precision factorization is pinned at each of its
+rounding points (O3 input quantization, quantize-after-TRSM, operand down-cast)
+by hand-derived cases in tests/golden/mxp_rounding_points.json, plus its exact
+special cases (banded integer L0, reduction to the FP64 map).
 """
 from __future__ import annotations
 

@@ -22,9 +22,13 @@
  *        closed forms, monotonicity)
  *   orc_factor (all-FP64 map) ....... pinned (KMS closed form, integer-L0
  *        exact recovery, Cholesky-Banachiewicz brute force, LAPACK)
- *   orc_factor (mixed map) .......... PARITY UNPINNED beyond the exact
- *        banded-L0 case and the reduction to the FP64 map; accuracy is
- *        pinned only through log-det / log-likelihood vs the FP64 factor.
+ *   orc_factor (mixed map) .......... pinned at its three rounding points
+ *        (O3 input quantization, quantize once after the TRSM, operand
+ *        down-cast cast_c with the operand's own scale) by hand-derived
+ *        Nt = 2..3 cases (tests/golden/mxp_rounding_points.json) that each
+ *        misreading fails; plus the exact banded-L0 case and the reduction
+ *        to the FP64 map.  Its accuracy on real maps is bounded through
+ *        log-det / log-likelihood vs the FP64 factor.
  *   orc_logdet / orc_forward_solve .. pinned (SPEC examples, KMS closed form)
  *
  * Layout: A is column-major with leading dimension lda; only the lower
