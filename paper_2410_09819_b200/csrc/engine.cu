@@ -136,6 +136,7 @@ struct mxp_plan_s {
     cudaStream_t sU = 0, sP = 0;
     std::vector<cudaEvent_t> ev_panel, ev_bulk;
     cudaEvent_t ev_start = nullptr, ev_done = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_sched_end = nullptr, ev_potrf_end = nullptr;  // schedule kernels finished (failure watcher)
     cudaStream_t sMain = nullptr;      // ordering stream of a multi-rank call (joined to user_stream)
 
     int64_t launches = 0, h2d = 0, d2h = 0;
@@ -176,6 +177,8 @@ mxp_plan_s::~mxp_plan_s() {
     if (sMain) cudaStreamDestroy(sMain);
     if (sT) cudaStreamDestroy(sT);
     if (ev_join) cudaEventDestroy(ev_join);
+    if (ev_sched_end) cudaEventDestroy(ev_sched_end);
+    if (ev_potrf_end) cudaEventDestroy(ev_potrf_end);
     for (int q = 0; q < MAX_RANKS; ++q)
         if (peer_ipc[q] && peer_ws[q]) cudaIpcCloseMemHandle(peer_ws[q]);
     if (h_stage) cudaFreeHost(h_stage);
@@ -535,6 +538,19 @@ size_t workspace_need(const mxp_plan_s* p) { return layout(p).total; }
 
 void bind_workspace(mxp_plan_s* p) {
     Layout L = layout(p);
+    if (p->ws && L.total > p->ws_bytes) {
+        // the layout grew since the workspace was bound (e.g. RANK/NRANKS changed the image plan)
+        if (!p->ws_owned) {
+            g_last_error = "user workspace smaller than the plan's current layout (mxp_chol_workspace_size)";
+            throw CudaError{cudaErrorInvalidValue};
+        }
+        cudaFree(p->ws);
+        p->ws = nullptr;
+        p->ws_owned = false;
+        for (int q = 0; q < MAX_RANKS; ++q)  // peers must re-attach the new workspace
+            if (p->peer_ws[q] && p->peer_ipc[q]) cudaIpcCloseMemHandle(p->peer_ws[q]);
+        for (int q = 0; q < MAX_RANKS; ++q) p->peer_ws[q] = nullptr, p->peer_ipc[q] = false;
+    }
     if (!p->ws) {
         void* ptr = nullptr;
         cudaError_t e = cudaMalloc(&ptr, L.total);
@@ -594,6 +610,8 @@ void ensure_streams(mxp_plan_s* p) {
     CK(cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&p->ev_sched_end, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&p->ev_potrf_end, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&p->sMain, cudaStreamNonBlocking));
     p->streams_ready = true;
 }
@@ -1008,6 +1026,30 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
         feeders.clear();
     };
     int64_t d2h_bytes = 0;  // (outlives the feeders: they are joined on every path)
+    // Failure watcher: the copy streams park on Ready / column words that a
+    // failed column (info != 0) or a scheduler timeout never sets, and a
+    // feeder blocked in an enqueue into a parked stream's full queue would
+    // never return.  So the release is independent of the feeders: once the
+    // schedule kernels have ended, a failed run's Ready and column words are
+    // set to a value above every epoch, which drains every parked stream.
+    CK(cudaEventRecord(p->ev_sched_end, p->sU));
+    CK(cudaEventRecord(p->ev_potrf_end, p->sP));
+    if (host_mode || p->nranks > 1)
+        feed([&] {
+            CK(cudaEventSynchronize(p->ev_sched_end));
+            CK(cudaEventSynchronize(p->ev_potrf_end));
+            int64_t hinfo = 0;
+            int herr = 0;
+            CK(cudaMemcpyAsync(&hinfo, p->d_info, sizeof(int64_t), cudaMemcpyDeviceToHost, p->sAux));
+            CK(cudaMemcpyAsync(&herr, a.err, sizeof(int), cudaMemcpyDeviceToHost, p->sAux));
+            CK(cudaStreamSynchronize(p->sAux));
+            if (hinfo != 0 || herr || p->debug_sync == 2) {
+                CK(cudaMemsetAsync(a.ready, 0x7f, sizeof(int) * T, p->sAux));
+                CK(cudaMemsetAsync(a.col_ready, 0x7f, sizeof(int) * Nt, p->sAux));
+                CK(cudaStreamSynchronize(p->sAux));
+                p->ready_dirty = true;
+            }
+        });
     if (p->nranks > 1) feed([&] { push_tiles(p, a); });
     if (host_mode && !gen) try {
         // H2D in schedule (column) order; the GPU front-end publishes loaded[t]
@@ -1113,6 +1155,7 @@ void finish_pushes(mxp_plan_s* p, cudaStream_t s0) {
 
 int status_from_exception(const CudaError& e) {
     if (e.e == cudaErrorMemoryAllocation) return MXP_ENOMEM;
+    if (e.e == cudaErrorInvalidValue) return MXP_ESTATE;
     return MXP_ECUDA;
 }
 
@@ -1206,13 +1249,22 @@ int mxp_chol_plan_set(mxp_plan_t p, mxp_attr_t key, int64_t v) {
         return MXP_OK;
     case MXP_ATTR_PROFILE: p->profile = v ? 1 : 0; return MXP_OK;
     case MXP_ATTR_RANK:
-        if (v < 0 || v >= MAX_RANKS) return -3;
-        p->rank = (int)v;
-        p->list_uploaded = false;
-        return MXP_OK;
     case MXP_ATTR_NRANKS:
-        if (v < 1 || v > MAX_RANKS) return -3;
-        p->nranks = (int)v;
+        if (key == MXP_ATTR_RANK && (v < 0 || v >= MAX_RANKS)) return -3;
+        if (key == MXP_ATTR_NRANKS && (v < 1 || v > MAX_RANKS)) return -3;
+        // nranks is part of the image plan (workspace layout): drop an owned
+        // workspace, refuse a user one that may no longer fit
+        if (p->ws && !p->ws_owned && key == MXP_ATTR_NRANKS && v != p->nranks) return MXP_ESTATE;
+        if (p->ws_owned && (key == MXP_ATTR_NRANKS ? v != p->nranks : v != p->rank)) {
+            cudaFree(p->ws);
+            p->ws = nullptr;
+            p->ws_owned = false;
+            for (int q = 0; q < MAX_RANKS; ++q)
+                if (p->peer_ws[q] && p->peer_ipc[q]) cudaIpcCloseMemHandle(p->peer_ws[q]);
+            for (int q = 0; q < MAX_RANKS; ++q) p->peer_ws[q] = nullptr, p->peer_ipc[q] = false;
+        }
+        if (key == MXP_ATTR_RANK) p->rank = (int)v;
+        else p->nranks = (int)v;
         p->list_uploaded = false;
         return MXP_OK;
     case MXP_ATTR_SM_FIRST:

@@ -261,3 +261,29 @@ def test_out_of_core_mxp():
     Lo, info2, _, _ = gpu_factor(S, nb, pmap, host=True, plan=plan)
     assert info == info2 == 0
     assert np.array_equal(Lo, Lin)
+
+
+@pytest.mark.parametrize("j,cap_frac", [(0, 0.0), (5000, 0.0), (5000, 0.6)])
+def test_host_path_not_pd_large_nt_does_not_hang(j, cap_frac):
+    """with Nt = 48 the copy-stream queues fill up behind
+    parked waits; a failed column must still release every parked stream (the
+    failure watcher in factor_incore_f64), in core and out of core."""
+    import torch
+
+    import paper_2410_09819_b200 as m
+    n, nb = 12288, 256
+    Ad = torch.empty((n, n), dtype=torch.float64, device="cuda").T
+    m.generate_plgsy_device(Ad, seed=3)
+    Ad[j, j] = -1.0
+    Ah = Ad.T.cpu().pin_memory()  # row-major (n,n) of a symmetric matrix == column-major A
+    Ad[j, j] = float(n)
+    Agood = Ad.T.cpu().pin_memory()
+    del Ad
+    plan = m.Plan(n, nb)
+    if cap_frac:
+        plan.set("hbm_bytes_cap", int(cap_frac * 8 * nb * nb * 48 * 49 // 2))
+    info = plan.factor(Ah.T)
+    assert info == j + 1
+    # the plan is reusable afterwards: a good matrix factors
+    assert plan.factor(Agood.T) == 0
+    plan.close()
