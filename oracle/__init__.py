@@ -63,6 +63,8 @@ def _load():
         lib.orc_unit_roundoff.restype = dbl
         lib.orc_quantize_tile.argtypes = [ctypes.c_int, i64, pd, pd]
         lib.orc_quantize_tile.restype = dbl
+        lib.orc_cast_tile.argtypes = [ctypes.c_int, ctypes.c_int, i64, pd, pd]
+        lib.orc_cast_tile.restype = None
         lib.orc_tile_index.argtypes = [i64, i64, i64]
         lib.orc_tile_index.restype = i64
         lib.orc_tile_norms.argtypes = [i64, i64, pd, i64, pd]
@@ -111,6 +113,14 @@ def quantize_tile(prec: int, T) -> tuple[np.ndarray, float]:
     out = np.empty_like(T)
     s = _load().orc_quantize_tile(prec, T.size, _pd(T), _pd(out))
     return out, s
+
+
+def cast_tile(c: int, stored: int, T) -> np.ndarray:
+    """O4.2.3: operand cast of a tile stored at ``stored`` to compute precision ``c``."""
+    T = np.ascontiguousarray(T, dtype=np.float64)
+    out = np.empty_like(T)
+    _load().orc_cast_tile(c, stored, T.size, _pd(T), _pd(out))
+    return out
 
 
 def tile_index(Nt: int, i: int, j: int) -> int:

@@ -128,6 +128,23 @@ double orc_quantize_tile(int prec, int64_t cnt, const double* in, double* out) {
     return s;
 }
 
+/* O4.2.3 / G12: operand cast to the compute precision c of a GEMM,
+ *   cast_c(T) = deq(q_c(deq(T)))  when T is stored MORE precise than c
+ *                                  (down-cast with T's own new scale);
+ *   cast_c(T) = T                  when T is stored no more precise than c
+ *                                  (an exact up-cast, "up/down-casting").
+ * (Re-quantizing an up-cast with a scale recomputed from the stored amax is
+ * not always the identity: when the tile's amax rounded up into the next
+ * binade its scale halves, and odd subnormal codes would round again.)
+ * Codes: lower = more precise (FP64 0 ... FP8 3). */
+void orc_cast_tile(int c, int stored, int64_t cnt, const double* in, double* out) {
+    if (stored >= c) {
+        if (out != in) memcpy(out, in, sizeof(double) * (size_t)cnt);
+        return;
+    }
+    orc_quantize_tile(c, cnt, in, out);
+}
+
 /* ------------------------------------------------------------------------ */
 /* O0 tiling helpers.  Tile (i,j) holds rows i*nb.., cols j*nb..; padding   */
 /* is 0, with 1 on the padded diagonal.                              */
@@ -252,7 +269,7 @@ int64_t orc_potrf_unblocked(int64_t m, double* C, int64_t ldc) {
 /*   X solves X L_kk^T = C, column-wise forward substitution (G13);    */
 /*   L_mk = deq(q_{p_mk}(X))   (quantize once per task, after TRSM).          */
 /* A^_ij = deq(q_{p_ij}(A_ij)) is the stored input (O3, G14).                 */
-/* cast_c(T) = deq(q_c(T)) for a stored tile T (P:42 up/down-casting).         */
+/* cast_c(T): orc_cast_tile (down-cast deq(q_c(T)), up-cast identity). */
 /*                                                                            */
 /* A (n x n, lda, lower) is overwritten by L (dequantized values); the strict */
 /* upper triangle is untouched.  map = NULL means all FP64.                   */
@@ -299,8 +316,8 @@ int64_t orc_factor(int64_t n, int64_t nb, double* A, int64_t lda, const uint8_t*
             double* X = (double*)malloc(sizeof(double) * (size_t)tsz);
             double* Y = (double*)malloc(sizeof(double) * (size_t)tsz);
             for (int64_t nn = 0; nn < k; ++nn) {
-                orc_quantize_tile(c_prec, tsz, TILE(m, nn), X);   /* cast_c(L_mn) */
-                orc_quantize_tile(c_prec, tsz, TILE(k, nn), Y);   /* cast_c(L_kn) */
+                orc_cast_tile(c_prec, PREC(m, nn), tsz, TILE(m, nn), X);   /* cast_c(L_mn) */
+                orc_cast_tile(c_prec, PREC(k, nn), tsz, TILE(k, nn), Y);   /* cast_c(L_kn) */
                 for (int64_t c = 0; c < nb; ++c)
                     for (int64_t p = 0; p < nb; ++p) {
                         double y = Y[c + p * nb];

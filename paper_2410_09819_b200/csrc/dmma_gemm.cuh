@@ -12,6 +12,16 @@
 namespace mxp {
 
 // ------------------------------------------------------------------ helpers
+// CTA-internal barrier of the NT "worker" threads 0..NT-1 (named barrier 1).
+// The task bodies shared by k_sched (128 threads) and the tensor-core kernel
+// k_tc (128 workers + 2 tcgen05 producer / MMA warps that skip non-GEMM
+// tasks) synchronize with it instead of __syncthreads; with NT = blockDim.x
+// it is the same as __syncthreads.
+template <int NT>
+__device__ __forceinline__ void sync_nt() {
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+}
+__device__ __forceinline__ void sync_workers() { sync_nt<128>(); }
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
@@ -96,14 +106,14 @@ __device__ __forceinline__ void gemm_mainloop(double (&acc)[C::MI][C::NI][2], co
     }
     for (int it = 0; it < nk; ++it) {
         cp_async_wait<STAGES - 2>();
-        __syncthreads();
+        sync_nt<NT>();
         int nxt = it + STAGES - 1;
         if (nxt < nk) load_stage(nxt % STAGES, nxt);
         cp_async_commit();
         if constexpr (Post::active) {
             double* wA = smem + (it % STAGES) * C::STAGE_DOUBLES;
             post(it, wA, wA + BK * C::LDA_S);
-            __syncthreads();
+            sync_nt<NT>();
         }
         const double* sA = smem + (it % STAGES) * C::STAGE_DOUBLES;
         const double* sB = sA + BK * C::LDA_S;
@@ -123,7 +133,7 @@ __device__ __forceinline__ void gemm_mainloop(double (&acc)[C::MI][C::NI][2], co
         }
     }
     cp_async_wait<0>();
-    __syncthreads();
+    sync_nt<NT>();
 }
 
 // Element (row, col) of the CTA block owned by fragment (mi, ni, i) of this thread.

@@ -238,7 +238,7 @@ __device__ __forceinline__ bool task_trsm(const SchedArgs& a, int64_t m, int64_t
             tw0 = tw1;
         }
     }
-    __syncthreads();
+    sync_workers();
     if (!*s_flag) return false;
     double* X = tile_ptr(a.pool, a.slot, Nt, nb, m, k) + r * 64;
     const double* L = tile_ptr(a.pool, a.slot, Nt, nb, k, k);
@@ -268,7 +268,7 @@ __device__ __forceinline__ bool task_trsm(const SchedArgs& a, int64_t m, int64_t
                     __stcg(p, __ldcg(p) - acc[mi][ni][i]);
                 }
         __threadfence_block();
-        __syncthreads();
+        sync_workers();
         zero_acc<CC>(acc);
         const double* W = Wk + J * (128 * 128);
         auto src2 = [&](int it, const double*& pa, const double*& pb) {
@@ -289,12 +289,12 @@ __device__ __forceinline__ bool task_trsm(const SchedArgs& a, int64_t m, int64_t
                     xmax = fmax(xmax, fabs(acc[mi][ni][i]));
                 }
         __threadfence_block();
-        __syncthreads();
+        sync_workers();
     }
     for (int o = 16; o > 0; o >>= 1) xmax = fmax(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
     if ((threadIdx.x & 31) == 0) atomic_max_abs(a.amax_x + t, xmax);
     __threadfence();
-    __syncthreads();
+    sync_workers();
     if (threadIdx.x == 0) {
         int old = atom_add_release(a.trsm_done + t, 1);
         const bool fp64 = !a.prec || !a.qtile[t];  // no QUANT task follows
@@ -520,7 +520,7 @@ __device__ void oz_slice_rows(const SchedArgs& a, const double* X, int64_t r, ui
     double mx = 0.0;
     for (int64_t cc = c0; cc < c1; ++cc) mx = fmax(mx, fabs(__ldcg(X + row + cc * nb)));
     red[tid] = mx;
-    __syncthreads();
+    sync_workers();
     double inv;
     const double sc = oz::row_scale(fmax(red[row], red[row + 64]), inv);
     if (half == 0) reinterpret_cast<double*>(img + (int64_t)s * nb * nb)[r * 64 + row] = sc;
@@ -540,7 +540,7 @@ __device__ __noinline__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k
     const int64_t Nt = a.Nt, nb = a.nb;
     const int64_t t = tile_index(Nt, m, k);
     if (threadIdx.x == 0) *s_flag = wait_flag(a.trsm_done + t, (int)(nb / 64), a, k);
-    __syncthreads();
+    sync_workers();
     if (!*s_flag) return false;
     const int p = a.prec ? a.prec[t] : P_FP64;
     const double amax = amax_of(a.amax_x + t);
@@ -564,7 +564,7 @@ __device__ __noinline__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k
     }
     if (p != P_FP64 || any) {
         const int64_t kper = nb / tc::KS;
-        for (int64_t idx = threadIdx.x; idx < 16 * nb; idx += blockDim.x) {
+        for (int64_t idx = threadIdx.x; idx < 16 * nb; idx += CC::NT) {
             const int q4 = (int)(idx & 15), col = (int)(idx >> 4);
             double* q = X + 4 * q4 + (int64_t)col * nb;
             double2 v01 = __ldcg(reinterpret_cast<const double2*>(q));
@@ -602,11 +602,11 @@ __device__ __noinline__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k
     }
     if (a.oz_img && a.oz_img[t] >= 0) {  // int8 slices of the stored values (FP64 GEMM operands)
         __threadfence_block();
-        __syncthreads();
+        sync_workers();
         oz_slice_rows(a, X, r, a.shadow + a.oz_img[t], red);
     }
     __threadfence();
-    __syncthreads();
+    sync_workers();
     if (threadIdx.x == 0) {
         a.amax_s[t] = amax_st;
         __threadfence();
@@ -642,40 +642,40 @@ __device__ __noinline__ bool task_prep(const SchedArgs& a, int64_t m, int64_t k,
         }
         *s_flag = ok;
     }
-    __syncthreads();
+    sync_workers();
     if (!*s_flag) return false;
     double* T = tile_ptr(a.pool, a.slot, Nt, nb, m, k);
     const int64_t rr = n - m * nb, cr = n - k * nb;  // real rows / columns of this tile
     if (a.gen_mode) {  // N2: generate the tile in place (fused generation, no input copy)
-        for (int64_t e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+        for (int64_t e = threadIdx.x; e < nb * nb; e += CC::NT) {
             const int64_t r = e % nb, c = e / nb;
             double v;
             if (r < rr && c < cr) v = matern_entry(a, m * nb + r, k * nb + c);
             else v = (m == k && r == c) ? 1.0 : 0.0;
             __stcg(T + e, v);
         }
-        __syncthreads();
+        sync_workers();
     } else if (rr < nb || cr < nb) {
-        for (int64_t e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+        for (int64_t e = threadIdx.x; e < nb * nb; e += CC::NT) {
             const int64_t r = e % nb, c = e / nb;
             if (r >= rr || c >= cr) __stcg(T + e, (m == k && r == c) ? 1.0 : 0.0);
         }
-        __syncthreads();
+        sync_workers();
     }
     const int p = a.prec ? a.prec[t] : P_FP64;
     if (p != P_FP64) {
         double v = 0.0;
-        for (int64_t e = threadIdx.x; e < nb * nb; e += blockDim.x) v = fmax(v, fabs(__ldcg(T + e)));
+        for (int64_t e = threadIdx.x; e < nb * nb; e += CC::NT) v = fmax(v, fabs(__ldcg(T + e)));
         for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-        __syncthreads();
+        sync_workers();
         double amax = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) amax = fmax(amax, red[w]);
+        for (int w = 0; w < (CC::NT >> 5); ++w) amax = fmax(amax, red[w]);
         const double sc = tile_scale(p, amax), isc = 1.0 / sc;
-        for (int64_t e = threadIdx.x; e < nb * nb; e += blockDim.x) __stcg(T + e, quantize_value(p, __ldcg(T + e), sc, isc));
+        for (int64_t e = threadIdx.x; e < nb * nb; e += CC::NT) __stcg(T + e, quantize_value(p, __ldcg(T + e), sc, isc));
     }
     __threadfence();
-    __syncthreads();
+    sync_workers();
     if (threadIdx.x == 0) st_release(a.prep_done + t, 1);
     return true;
 }
@@ -750,7 +750,7 @@ __device__ bool potrf_tile_body(const SchedArgs& a, int64_t k, double* smem, int
                     gemm_mainloop<G>(acc, src, nb, nb, J * 128 / BK, smem);
                     store_acc<G>(acc, D + (int64_t)I * 128 + h * G::BM + (int64_t)J * 128 * nb, nb, true);
                     __threadfence_block();
-                    __syncthreads();
+                    sync_nt<NT>();
                 }
         }
         phase(STAT_PF_UPD);
@@ -760,7 +760,7 @@ __device__ bool potrf_tile_body(const SchedArgs& a, int64_t k, double* smem, int
             if (r >= c) P[pidx_c(r, c)] = __ldcg(DJJ + r + (int64_t)c * nb);
         }
         if (t == 0) *s_flag = 0;
-        __syncthreads();
+        sync_nt<NT>();
         // ---- unblocked left-looking (column) Cholesky of the packed block:
         //      thread i computes L[i,j] = (D[i,j] - sum_{q<j} L[i,q] L[j,q]) / L[j,j]
         //      (S:144 up to summation order); 2 barriers per column.
@@ -796,10 +796,10 @@ __device__ bool potrf_tile_body(const SchedArgs& a, int64_t k, double* smem, int
                     P[pidx_c(j, j)] = sqrt(sv);
                 }
             }
-            __syncthreads();
+            sync_nt<NT>();
             if (*s_flag) return false;
             if (t > j && t < 128) P[pidx_c(t, j)] = sv / P[pidx_c(j, j)];
-            __syncthreads();
+            sync_nt<NT>();
         }
         phase(STAT_PF_CHOL);
         // ---- W = L^-1 row by row: W[r,c] = (delta_rc - sum_{q<r} L[r,q] W[q,c]) / L[r,r]
@@ -837,7 +837,7 @@ __device__ bool potrf_tile_body(const SchedArgs& a, int64_t k, double* smem, int
             }
             // (no barrier: column c of W is read and written by thread c only)
         }
-        __syncthreads();
+        sync_nt<NT>();
         if (NT != 256) {  // row-major -> column-major in place
             for (int idx = t; idx < 128 * 128; idx += NT) {
                 const int r = idx >> 7, c = idx & 127;
@@ -849,7 +849,7 @@ __device__ bool potrf_tile_body(const SchedArgs& a, int64_t k, double* smem, int
             }
             __threadfence_block();
         }
-        __syncthreads();
+        sync_nt<NT>();
         // ---- write L_JJ (zero upper) [and W_J, col-major, zero upper]
         for (int idx = t; idx < 128 * 128; idx += NT) {
             int c = idx >> 7, r = idx & 127;
@@ -857,7 +857,7 @@ __device__ bool potrf_tile_body(const SchedArgs& a, int64_t k, double* smem, int
             if (NT == 256) __stcg(W + r + c * 128, r >= c ? R[pidx_r(r, c)] : 0.0);
         }
         __threadfence_block();
-        __syncthreads();
+        sync_nt<NT>();
         phase(STAT_PF_INV);
         // ---- TRSM of the blocks below: D[I,J] = D[I,J] W^T (the mainloop
         //      consumes all of D[I,J] before the epilogue overwrites it)
@@ -873,7 +873,7 @@ __device__ bool potrf_tile_body(const SchedArgs& a, int64_t k, double* smem, int
                 gemm_mainloop<G>(acc, src, nb, 128, 128 / BK, smem);
                 store_acc<G>(acc, DIJ, nb, false);
                 __threadfence_block();
-                __syncthreads();
+                sync_nt<NT>();
             }
         phase(STAT_PF_TRSM);
     }
@@ -895,6 +895,7 @@ __device__ void claim_potrf(const SchedArgs& a, int64_t k, uint64_t grace_ns, in
     *s_flag = ok && atomicCAS(a.potrf_claim + k, 0, 1) == 0;
 }
 
+template <int NT>
 __device__ void publish_potrf(const SchedArgs& a, int64_t k, double* red) {
     // this tile's share of log|A| = 2 sum log L_ii: fixed-order tree
     // reduction over the real diagonal entries (deterministic)
@@ -902,18 +903,18 @@ __device__ void publish_potrf(const SchedArgs& a, int64_t k, double* red) {
     const double* D = tile_ptr(a.pool, a.slot, a.Nt, nb, k, k);
     const int64_t real = a.n - k * nb < nb ? a.n - k * nb : nb;
     double v = 0.0;
-    for (int64_t r = threadIdx.x; r < real; r += blockDim.x) v += log(__ldcg(D + r + r * nb));
+    for (int64_t r = threadIdx.x; r < real; r += NT) v += log(__ldcg(D + r + r * nb));
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    __syncthreads();
+    sync_nt<NT>();
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
+    sync_nt<NT>();
     if (threadIdx.x == 0) {
         double sum = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) sum += red[w];
+        for (int w = 0; w < (NT >> 5); ++w) sum += red[w];
         a.logdet_parts[k] = sum;
     }
     __threadfence();
-    __syncthreads();
+    sync_nt<NT>();
     if (threadIdx.x == 0) {
         st_release(a.ready + tile_index(a.Nt, k, k), a.epoch);
         atom_add_release(a.col_ready + k, 1);
@@ -926,9 +927,9 @@ __device__ void publish_potrf(const SchedArgs& a, int64_t k, double* red) {
 // profiler, or the reserved SM busy) a scheduler CTA factors the tile itself.
 __device__ __noinline__ void task_potrf_fallback(const SchedArgs& a, int64_t k, double* smem, int* s_flag) {
     if (threadIdx.x == 0) claim_potrf(a, k, 200000, s_flag);
-    __syncthreads();
+    sync_workers();
     if (!*s_flag) return;
-    if (potrf_tile_body<CC::NT>(a, k, smem, s_flag)) publish_potrf(a, k, smem + CC::LDA_S + CC::BM);
+    if (potrf_tile_body<CC::NT>(a, k, smem, s_flag)) publish_potrf<CC::NT>(a, k, smem + CC::LDA_S + CC::BM);
 }
 
 // Ozaki mode: a non-GEMM task is listed for both kernels and run by whichever
@@ -1135,7 +1136,7 @@ __global__ void __launch_bounds__(256, 1) k_potrf_tile(SchedArgs a, int64_t k) {
     }
     __syncthreads();
     if (!s_flag) return;
-    if (potrf_tile_body<256>(a, k, smem, &s_flag)) publish_potrf(a, k, smem);
+    if (potrf_tile_body<256>(a, k, smem, &s_flag)) publish_potrf<256>(a, k, smem);
 }
 
 // ------------------------------------------------- generated-matrix planner

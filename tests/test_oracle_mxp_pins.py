@@ -115,3 +115,26 @@ def test_oracle_identity_embedding(case, nb):
     L, info = oracle.factor(embed(A, nb), nb, pmap)
     assert info == 0
     assert np.array_equal(L, embed(Lexp, nb))
+
+
+def test_upcast_is_identity_even_when_the_stored_amax_crossed_a_binade():
+    """O4.2.3 / P:42: an operand stored no more precisely than the compute
+    precision c is used as stored (an exact up-cast), including c equal to
+    its own precision.  Hand derivation (E4M3, nb = 2 tile [0.99, 2^-17]):
+      q_FP8: amax = 0.99, floor(log2 0.99) = -1, s = 2^(7+1) = 2^8;
+        0.99 * 256 = 253.44 in [2^7, 2^8), spacing 16 -> 15.84 -> 16 -> code 256 -> 1.0
+        2^-17 * 256 = 2^-9 = the smallest E4M3 subnormal -> exact -> 2^-17
+      stored T = [1.0, 2^-17].  cast_FP8(T) = T and cast_FP16(T) = T.
+    The misreading 're-quantize with the stored amax' gives s' = 2^(7-0) = 2^7,
+    2^-17 * 2^7 = 2^-10 = half the subnormal spacing -> tie -> even -> 0."""
+    T, s = oracle.quantize_tile(3, np.array([0.99, 2.0 ** -17]))
+    assert s == 2.0 ** 8 and T[0] == 1.0 and T[1] == 2.0 ** -17
+    assert np.array_equal(oracle.cast_tile(3, 3, T), T)
+    assert np.array_equal(oracle.cast_tile(2, 3, T), T)
+    assert np.array_equal(oracle.cast_tile(0, 3, T), T)
+    requant, _ = oracle.quantize_tile(3, T)      # the misreading
+    assert requant[1] == 0.0 and requant[1] != T[1]
+    # a genuine down-cast (stored FP32, c = FP8) rounds with the tile's own scale:
+    # amax 1.03125 -> s = 2^7: 132 -> 128 -> 1.0;  0.1 * 128 = 12.8 in [2^3, 2^4), spacing 1 -> 13 -> 0.1015625
+    D = oracle.cast_tile(3, 1, np.array([1.03125, 0.1]))
+    assert D[0] == 1.0 and D[1] == 13 / 128
