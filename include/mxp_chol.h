@@ -68,12 +68,18 @@ typedef enum mxp_attr {
                                      diagonal tile) */
     MXP_ATTR_PROFILE = 6,         /* 1 = time every launch with CUDA events on its stream (mxp_chol_kernel_stats) */
     MXP_ATTR_TC_ENGINE = 7,       /* GEMM tasks of tiles below FP64 (G12):
-                                     1 (default) = tcgen05 kind::tf32 (3xTF32 for FP32 tiles, 1xTF32 for the exact
+                                     3 (default) = native operand width: FP16 outputs on tcgen05 kind::f16 (fp16
+                                       codes), FP8 outputs on kind::f8f6f4 (E4M3 codes), per-tile power-of-two
+                                       scales applied to the fp32 TMEM partial of every K tile; FP32 outputs on
+                                       3xTF32 as 1.  Needs the tensor-core kernel of MXP_ATTR_FP64_ENGINE = 1 (in
+                                       core, single rank); otherwise it behaves as 1 (MXP_ATTR_TC_ENGINE_USED);
+                                     1 = tcgen05 kind::tf32 (3xTF32 for FP32 tiles, 1xTF32 for the exact
                                        FP16/FP8 values) fed by bulk copies of per-tile fp32 operand images written
                                        once by the QUANT tasks (in core; out of core it behaves as 2);
                                      2 = tcgen05, operands converted from the fp64 tiles in registers;
                                      0 = FP64 DMMA with the same casts (fp64 accumulation).
-                                     Changing it re-sizes the workspace (images: up to 4 nb^2 fp32 per tile). */
+                                     Changing it re-sizes the workspace (images: 1, 2 or 4(+4) bytes per element
+                                     and consumer precision). */
     MXP_ATTR_RANK = 8,            /* this plan's rank in a row-cyclic distribution (tile (m,n) on rank m mod nranks) */
     MXP_ATTR_NRANKS = 9,          /* ranks (GPUs) sharing the factorization, <= 8; peers attached with
                                      mxp_chol_ipc_attach / mxp_chol_attach_peer_plan.  Each rank keeps streams
@@ -99,7 +105,9 @@ typedef enum mxp_attr {
     MXP_ATTR_POOL_SLOTS = 103,    /* (get only) tile slots in the device pool */
     MXP_ATTR_NT = 104,            /* (get only) Nt = ceil(n/nb) */
     MXP_ATTR_IMAGE_BYTES = 105,   /* (get only) bytes of tcgen05 operand images in the workspace (0: none) */
-    MXP_ATTR_FP64_ENGINE_USED = 106 /* (get only) FP64 engine the next factorization uses (0 DMMA, 1 Ozaki) */
+    MXP_ATTR_FP64_ENGINE_USED = 106, /* (get only) FP64 engine the next factorization uses (0 DMMA, 1 Ozaki) */
+    MXP_ATTR_TC_ENGINE_USED = 107 /* (get only) engine of the tiles below FP64 the next factorization uses
+                                     (-1: all-FP64 map; else as MXP_ATTR_TC_ENGINE) */
 } mxp_attr_t;
 
 /*

@@ -19,6 +19,7 @@
 #include "../../include/mxp_chol.h"
 #include "internal.h"
 #include "oz_i8.cuh"
+#include "tc_native.cuh"
 
 using namespace mxp;
 
@@ -91,7 +92,7 @@ struct mxp_plan_s {
     std::vector<int> expected;
     bool list_uploaded = false;
     int reserved_sms = 1;
-    int tc_engine = 1;             // non-FP64 GEMM tasks: 0 DMMA with casts, 1 tcgen05 on operand
+    int tc_engine = 3;             // non-FP64 GEMM tasks: 0 DMMA with casts, 1 tcgen05 on operand
                                    // images (register-staged when out of core), 2 tcgen05 register-staged
     // operand images (tcgen05 engine, in core): see SchedArgs::img
     std::vector<long long> img;    // [4T] byte offsets into the image arena, -1 = absent
@@ -105,6 +106,7 @@ struct mxp_plan_s {
     // oz_on = the engine actually used by the current image plan
     int fp64_engine = 0, oz_slices = 8;
     bool oz_on = false;
+    bool nat_on = false;            // tiles below FP64 on the native-width engine (tc_engine 3, k_tc)
     std::vector<long long> oz_img;  // [T] byte offsets of the int8 slice images, -1 = none
     long long* d_oz_img = nullptr;
     double* d_solve = nullptr;      // forward-solve work vectors (r | z | scalars)
@@ -114,6 +116,7 @@ struct mxp_plan_s {
     uint8_t* d_prec = nullptr;
     unsigned long long* d_amax_x = nullptr;
     double* d_amax_s = nullptr;
+    double* d_iscale = nullptr;     // [2T] scales of the native fp16 / E4M3 code images
     SchedArgs* d_args = nullptr;
     SchedArgs h_args{};
     bool host_mode = false;        // task list built for the host-streaming path (PREP tasks)
@@ -293,55 +296,81 @@ void build_task_list(mxp_plan_s* p) {
 // remainder for e = FP32.  Out of core (pool < T) the register-staged engine
 // is used instead (images would be sized by the whole lower triangle).
 int64_t pool_slots(const mxp_plan_s* p);
+// does a workspace of `need` bytes beside the fp64 pool fit in this device's free memory
+// (2 GB headroom; the plan's own current workspace counts as free)
+bool fits_beside_pool(const mxp_plan_s* p, double need) {
+    size_t fr = 0, tot = 0;
+    int cur = 0;
+    bool ok = true;
+    cudaGetDevice(&cur);
+    if (cudaSetDevice(p->device) == cudaSuccess && cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+        const double pool = (double)sizeof(double) * p->nb * p->nb * p->T;
+        ok = pool + need <= (double)fr + (double)p->ws_bytes - 2e9;
+    }
+    cudaGetLastError();
+    cudaSetDevice(cur);
+    return ok;
+}
+void plan_images_as(mxp_plan_s* p, bool native);
 void plan_images(mxp_plan_s* p) {
-    const long long key = ((((long long)p->oz_slices * 2 + p->fp64_engine) * 9 + p->nranks) * 3 + p->tc_engine) * 2 +
+    const long long key = ((((long long)p->oz_slices * 2 + p->fp64_engine) * 9 + p->nranks) * 4 + p->tc_engine) * 2 +
                           (pool_slots(p) == p->T ? 1 : 0);
     if (key == p->img_key) return;
     p->img_key = key;
+    // native-width images (kind::f16 / kind::f8f6f4) run in the tensor-core kernel k_tc, which
+    // exists with the Ozaki FP64 engine (in core, single rank); otherwise (or if the Ozaki
+    // images do not fit) the fp32 tf32 images
+    const bool try_native = p->mxp && p->tc_engine == 3 && p->fp64_engine == 1 && p->nranks == 1 &&
+                            pool_slots(p) == p->T;
+    plan_images_as(p, try_native);
+    if (try_native && !p->oz_on) plan_images_as(p, false);
+}
+void plan_images_as(mxp_plan_s* p, bool native) {
     const int64_t Nt = p->Nt, T = p->T;
     p->img.assign(4 * T, -1);
     p->oz_img.assign(T, -1);
     p->oz_on = false;
+    p->nat_on = false;
     p->qtile.assign(T, 0);
     p->shadow_bytes = 0;
-    bool images = p->mxp && p->tc_engine == 1 && pool_slots(p) == T;
+    bool images = p->mxp && p->tc_engine != 0 && p->tc_engine != 2 && pool_slots(p) == T;
     const long long img_bytes = (long long)sizeof(float) * p->nb * p->nb;
-    if (images) {  // the images must fit beside the pool in this device's free memory
+    if (images) {  // lower bound of the image bytes (each non-FP64 tile at least its own image)
         long long need = 0;
-        for (int64_t t = 0; t < T; ++t) need += p->map[t] == MXP_FP32 ? 2 : (p->map[t] != MXP_FP64 ? 1 : 0);
-        size_t fr = 0, tot = 0;
-        int cur = 0;
-        cudaGetDevice(&cur);
-        if (cudaSetDevice(p->device) == cudaSuccess && cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
-            const double pool = (double)sizeof(double) * p->nb * p->nb * T;
-            // lower bound of the image bytes (each non-FP64 tile at least its own image)
-            if (pool + (double)need * img_bytes > (double)fr + (double)p->ws_bytes - 2e9) images = false;
-        }
-        cudaGetLastError();
-        cudaSetDevice(cur);
+        for (int64_t t = 0; t < T; ++t)
+            need += p->map[t] == MXP_FP32 ? 2 * img_bytes
+                    : p->map[t] == MXP_FP16 ? (native ? img_bytes / 2 : img_bytes)
+                    : p->map[t] == MXP_FP8 ? (native ? img_bytes / 4 : img_bytes) : 0;
+        if (!fits_beside_pool(p, (double)need)) images = false;
     }
+    // Tile t = (i, n) is an operand of the GEMMs of row i (outputs (i, k), n < k < i) and of
+    // column i (outputs (m, i), m > i).  tf32 engine: one fp32 image per distinct
+    // e = max(c, p_t) (+ the TF32 remainder for e = FP32).  Native engine: slot 0 (+ 3) = fp32
+    // values of cast_max(FP32, p_t) for FP32 outputs, slot 1 = fp16 codes for FP16 outputs,
+    // slot 2 = E4M3 codes for FP8 outputs.
     for (int64_t n = 0; n < Nt; ++n)
         for (int64_t i = n + 1; i < Nt; ++i) {
             const int64_t t = tile_index(Nt, i, n);
             const int pt = p->map[t];
-            bool need[4] = {false, false, false, false};
+            bool need[4] = {false, false, false, false};  // by consumer precision c (native) / e (tf32)
             if (images) {
-                for (int64_t k = n + 1; k < i; ++k) {
-                    const int c = p->map[tile_index(Nt, i, k)];
-                    if (c != MXP_FP64) need[std::max(c, pt)] = true;
-                }
-                for (int64_t m = i + 1; m < Nt; ++m) {
-                    const int c = p->map[tile_index(Nt, m, i)];
-                    if (c != MXP_FP64) need[std::max(c, pt)] = true;
-                }
+                auto consumer = [&](int c) {
+                    if (c == MXP_FP64) return;
+                    need[native ? c : std::max(c, pt)] = true;
+                };
+                for (int64_t k = n + 1; k < i; ++k) consumer(p->map[tile_index(Nt, i, k)]);
+                for (int64_t m = i + 1; m < Nt; ++m) consumer(p->map[tile_index(Nt, m, i)]);
             }
             bool any = false;
             for (int e = 1; e <= 3; ++e)
                 if (need[e]) {
                     any = true;
                     p->img[4 * t + e - 1] = (long long)p->shadow_bytes;
-                    p->shadow_bytes += img_bytes;
-                    if (e == MXP_FP32) {
+                    if (native && e == MXP_FP16) p->shadow_bytes += nat::image_bytes(nat::K_F16, p->nb);
+                    else if (native && e == MXP_FP8) p->shadow_bytes += nat::image_bytes(nat::K_F8, p->nb);
+                    else p->shadow_bytes += img_bytes;
+                    // TF32 remainder: FP32 image of an operand stored at FP32 or finer
+                    if (e == MXP_FP32 && (!native || pt <= MXP_FP32)) {
                         p->img[4 * t + 3] = (long long)p->shadow_bytes;
                         p->shadow_bytes += img_bytes;
                     }
@@ -364,42 +393,26 @@ void plan_images(mxp_plan_s* p) {
                 p->qtile[t] = 1;
             }
         p->oz_on = true;
-        size_t fr = 0, tot = 0;
-        int cur = 0;
-        cudaGetDevice(&cur);
-        if (cudaSetDevice(p->device) == cudaSuccess && cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
-            const double pool = (double)sizeof(double) * p->nb * p->nb * T;
-            if (pool + (double)p->shadow_bytes > (double)fr + (double)p->ws_bytes - 2e9) {  // does not fit: DMMA
-                p->oz_img.assign(T, -1);
-                p->shadow_bytes = before;
-                p->oz_on = false;
-                for (int64_t t = 0; t < T; ++t) p->qtile[t] = 0;
-                for (int64_t t = 0; t < T; ++t)
-                    if (p->map[t] != MXP_FP64) p->qtile[t] = 1;
-                for (int64_t t = 0; t < T; ++t)
-                    for (int e = 0; e < 4; ++e)
-                        if (p->img[4 * t + e] >= 0) p->qtile[t] = 1;
-                for (int64_t k = 0; k < Nt; ++k) p->qtile[tile_index(Nt, k, k)] = 0;
-            }
+        if (!fits_beside_pool(p, (double)p->shadow_bytes)) {  // does not fit: DMMA
+            p->oz_img.assign(T, -1);
+            p->shadow_bytes = before;
+            p->oz_on = false;
+            for (int64_t t = 0; t < T; ++t) p->qtile[t] = 0;
+            for (int64_t t = 0; t < T; ++t)
+                if (p->map[t] != MXP_FP64) p->qtile[t] = 1;
+            for (int64_t t = 0; t < T; ++t)
+                for (int e = 0; e < 4; ++e)
+                    if (p->img[4 * t + e] >= 0) p->qtile[t] = 1;
+            for (int64_t k = 0; k < Nt; ++k) p->qtile[tile_index(Nt, k, k)] = 0;
         }
-        cudaGetLastError();
-        cudaSetDevice(cur);
     }
-    if (images && !p->oz_on) {  // full size known now: re-check, else use the register-staged engine
-        size_t fr = 0, tot = 0;
-        int cur = 0;
-        cudaGetDevice(&cur);
-        if (cudaSetDevice(p->device) == cudaSuccess && cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
-            const double pool = (double)sizeof(double) * p->nb * p->nb * T;
-            if (pool + (double)p->shadow_bytes > (double)fr + (double)p->ws_bytes - 2e9) {  // 2 GB headroom
-                p->img.assign(4 * T, -1);
-                p->shadow_bytes = 0;
-                for (int64_t t = 0; t < T; ++t) p->qtile[t] = p->map[t] != MXP_FP64 ? 1 : 0;
-                for (int64_t k = 0; k < p->Nt; ++k) p->qtile[tile_index(p->Nt, k, k)] = 0;
-            }
-        }
-        cudaGetLastError();
-        cudaSetDevice(cur);
+    p->nat_on = native && p->oz_on;
+    if (images && !p->oz_on && !fits_beside_pool(p, (double)p->shadow_bytes)) {
+        // full size known now: does not fit -> the register-staged engine
+        p->img.assign(4 * T, -1);
+        p->shadow_bytes = 0;
+        for (int64_t t = 0; t < T; ++t) p->qtile[t] = p->map[t] != MXP_FP64 ? 1 : 0;
+        for (int64_t k = 0; k < p->Nt; ++k) p->qtile[tile_index(p->Nt, k, k)] = 0;
     }
 }
 
@@ -426,7 +439,7 @@ size_t flag_ints(const mxp_plan_s* p) {
     // + Ozaki-mode task claims (TRSM, QUANT: T * nb/64 each; PREP: T) + timeout diagnostics (8)
     // + per-SM claim words of k_sched in the Ozaki mode (256) + counter2 (last)
     return (size_t)(2 + 7 * p->T + p->T * blocks_per_tile(p->nb) + 2 * p->Nt + (2 * p->T * (p->nb / 64) + p->T) +
-                    8 + 256 + 1);
+                    24 + 256 + 1);
 }
 
 // Tile slots of the device pool: every lower tile in core; with
@@ -485,8 +498,8 @@ bool plan_slots(mxp_plan_s* p, int64_t C) {
 }
 
 struct Layout {
-    size_t slot, prev, epoch, flags, flags_bytes, expected, items, wbuf, stats, prec, amax_x, amax_s, args, qtile, img,
-        ozimg, solve, shadow, pool, total;
+    size_t slot, prev, epoch, flags, flags_bytes, expected, items, wbuf, stats, prec, amax_x, amax_s, iscale, args,
+        qtile, img, ozimg, solve, shadow, pool, total;
 };
 
 Layout layout(const mxp_plan_s* p) {
@@ -516,6 +529,8 @@ Layout layout(const mxp_plan_s* p) {
     off += align_up((size_t)p->T, 256);
     L.amax_s = off;
     off += align_up(sizeof(double) * (size_t)p->T, 256);
+    L.iscale = off;
+    off += align_up(sizeof(double) * 2 * (size_t)p->T, 256);
     L.args = off;
     off += align_up(sizeof(SchedArgs), 256);
     L.qtile = off;
@@ -581,6 +596,7 @@ void bind_workspace(mxp_plan_s* p) {
     p->d_stats = (unsigned long long*)(p->ws + L.stats);
     p->d_prec = (uint8_t*)(p->ws + L.prec);
     p->d_amax_s = (double*)(p->ws + L.amax_s);
+    p->d_iscale = (double*)(p->ws + L.iscale);
     p->d_args = (SchedArgs*)(p->ws + L.args);
     p->d_qtile = (uint8_t*)(p->ws + L.qtile);
     p->d_img = (long long*)(p->ws + L.img);
@@ -812,7 +828,7 @@ std::string sched_timeout_detail(mxp_plan_s* p) {
         cudaGetLastError();
         return "";
     }
-    const int* d = f.data() + nf - 1 - 256 - 8;
+    const int* d = f.data() + nf - 1 - 256 - 24;
     if (!d[7]) return "";
     const int64_t T = p->T, NB = blocks_per_tile(p->nb);
     int64_t o = d[0];
@@ -829,7 +845,20 @@ std::string sched_timeout_detail(mxp_plan_s* p) {
     } else {
         what = "flag offset " + std::to_string(o);
     }
+    // progress of the first tile column (ready / trsm_done / quant_done / gemm_done of tiles (m, 0))
+    std::string col0;
+    for (int64_t m = 0; m < std::min<int64_t>(p->Nt, 4); ++m) {
+        const int64_t t = tile_index(p->Nt, m, 0);
+        col0 += " (" + std::to_string(m) + ",0):" + std::to_string(f[2 + t]) + "/" + std::to_string(f[2 + 2 * T + t]) +
+                "/" + std::to_string(f[2 + 3 * T + t]) + "/" + std::to_string(f[2 + T + t]);
+    }
     return " [first timeout: " + what + " target " + std::to_string(d[1]) + " value " + std::to_string(d[2]) +
+           "; column 0 ready/trsm/quant/gemm" + col0 + "; k_tc CTAs started/ended " + std::to_string(d[8]) + "/" +
+           std::to_string(d[9]) + ", k_sched " + std::to_string(d[10]) + "/" + std::to_string(d[11]) +
+           ", k_tc GEMM tasks begun/done " + std::to_string(d[12]) + "/" + std::to_string(d[13]) +
+           ", k_tc first start - k_sched first start " + std::to_string(d[14] - d[15]) + " us" +
+           ", k_tc CTAs launched " + std::to_string(d[16]) + " first launch - k_sched start " +
+           std::to_string(d[17] - d[15]) + " us" +
            " column " + std::to_string(d[6]) + " sm " + std::to_string(d[3]) + " block " + std::to_string(d[4]) + "/" +
            std::to_string(d[5]) + "; tickets k_sched " + std::to_string(f[0]) + "/" + std::to_string(p->items.size()) +
            " k_tc " + std::to_string(f[nf - 1]) + "/" + std::to_string(p->items2.size()) + "]";
@@ -873,6 +902,13 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     CK(cudaStreamWaitEvent(p->sU, p->ev_start, 0));
     CK(cudaStreamWaitEvent(p->sP, p->ev_start, 0));
     if (p->oz_on) {
+        // The two persistent kernels of the Ozaki mode must share every SM (one
+        // k_tc + one k_sched CTA).  When both wait on the same event (e.g. behind
+        // the input quantization), k_sched CTAs were observed to land first and
+        // keep k_tc off the SMs until the 20 s scheduler timeout; launched in host
+        // order onto idle streams, k_tc lands first.  So the host waits for the
+        // preceding work (a few microseconds after it ends) before the launches.
+        CK(cudaEventSynchronize(p->ev_start));
         if (!p->sT) {  // created only when used: every stream takes a hardware queue, and parked
                        // streams (stream memory waits) must not share one with the others
             int lo = 0, hi = 0;
@@ -916,12 +952,14 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     a.nitems2 = (int)p->items2.size();
     a.counter2 = p->d_flags + flag_ints(p) - 1;
     a.sm_claim = a.counter2 - 256;
-    a.tdiag = a.sm_claim - 8;
+    a.tdiag = a.sm_claim - 24;
     a.task_claim = a.tdiag - (2 * T * (p->nb / 64) + T);
     a.qtile = p->d_qtile;
     a.img = (p->mxp && p->shadow_bytes > 0) ? p->d_img : nullptr;  // (null when no fp32 image exists)
     a.shadow = p->d_shadow;
     a.tc_engine = p->tc_engine;
+    a.native = p->nat_on ? 1 : 0;
+    a.iscale = p->d_iscale;
     a.amax_x = p->d_amax_x;
     a.amax_s = p->d_amax_s;
     a.gemm_expected = p->d_expected;
@@ -1290,7 +1328,7 @@ int mxp_chol_plan_set(mxp_plan_t p, mxp_attr_t key, int64_t v) {
         p->list_uploaded = false;
         return MXP_OK;
     case MXP_ATTR_TC_ENGINE:
-        if (v < 0 || v > 2) return -3;
+        if (v < 0 || v > 3) return -3;
         if (p->ws && !p->ws_owned) return MXP_ESTATE;  // changes the task list / image sizes
         if (p->ws_owned) {
             cudaFree(p->ws);
@@ -1347,6 +1385,13 @@ int mxp_chol_plan_get(mxp_plan_t p, mxp_attr_t key, int64_t* v) {
     case MXP_ATTR_POOL_SLOTS: *v = pool_slots(p); return MXP_OK;
     case MXP_ATTR_NT: *v = p->Nt; return MXP_OK;
     case MXP_ATTR_IMAGE_BYTES: plan_images(p); *v = (int64_t)p->shadow_bytes; return MXP_OK;
+    case MXP_ATTR_TC_ENGINE_USED: {
+        plan_images(p);
+        bool any_img = false;
+        for (long long o : p->img) any_img |= o >= 0;
+        *v = !p->mxp ? -1 : p->tc_engine == 0 ? 0 : p->nat_on ? 3 : any_img ? 1 : 2;
+        return MXP_OK;
+    }
     default: return -2;
     }
 }

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include "../../include/mxp_chol.h"
+#include "internal.h"
 
 namespace {
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
@@ -76,6 +77,7 @@ extern "C" int mxp_generate_plgsy_device(int64_t n, uint64_t seed, double* A, in
     s = s ^ (s >> 31);
     dim3 g;
     grid_for(n, g);
+    MXP_CARVEOUT_MAX(k_gen_plgsy);
     k_gen_plgsy<<<g, 256, 0, (cudaStream_t)stream>>>(n, s, A, lda);
     return cudaGetLastError() == cudaSuccess ? MXP_OK : MXP_ECUDA;
 }
@@ -86,6 +88,7 @@ extern "C" int mxp_generate_kms_device(int64_t n, double rho, double* A, int64_t
     if (lda < n) return -4;
     dim3 g;
     grid_for(n, g);
+    MXP_CARVEOUT_MAX(k_gen_kms);
     k_gen_kms<<<g, 256, 0, (cudaStream_t)stream>>>(n, rho, A, lda);
     return cudaGetLastError() == cudaSuccess ? MXP_OK : MXP_ECUDA;
 }
@@ -101,6 +104,7 @@ extern "C" int mxp_generate_matern_device(int64_t n, const double* xy_dev, doubl
     if (lda < n) return -7;
     dim3 g;
     grid_for(n, g);
+    MXP_CARVEOUT_MAX(k_gen_matern);
     k_gen_matern<<<g, 256, 0, (cudaStream_t)stream>>>(n, xy_dev, sigma2, range_a, nugget, A, lda);
     return cudaGetLastError() == cudaSuccess ? MXP_OK : MXP_ECUDA;
 }

@@ -6,6 +6,21 @@
 
 namespace mxp {
 
+// Every kernel of the library asks for the maximum shared-memory carve-out.
+// An SM keeps the L1/shared split of the CTAs resident on it, and a CTA that
+// fits the current split does not make the SM switch: if a small kernel (pack,
+// input quantization, ...) leaves SMs at a small split and a k_sched CTA lands
+// there, the tensor-core kernel k_tc (~150 KB) cannot join it until k_sched
+// exits -- the two persistent kernels of the Ozaki mode must share every SM.
+#define MXP_CARVEOUT_MAX(kernel)                                                                   \
+    do {                                                                                           \
+        static bool mxp_carveout_done_ = false;                                                    \
+        if (!mxp_carveout_done_) {                                                                 \
+            cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);     \
+            mxp_carveout_done_ = true;                                                             \
+        }                                                                                          \
+    } while (0)
+
 // Tile pool: every lower tile (i,j) of the matrix lives in a pool slot of
 // nb*nb elements, column-major inside the tile (ld = nb).  slot_of[t] maps
 // the column-major lower-tile index t(i,j) to its slot (in-core: identity).
@@ -78,8 +93,13 @@ struct SchedArgs {
     int nitems2;               //   schedule, e.g. when a profiler serializes the kernels); k_sched
     int* counter2;             //   takes the non-GEMM subsequence (items); both claim non-GEMM tasks
     int* task_claim;           //   by CAS here: TRSM [T*R] | QUANT [T*R] | PREP [T]  (R = nb/64)
-    int* tdiag;                // [8] first timed-out wait: flag offset from `ready`, target, value, smid,
+    int* tdiag;                // [24] first timed-out wait: flag offset from `ready`, target, value, smid,
                                //     block, grid, column, taken (host reports it in mxp_last_error)
+    // native-width operand images (tc_native.cuh; MXP_ATTR_TC_ENGINE = 3, tensor-core kernel k_tc):
+    // img[4t+1] = fp16 codes of cast_FP16(L) for FP16 outputs, img[4t+2] = E4M3 codes of cast_FP8(L)
+    // for FP8 outputs, iscale[2t + kind] = the power-of-two scale of those codes (code = value * scale)
+    int native;
+    double* iscale;            // [2T]
     int* sm_claim;             // [256] k_sched CTAs per SM in the Ozaki mode (extras leave at once,
                                //       keeping room for the k_tc CTA of every SM)
     unsigned long long* stats; // optional diagnostics (MXP_ATTR_PROFILE): see STAT_*

@@ -46,11 +46,13 @@ __global__ void k_unpack(double* __restrict__ A, int64_t lda, int64_t n, const d
 void launch_pack_f64(const double* A, int64_t lda, int64_t n, double* pool, const int32_t* slot,
                      int64_t Nt, int64_t nb, int64_t col0, int64_t col1, cudaStream_t s, int rank, int nranks) {
     dim3 grid((unsigned)(nb / 8), (unsigned)(col1 - col0), (unsigned)(Nt - col0));
+    MXP_CARVEOUT_MAX(k_pack);
     k_pack<<<grid, 256, 0, s>>>(A, lda, n, pool, slot, Nt, nb, col0, rank, nranks);
 }
 void launch_unpack_f64(double* A, int64_t lda, int64_t n, const double* pool, const int32_t* slot,
                        int64_t Nt, int64_t nb, int64_t col0, int64_t col1, cudaStream_t s) {
     dim3 grid((unsigned)(nb / 8), (unsigned)(col1 - col0), (unsigned)(Nt - col0));
+    MXP_CARVEOUT_MAX(k_unpack);
     k_unpack<<<grid, 256, 0, s>>>(A, lda, n, pool, slot, Nt, nb, col0);
 }
 
@@ -63,6 +65,7 @@ __global__ void k_logdet_final(const double* parts, int64_t Nt, double* out) {
     *out = 2.0 * s;
 }
 void launch_logdet_final(const double* parts, int64_t Nt, double* out, cudaStream_t s) {
+    MXP_CARVEOUT_MAX(k_logdet_final);
     k_logdet_final<<<1, 1, 0, s>>>(parts, Nt, out);
 }
 
@@ -92,6 +95,7 @@ __global__ void k_tile_norms(const double* __restrict__ A, int64_t lda, int64_t 
 void launch_tile_norms(const double* A, int64_t lda, int64_t n, int64_t nb, double* norms, cudaStream_t s) {
     int64_t Nt = (n + nb - 1) / nb;
     dim3 grid((unsigned)Nt, (unsigned)Nt, 1);
+    MXP_CARVEOUT_MAX(k_tile_norms);
     k_tile_norms<<<grid, 256, 0, s>>>(A, lda, n, nb, Nt, norms);
 }
 

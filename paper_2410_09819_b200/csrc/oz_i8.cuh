@@ -274,12 +274,15 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
             __syncwarp();
         }
         // drain: ACC levels of tile i -> fp64, scaled by the row scales
+        // (threads 0..127 = TMEM lanes; in k_tc warp 4 only join the barriers)
+        const bool wk = tid < 128;
         if (tid < BN) s_sb[tid] = __ldcg(src(i).sb + tid);
-        const double sa_r = __ldcg(src(i).sa + tid);
-        tc::mbar_wait(tbar, (uint32_t)(i & 1));
+        const double sa_r = wk ? __ldcg(src(i).sa + tid) : 0.0;
+        if (wk) tc::mbar_wait(tbar, (uint32_t)(i & 1));
         tc::fence_after();
         __syncthreads();  // s_sb visible
         __syncwarp();     // (converged warp for the .sync.aligned TMEM loads)
+        if (wk) {
 #pragma unroll
         for (int g8 = 0; g8 < BN / 8; ++g8) {
             int x[S][8];
@@ -295,13 +298,16 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
                 acc[g8 * 8 + j] = fma(v * sa_r, s_sb[g8 * 8 + j], acc[g8 * 8 + j]);
             }
         }
+        }
         tc::fence_before();
         __syncthreads();  // TMEM and s_sb free for tile i + 1
     }
+    if (tid < 128) {
 #pragma unroll
-    for (int j = 0; j < BN; ++j) {
-        double* p = C + tid + (int64_t)j * ldc;
-        __stcg(p, __ldcg(p) - acc[j]);
+        for (int j = 0; j < BN; ++j) {
+            double* p = C + tid + (int64_t)j * ldc;
+            __stcg(p, __ldcg(p) - acc[j]);
+        }
     }
     __syncthreads();
     if (tid == 0) {

@@ -25,6 +25,7 @@
 #include "quant.cuh"
 #include "tc_block.cuh"
 #include "oz_i8.cuh"
+#include "tc_native.cuh"
 
 namespace mxp {
 
@@ -428,10 +429,14 @@ __device__ __noinline__ bool task_gemm_img(const SchedArgs& a, int64_t m, int64_
             const int64_t ta = tile_index(Nt, m, cur_n), tb = tile_index(Nt, k, cur_n);
             const int ea = a.prec[ta] > cprec ? a.prec[ta] : cprec;
             const int eb = a.prec[tb] > cprec ? a.prec[tb] : cprec;
-            ahi = a.shadow + a.img[4 * ta + ea - 1] + aoff;
-            bhi = a.shadow + a.img[4 * tb + eb - 1] + boff;
-            alo = (THREE && ea == P_FP32) ? a.shadow + a.img[4 * ta + 3] + aoff : nullptr;
-            blo = (THREE && eb == P_FP32) ? a.shadow + a.img[4 * tb + 3] + boff : nullptr;
+            // tf32 images: slot e - 1 of e = max(c, p); native mode: the FP32 consumers' slot 0
+            // (values of cast_max(FP32, p)), remainder slot 3 only for operands stored at FP32 or finer
+            ahi = a.shadow + a.img[4 * ta + (a.native ? 0 : ea - 1)] + aoff;
+            bhi = a.shadow + a.img[4 * tb + (a.native ? 0 : eb - 1)] + boff;
+            const bool la = THREE && (a.native ? a.img[4 * ta + 3] >= 0 : ea == P_FP32);
+            const bool lb = THREE && (a.native ? a.img[4 * tb + 3] >= 0 : eb == P_FP32);
+            alo = la ? a.shadow + a.img[4 * ta + 3] + aoff : nullptr;
+            blo = lb ? a.shadow + a.img[4 * tb + 3] + boff : nullptr;
         }
         const int64_t o = kc * tc::SUB_BYTES;
         ++kc;
@@ -439,6 +444,60 @@ __device__ __noinline__ bool task_gemm_img(const SchedArgs& a, int64_t m, int64_
     };
     double* Ct = tile_ptr(a.pool, a.slot, Nt, nb, m, k) + bi * 128 + bj * 128 * nb;
     tc::block_gemm_img<THREE, NST>(Ct, nb, src, nsteps, smem, tmem);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        st_release(chunk_flag, (int)c + 1);
+        atom_add_release(a.gemm_done + t, 1);
+        if (a.stats) {
+            atomicAdd(a.stats + STAT_GEMM_BUSY, globaltimer() - tw0);
+            atomicAdd(a.stats + STAT_GEMM_N, 1ull);
+        }
+    }
+    return true;
+}
+
+// GEMM task of an FP16 / FP8 output tile at native operand width (tc_native.cuh):
+// C(m,k)[128x128 block b] -= sum over the chunk of cast_c(L(m,n)) cast_c(L(k,n))^T
+// as fp16 (kind::f16) or E4M3 (kind::f8f6f4) code products, rescaled per K tile.
+template <int KIND>
+__device__ __noinline__ bool task_gemm_nat(const SchedArgs& a, int64_t m, int64_t k, int64_t b, int64_t c,
+                                           uint8_t* smem, uint32_t tmem, int* s_flag) {
+    const int64_t Nt = a.Nt, nb = a.nb, S = nb / 128;
+    const int64_t bi = b % S, bj = b / S;
+    const int64_t t = tile_index(Nt, m, k);
+    int64_t n0, n1;
+    chunk_range(k, c, a.KC, n0, n1);
+    int* chunk_flag = a.blk_chunk + t * a.NB + b;
+    uint64_t tw0 = 0;
+    if (threadIdx.x == 0) {
+        if (a.stats) tw0 = globaltimer();
+        bool ok = wait_input(a, t, k);
+        for (int64_t n = n0; n < n1 && ok; ++n)
+            ok = wait_flag(a.ready + tile_index(Nt, m, n), a.epoch, a, k) &&
+                 wait_flag(a.ready + tile_index(Nt, k, n), a.epoch, a, k);
+        if (ok) ok = wait_flag(chunk_flag, (int)c, a, k);
+        *s_flag = ok;
+        if (a.stats) {
+            uint64_t tw1 = globaltimer();
+            atomicAdd(a.stats + STAT_GEMM_WAIT, tw1 - tw0);
+            tw0 = tw1;
+        }
+    }
+    __syncthreads();
+    if (!*s_flag) return false;
+    const int slot = 1 + KIND;  // img[4t+1]: fp16 codes, img[4t+2]: E4M3 codes
+    auto src = [&](int i) {
+        const int64_t n = n0 + i;
+        const int64_t ta = tile_index(Nt, m, n), tb = tile_index(Nt, k, n);
+        nat::NatTile o;
+        o.a = a.shadow + a.img[4 * ta + slot] + nat::chunk_offset(KIND, nb, bi, 0);
+        o.b = a.shadow + a.img[4 * tb + slot] + nat::chunk_offset(KIND, nb, bj, 0);
+        nat::inv_scales(__ldcg(a.iscale + 2 * ta + KIND), __ldcg(a.iscale + 2 * tb + KIND), o.inv0, o.inv1);
+        return o;
+    };
+    double* Ct = tile_ptr(a.pool, a.slot, Nt, nb, m, k) + bi * 128 + bj * 128 * nb;
+    nat::block_gemm<KIND>(Ct, nb, src, (int)(n1 - n0), (int)(nb / nat::ke(KIND)), smem, tmem);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -582,22 +641,54 @@ __device__ __noinline__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k
             const uint32_t off = tc::sw_offset(row & 127, col & 15);
 #pragma unroll
             for (int e = 0; e < 3; ++e) {
-                if (!im[e]) continue;
+                if (!im[e] || (a.native && e > 0)) continue;
                 float f[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) f[i] = (float)apply_cast(ce[e], x[i]);
                 uint8_t* dst = im[e] + chunk * tc::SUB_BYTES + off;
-                if (e == 0) {  // FP32: hi = RNE_tf32(v), lo = RNE_tf32(v - hi)
+                if (e == 0 && im[3]) {  // FP32: hi = RNE_tf32(v), lo = RNE_tf32(v - hi)
                     float h[4], l[4];
 #pragma unroll
                     for (int i = 0; i < 4; ++i) h[i] = tc::rne_tf32(f[i]), l[i] = tc::rne_tf32(f[i] - h[i]);
                     __stcg(reinterpret_cast<float4*>(dst), make_float4(h[0], h[1], h[2], h[3]));
                     __stcg(reinterpret_cast<float4*>(im[3] + chunk * tc::SUB_BYTES + off),
                            make_float4(l[0], l[1], l[2], l[3]));
-                } else {
+                } else {  // (native FP32 image of an FP16 / E4M3 operand: its values are exact in TF32)
                     __stcg(reinterpret_cast<float4*>(dst), make_float4(f[0], f[1], f[2], f[3]));
                 }
             }
+        }
+    }
+    if (a.native && (im[1] || im[2])) {  // native-width code images (tc_native.cuh) of cast_FP16 / cast_FP8
+        sync_workers();
+        // scale of the codes: the stored scale when the tile is stored at or below the image's
+        // precision (up-cast: the stored codes themselves, exact in fp16 / E4M3), else the
+        // down-cast's own scale from the stored amax (G11)
+        const double s16 = p >= P_FP16 ? sc : tile_scale(P_FP16, amax_st);
+        const double s8 = p == P_FP8 ? sc : tile_scale(P_FP8, amax_st);
+        const Cast c16 = make_cast(p, P_FP16, amax_st), c8 = make_cast(p, P_FP8, amax_st);
+        const int tid = threadIdx.x, row = (int)(r * 64) + (tid & 63), half = tid >> 6;
+        const int64_t c0 = half * (nb / 2), c1 = c0 + nb / 2;
+        for (int64_t k0 = c0; k0 < c1; k0 += 16) {
+            double x[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) x[e] = __ldcg(X + (tid & 63) + (k0 + e) * nb);
+            if (im[1]) {
+                double y[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) y[e] = apply_cast(c16, x[e]);
+                nat::write_f16_16(im[1], nb, row, (int)k0, y, s16);
+            }
+            if (im[2]) {
+                double y[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) y[e] = apply_cast(c8, x[e]);
+                nat::write_f8_16(im[2], nb, row, (int)k0, y, s8);
+            }
+        }
+        if (tid == 0) {
+            a.iscale[2 * t + 0] = s16;
+            a.iscale[2 * t + 1] = s8;
         }
     }
     if (a.oz_img && a.oz_img[t] >= 0) {  // int8 slices of the stored values (FP64 GEMM operands)
@@ -605,6 +696,7 @@ __device__ __noinline__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k
         sync_workers();
         oz_slice_rows(a, X, r, a.shadow + a.oz_img[t], red);
     }
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // images are read by bulk copies
     __threadfence();
     sync_workers();
     if (threadIdx.x == 0) {
@@ -971,6 +1063,10 @@ __global__ void __launch_bounds__(CC::NT, 3) k_sched(const SchedArgs a_param, co
         if (s_idx > 0) return;
         __syncthreads();
     }
+    if (threadIdx.x == 0) {
+        atomicAdd(a.tdiag + 10, 1);
+        atomicCAS(a.tdiag + 15, 0, (int)((globaltimer() >> 10) & 0x3FFFFFFF) | 1);
+    }
     // tcgen05 state in the last 32 bytes (padding of the last B row of the DMMA
     // pipeline, never touched by it): two mbarriers + the TMEM base address.
     uint8_t* smem_b = reinterpret_cast<uint8_t*>(smem);
@@ -1049,6 +1145,7 @@ __global__ void __launch_bounds__(CC::NT, 3) k_sched(const SchedArgs a_param, co
         __syncthreads();
         if (threadIdx.x < 32) tc::tmem_dealloc(tmem, tc::TMEM_COLS);
     }
+    if (threadIdx.x == 0) atomicAdd(a.tdiag + 11, 1);
     if (a.stats && threadIdx.x == 0) atomicMax(a.stats + STAT_TEND, globaltimer());
 }
 
@@ -1063,6 +1160,9 @@ __global__ void __launch_bounds__(CC::NT, 3) k_sched(const SchedArgs a_param, co
 // k_sched holds for it), and k_sched only takes work off it -- a task claimed
 // by k_sched depends on earlier tasks only, which k_tc or k_sched finish.
 // (Profilers that serialize kernels run k_tc alone: still correct.)
+// (4 warps: with one k_sched CTA beside it every SM sub-partition holds one
+// warp of each kernel -- 255 + 168 registers x 32 lanes fit its 16K registers;
+// a fifth warp would not, and k_tc would wait for k_sched to exit)
 __global__ void __launch_bounds__(128, 1) k_tc(const SchedArgs* __restrict__ ap) {
     const SchedArgs& a = *ap;
     const int id = (int)smid();
@@ -1070,11 +1170,19 @@ __global__ void __launch_bounds__(128, 1) k_tc(const SchedArgs* __restrict__ ap)
     extern __shared__ __align__(1024) uint8_t smem_t[];
     __shared__ int s_idx, s_flag;
     __shared__ uint32_t tmem_slot;
+    if (threadIdx.x == 0) {
+        atomicAdd(a.tdiag + 16, 1);
+        atomicCAS(a.tdiag + 17, 0, (int)((globaltimer() >> 10) & 0x3FFFFFFF) | 1);
+    }
     if (threadIdx.x < 32) tc::tmem_alloc(&tmem_slot, oz::TMEM_COLS);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t tmem = tmem_slot;
+    if (threadIdx.x == 0) {  // (diagnostics: CTAs started / ended, first start in us)
+        atomicAdd(a.tdiag + 8, 1);
+        atomicCAS(a.tdiag + 14, 0, (int)((globaltimer() >> 10) & 0x3FFFFFFF) | 1);
+    }
     if (a.stats && threadIdx.x == 0) atomicMin(a.stats + STAT_T0, globaltimer());
     while (true) {
         if (threadIdx.x == 0) {
@@ -1093,18 +1201,24 @@ __global__ void __launch_bounds__(128, 1) k_tc(const SchedArgs* __restrict__ ap)
         double* smem_d = reinterpret_cast<double*>(smem_t);
         if (it.x == ITEM_GEMM) {
             const int cp = a.prec[tile_index(a.Nt, m, k)];
+            if (threadIdx.x == 0) atomicAdd(a.tdiag + 12, 1);
             if (cp == P_FP64)
                 task_gemm_oz(a, m, k, it.w >> 16, it.w & 0xFFFF, smem_t, tmem, &s_flag);
             else if (cp == P_FP32)
                 task_gemm_img<true, 4>(a, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_t, tmem, &s_flag);
+            else if (a.native && cp == P_FP16)
+                task_gemm_nat<nat::K_F16>(a, m, k, it.w >> 16, it.w & 0xFFFF, smem_t, tmem, &s_flag);
+            else if (a.native)
+                task_gemm_nat<nat::K_F8>(a, m, k, it.w >> 16, it.w & 0xFFFF, smem_t, tmem, &s_flag);
             else
                 task_gemm_img<false, 4>(a, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_t, tmem, &s_flag);
+            if (threadIdx.x == 0) atomicAdd(a.tdiag + 13, 1);
         } else {
             if (threadIdx.x == 0) s_flag = claim_task(a, it);
             __syncthreads();
             const bool mine = s_flag;
             __syncthreads();
-            if (mine) {
+            if (mine && threadIdx.x < 128) {  // the 128 workers (named barrier 1); warp 4 waits below
                 if (it.x == ITEM_POTRF) task_potrf_fallback(a, k, smem_d, &s_flag);
                 else if (it.x == ITEM_PREP) task_prep(a, m, k, smem_d + CC::LDA_S + CC::BM, &s_flag);
                 else if (it.x == ITEM_TRSM) task_trsm_ool(a, m, k, it.w, smem_d, &s_flag);
@@ -1115,6 +1229,7 @@ __global__ void __launch_bounds__(128, 1) k_tc(const SchedArgs* __restrict__ ap)
     }
     tc::fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(a.tdiag + 9, 1);
     if (threadIdx.x < 32) tc::tmem_dealloc(tmem, oz::TMEM_COLS);
     if (a.stats && threadIdx.x == 0) atomicMax(a.stats + STAT_TEND, globaltimer());
 }
@@ -1165,6 +1280,7 @@ void launch_matern_tile_norms(const double* xy, int64_t n, int64_t nb, double si
                               double nugget, double* norms, cudaStream_t s) {
     int64_t Nt = (n + nb - 1) / nb;
     dim3 grid((unsigned)Nt, (unsigned)Nt, 1);
+    MXP_CARVEOUT_MAX(k_matern_tile_norms);
     k_matern_tile_norms<<<grid, 256, 0, s>>>(xy, n, nb, Nt, sigma2, range_a, nugget, norms);
 }
 
@@ -1199,11 +1315,14 @@ __global__ void k_tile_quantize(double* pool, const int32_t* slot, const uint8_t
 void launch_input_quantize(double* pool, const int32_t* slot, const uint8_t* prec, int64_t Nt, int64_t nb,
                            unsigned long long* amax_x, double* amax_s, cudaStream_t s, int rank, int nranks) {
     dim3 grid((unsigned)Nt, (unsigned)Nt, 8);
+    MXP_CARVEOUT_MAX(k_tile_amax);
     k_tile_amax<<<grid, 256, 0, s>>>(pool, slot, Nt, nb, amax_x, rank, nranks);
+    MXP_CARVEOUT_MAX(k_tile_quantize);
     k_tile_quantize<<<grid, 256, 0, s>>>(pool, slot, prec, Nt, nb, amax_x, amax_s, rank, nranks);
 }
 
 constexpr int POTRF_SMEM = (2 * PK * 8 > PC::SMEM_BYTES) ? 2 * PK * 8 : PC::SMEM_BYTES;
+constexpr int TC_SMEM = oz::SMEM_BYTES > nat::SMEM_BYTES ? oz::SMEM_BYTES : nat::SMEM_BYTES;
 
 void configure_sched() {
     static bool done = false;
@@ -1211,7 +1330,7 @@ void configure_sched() {
     cudaFuncSetAttribute(k_sched<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM_BYTES);
     cudaFuncSetAttribute(k_sched<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM_BYTES);
     cudaFuncSetAttribute(k_potrf_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF_SMEM);
-    cudaFuncSetAttribute(k_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, oz::SMEM_BYTES);
+    cudaFuncSetAttribute(k_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
     // every SM configured for the full 228 KB of shared memory: the Ozaki mode
     // co-schedules one k_tc CTA (~150 KB) and one k_sched CTA (~78 KB) per SM,
     // which a smaller carve-out picked for whichever kernel lands first would
@@ -1239,13 +1358,13 @@ void launch_sched(const SchedArgs& a, const SchedArgs* a_dev, bool mxp, int grid
 int tc_ctas_per_sm() {
     int occ = 0;
     configure_sched();
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tc, 128, oz::SMEM_BYTES);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tc, 128, TC_SMEM);
     return occ;
 }
 
 void launch_tc(const SchedArgs* a_dev, int grid, cudaStream_t s) {
     configure_sched();
-    k_tc<<<grid, 128, oz::SMEM_BYTES, s>>>(a_dev);
+    k_tc<<<grid, 128, TC_SMEM, s>>>(a_dev);
 }
 
 void launch_potrf_tile(const SchedArgs& a, int64_t k, cudaStream_t s) {

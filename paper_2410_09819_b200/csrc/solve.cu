@@ -102,11 +102,16 @@ void launch_forward_solve(const double* pool, const int32_t* slot, const double*
         configured = true;
     }
     for (int64_t k = 0; k < Nt; ++k) {
+        MXP_CARVEOUT_MAX(k_trsv_diag);
         k_trsv_diag<<<1, 256, sm_diag, s>>>(pool, slot, wbuf, Nt, nb, k, r, z);
+        MXP_CARVEOUT_MAX(k_trsv_gemv);
         if (k + 1 < Nt) k_trsv_gemv<<<(unsigned)((Nt - k - 1) * (nb / 128)), 256, sm_gemv, s>>>(pool, slot, Nt, nb, k, r, z);
     }
 }
 
-void launch_sumsq(const double* z, int64_t n, double* out, cudaStream_t s) { k_sumsq<<<1, 1024, 0, s>>>(z, n, out); }
+void launch_sumsq(const double* z, int64_t n, double* out, cudaStream_t s) {
+    MXP_CARVEOUT_MAX(k_sumsq);
+    k_sumsq<<<1, 1024, 0, s>>>(z, n, out);
+}
 
 }  // namespace mxp

@@ -230,20 +230,22 @@ __device__ void block_gemm_img(double* C, int64_t ldc, const Src& src, int nstep
         commit(fin);  // tracks every earlier tcgen05 op of this thread
     }
     __syncwarp();
-    // (a one-shot barrier: the per-stage ones may be several phases ahead of
-    // a thread that starts waiting early, and parity waits would alias)
-    mbar_wait(fin, 0);
-    fence_after();
-    const int warp = threadIdx.x >> 5, row = threadIdx.x;
-    const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+    if (threadIdx.x < 128) {  // TMEM lanes 0..127 (k_tc's warp 4 only join the barriers)
+        // (a one-shot barrier: the per-stage ones may be several phases ahead of
+        // a thread that starts waiting early, and parity waits would alias)
+        mbar_wait(fin, 0);
+        fence_after();
+        const int warp = threadIdx.x >> 5, row = threadIdx.x;
+        const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
 #pragma unroll 1
-    for (int c0 = 0; c0 < N; c0 += 32) {
-        float v[32];
-        tmem_ld32(tl + c0, v);
+        for (int c0 = 0; c0 < N; c0 += 32) {
+            float v[32];
+            tmem_ld32(tl + c0, v);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            double* p = C + row + (int64_t)(c0 + i) * ldc;
-            __stcg(p, __ldcg(p) - (double)v[i]);
+            for (int i = 0; i < 32; ++i) {
+                double* p = C + row + (int64_t)(c0 + i) * ldc;
+                __stcg(p, __ldcg(p) - (double)v[i]);
+            }
         }
     }
     fence_before();

@@ -1,0 +1,306 @@
+// tc_native.cuh -- GEMM tasks of tiles stored below FP64 at the operands'
+// native width on the 5th-gen tensor cores (sm_100a):
+//   output tile FP16 -> tcgen05.mma kind::f16    (fp16 codes, K = 16 / MMA)
+//   output tile FP8  -> tcgen05.mma kind::f8f6f4 (E4M3 codes, K = 32 / MMA)
+// with fp32 accumulation in TMEM (G12: "FP32 accumulation for FP16/FP8 tiles
+// with per-tile scaling", BASELINE north_star; P:42 minimum bytes per word,
+// P:46 low-precision tensor cores).
+//
+// Operands are the CODES of cast_c(L) (c = the output tile's precision, G12):
+// every operand tile carries one power-of-two scale per image (G11), so the
+// product of a K tile n is   sum_k codeA codeB = (A B^T)_n * sA_n * sB_n.
+// Scales differ from K tile to K tile, so the TMEM partial of each K tile is
+// drained and rescaled by 1/(sA_n sB_n) (exact: a power of two) into fp32
+// registers; two TMEM accumulators alternate so the drain of tile n overlaps
+// the MMAs of tile n+1 (one thread of warp 0 issues the bulk copies and the
+// MMAs; warps 0-3 = TMEM lanes 0-127 drain).
+//
+// Image of a tile (written once by its QUANT tasks): 16 KB chunks of 128 rows
+// x 128 bytes (64 fp16 or 128 E4M3 along K), chunk (rb, kc) at
+// (rb * (nb / KE) + kc) * 16 KB, each in the canonical K-major SWIZZLE_128B
+// layout: row r at r*128 B, its 16-byte unit u stored at unit u ^ (r % 8).
+// An A operand (128 output rows) and a B operand (128 output columns) are
+// both one row block of their tile's image.
+#pragma once
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "tc_tf32.cuh"
+
+namespace mxp {
+namespace nat {
+
+enum { K_F16 = 0, K_F8 = 1 };
+constexpr int BM = 128, BN = 128;
+constexpr int CHUNK = 128 * 128;            // bytes per operand chunk
+constexpr int STAGE_BYTES = 2 * CHUNK;      // A | B
+constexpr int NST = 4;                      // stages
+constexpr int SMEM_BYTES = 1024 + NST * STAGE_BYTES + 128;
+
+__host__ __device__ constexpr int ke(int kind) { return kind == K_F16 ? 64 : 128; }  // K per chunk
+__host__ __device__ constexpr int64_t image_bytes(int kind, int64_t nb) { return nb * nb * (kind == K_F16 ? 2 : 1); }
+__host__ __device__ constexpr int64_t chunk_offset(int kind, int64_t nb, int64_t rb, int64_t kc) {
+    return (rb * (nb / ke(kind)) + kc) * CHUNK;
+}
+// byte offset of byte `kb` (0..127) of row `row` (0..127) inside a chunk
+__host__ __device__ __forceinline__ uint32_t sw128(int row, int kb) {
+    return (uint32_t)(row * 128 + ((((kb >> 4) ^ row) & 7) << 4) + (kb & 15));
+}
+
+// UMMA smem descriptor: K-major SWIZZLE_128B, 8-row groups 1024 B apart (SBO)
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)1 << 16;              // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;    // SBO
+    d |= (uint64_t)1 << 46;              // version 1 (sm100)
+    d |= (uint64_t)2 << 61;              // SWIZZLE_128B
+    return d;
+}
+// instruction descriptor: D f32, A/B F16 (kind::f16) or E4M3 (kind::f8f6f4)
+// -- format code 0 in both kinds --, both K-major, M = 128, N = 128
+constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+template <int KIND>
+__device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+    if constexpr (KIND == K_F16)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+    else
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+}
+
+// 32 consecutive fp32 columns of this thread's TMEM lane <- v (then wait for the store)
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+        "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]),
+        "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]),
+        "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+        : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(mbar)) : "memory");
+}
+
+// One K tile of the walk: the first chunk of the A rows / B rows of this
+// block (consecutive K chunks follow at CHUNK strides) and 1/(sA sB) split
+// into two powers of two that are each representable in fp32.
+struct NatTile {
+    const uint8_t* a;
+    const uint8_t* b;
+    float inv0, inv1;
+};
+
+// Drain of K tile i by this warp (its 32 TMEM lanes): R += P(buf) * inv.
+// The running fp32 sum R lives in TMEM columns [256, 384) (no 128-register
+// accumulator); partial P in columns [128 buf, 128 buf + 128).
+__device__ __forceinline__ void drain_tile(uint32_t tl, int buf, bool first, const NatTile& t) {
+    const uint32_t tr = tl + 2 * BN;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32], r[32];
+        tc::tmem_ld32(tl + (uint32_t)(buf * BN + c0), v);
+        if (!first) {
+            tc::tmem_ld32(tr + (uint32_t)c0, r);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) r[j] = fmaf(v[j] * t.inv0, t.inv1, r[j]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) r[j] = (v[j] * t.inv0) * t.inv1;
+        }
+        tmem_st32(tr + (uint32_t)c0, r);
+    }
+}
+
+// C(128 x 128, fp64, column-major ldc) -= sum over ntiles K tiles of
+// (A_n B_n^T) = codes products * inv;  kt = chunks per K tile (nb / KE).
+// All 128 threads call; tmem: >= 384 allocated columns (two accumulators + the
+// running sum).  One elected thread of warp 0 issues the bulk copies and the
+// MMAs; warps 0-3 drain their TMEM lanes (= output rows): warps 1-3 as soon as
+// a K tile's accumulator is complete, warp 0 after it has queued the MMAs of
+// the next K tile (the tensor core works through them meanwhile).  Four
+// warps, not five: k_tc must stay co-resident with a k_sched CTA, and a fifth
+// 255-register warp fills one SM sub-partition's register file.
+template <int KIND, class Src>
+__device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, int kt, uint8_t* smem, uint32_t tmem) {
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + NST * STAGE_BYTES);
+    uint64_t* empty = full + NST;
+    uint64_t* tfull = empty + NST;  // [2] accumulator ready for the drain
+    uint64_t* tempty = tfull + 2;   // [2] accumulator drained (4 warps arrive)
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int G = ntiles * kt;
+    const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+    if (tid == 0) {
+        for (int i = 0; i < NST; ++i) tc::mbar_init(full + i, 1), tc::mbar_init(empty + i, 1);
+        for (int i = 0; i < 2; ++i) tc::mbar_init(tfull + i, 1), tc::mbar_init(tempty + i, 4);
+        tc::fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == 0) {
+        NatTile cur{};
+        int cur_i = -1;
+        auto issue = [&](int g) {  // bulk copies of K step g into its stage (elected lane)
+            const int st = g % NST, i = g / kt, kc = g - i * kt;
+            if (i != cur_i) cur = src(i), cur_i = i;
+            uint8_t* sa = base + st * STAGE_BYTES;
+            tc::mbar_expect_tx(full + st, (uint32_t)STAGE_BYTES);
+            tc::bulk_g2s(sa, cur.a + (int64_t)kc * CHUNK, CHUNK, full + st);
+            tc::bulk_g2s(sa + CHUNK, cur.b + (int64_t)kc * CHUNK, CHUNK, full + st);
+        };
+        auto refill = [&](int g) {  // stage of step g (its MMAs issued) -> step g + NST
+            if (g >= 0 && g + NST < G) {
+                tc::mbar_wait(empty + (g % NST), (uint32_t)((g / NST) & 1));
+                issue(g + NST);
+            }
+        };
+        if (lane == 0)
+            for (int g = 0; g < NST && g < G; ++g) issue(g);
+        for (int i = 0; i < ntiles; ++i) {
+            const int buf = i & 1;
+            if (lane == 0) {
+                if (i >= 2) tc::mbar_wait(tempty + buf, (uint32_t)(((i >> 1) - 1) & 1));
+                tc::fence_after();
+                const uint32_t d = tmem + (uint32_t)(buf * BN);
+                for (int kc = 0; kc < kt; ++kc) {
+                    const int g = i * kt + kc, st = g % NST;
+                    tc::mbar_wait(full + st, (uint32_t)((g / NST) & 1));
+                    tc::fence_after();
+                    const uint32_t sa = tc::smem_u32(base + st * STAGE_BYTES);
+                    const uint64_t ad = make_desc(sa), bd = make_desc(sa + CHUNK);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)  // 32 bytes of K per MMA: +2 in the 16-byte address field
+                        mma<KIND>(d, ad + 2 * kk, bd + 2 * kk, (kc | kk) ? 1u : 0u);
+                    tc::commit(empty + st);
+                    // refill the previous step's stage once its MMAs have read it (this step's
+                    // MMAs stay queued behind them); at the last step of a K tile the refill
+                    // waits until after this warp's drain
+                    if (kc + 1 < kt || i == 0) refill(g - 1);
+                }
+                tc::commit(tfull + buf);
+            }
+            __syncwarp();
+            if (i >= 1) {  // drain K tile i-1 while the tensor core runs tile i
+                const int pb = (i - 1) & 1;
+                const NatTile t = src(i - 1);
+                tc::mbar_wait(tfull + pb, (uint32_t)(((i - 1) >> 1) & 1));
+                tc::fence_after();
+                __syncwarp();
+                drain_tile(tl, pb, i == 1, t);
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(tempty + pb);
+                    refill(i * kt + kt - 2);  // the refill deferred at tile i's last step
+                }
+                __syncwarp();
+            }
+        }
+        {  // the last K tile
+            const int i = ntiles - 1, pb = i & 1;
+            const NatTile t = src(i);
+            tc::mbar_wait(tfull + pb, (uint32_t)((i >> 1) & 1));
+            tc::fence_after();
+            __syncwarp();
+            drain_tile(tl, pb, i == 0, t);
+            tc::fence_before();
+            __syncwarp();
+        }
+    } else {  // warps 1-3: drain every K tile as soon as it is complete
+        for (int i = 0; i < ntiles; ++i) {
+            const int buf = i & 1;
+            const NatTile t = src(i);
+            tc::mbar_wait(tfull + buf, (uint32_t)((i >> 1) & 1));
+            tc::fence_after();
+            __syncwarp();
+            drain_tile(tl, buf, i == 0, t);
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty + buf);
+        }
+    }
+    // C -= R (fp64 read-modify-write of this thread's output row)
+    {
+        const uint32_t tr = tl + 2 * BN;
+        const int row = tid;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+            float r[32];
+            tc::tmem_ld32(tr + (uint32_t)c0, r);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                double* p = C + row + (int64_t)(c0 + j) * ldc;
+                __stcg(p, __ldcg(p) - (double)r[j]);
+            }
+        }
+        tc::fence_before();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int i = 0; i < NST; ++i) tc::mbar_inval(full + i), tc::mbar_inval(empty + i);
+        for (int i = 0; i < 2; ++i) tc::mbar_inval(tfull + i), tc::mbar_inval(tempty + i);
+    }
+}
+
+// ---------------------------------------------------------------- images
+// Codes of 16 consecutive K elements [k0, k0+16) of row `row` of a tile into
+// its image (values x already on the grid of cast_c with scale s: x*s is an
+// exact fp16 / E4M3 code).
+__device__ __forceinline__ void write_f16_16(uint8_t* img, int64_t nb, int row, int k0, const double (&x)[16],
+                                             double s) {
+    uint32_t w[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const unsigned short lo = __half_as_ushort(__double2half(x[2 * e] * s));
+        const unsigned short hi = __half_as_ushort(__double2half(x[2 * e + 1] * s));
+        w[e] = (uint32_t)lo | ((uint32_t)hi << 16);
+    }
+    const int64_t rb = row >> 7, kc = k0 >> 6;
+    const int kb = (k0 & 63) * 2;
+    uint8_t* ch = img + chunk_offset(K_F16, nb, rb, kc);
+    __stcg(reinterpret_cast<uint4*>(ch + sw128(row & 127, kb)), make_uint4(w[0], w[1], w[2], w[3]));
+    __stcg(reinterpret_cast<uint4*>(ch + sw128(row & 127, kb + 16)), make_uint4(w[4], w[5], w[6], w[7]));
+}
+__device__ __forceinline__ void write_f8_16(uint8_t* img, int64_t nb, int row, int k0, const double (&x)[16],
+                                            double s) {
+    uint32_t w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        uint32_t b = 0;
+#pragma unroll
+        for (int q = 0; q < 4; q += 2) {
+            unsigned short pair;
+            asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;"
+                : "=h"(pair)
+                : "f"((float)(x[4 * e + q + 1] * s)), "f"((float)(x[4 * e + q] * s)));
+            b |= (uint32_t)pair << (8 * q);
+        }
+        w[e] = b;
+    }
+    const int64_t rb = row >> 7, kc = k0 >> 7;
+    uint8_t* ch = img + chunk_offset(K_F8, nb, rb, kc);
+    __stcg(reinterpret_cast<uint4*>(ch + sw128(row & 127, k0 & 127)), make_uint4(w[0], w[1], w[2], w[3]));
+}
+
+// 1/(sA sB) as two fp32 powers of two (sA, sB = 2^kA, 2^kB with |kA|, |kB| <= 127)
+__device__ __forceinline__ void inv_scales(double sa, double sb, float& inv0, float& inv1) {
+    int ea = ilogb(sa), eb = ilogb(sb);
+    int e = -(ea + eb);
+    int e0 = e > 120 ? 120 : (e < -120 ? -120 : e);
+    inv0 = scalbnf(1.f, e0);
+    inv1 = scalbnf(1.f, e - e0);
+}
+
+}  // namespace nat
+}  // namespace mxp

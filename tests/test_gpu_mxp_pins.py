@@ -14,7 +14,8 @@ from mxp_pins import cases, embed, scalar_case
 pytestmark = pytest.mark.gpu
 
 ENGINES = {"dmma_cast": {"tc_engine": 0}, "tc_images": {"tc_engine": 1}, "tc_regs": {"tc_engine": 2},
-           "ozaki_images": {"tc_engine": 1, "fp64_engine": 1}}
+           "ozaki_images": {"tc_engine": 1, "fp64_engine": 1},
+           "ozaki_native": {"tc_engine": 3, "fp64_engine": 1}}
 
 
 @pytest.mark.parametrize("case", cases(), ids=lambda c: c["name"])

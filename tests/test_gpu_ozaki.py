@@ -127,17 +127,20 @@ def test_ozaki_fewer_slices_accuracy(s):
     assert np.linalg.norm(A - L @ L.T) / np.linalg.norm(A) <= 2.0 ** (-7 * s + 8)
 
 
+@pytest.mark.parametrize("tc", [1, 3])
 @pytest.mark.parametrize("eps", [1e-5, 1e-8])
 @pytest.mark.parametrize("n,nb", [(2048, 128), (1900, 256)])
-def test_ozaki_mxp_matern_against_oracle(n, nb, eps):
+def test_ozaki_mxp_matern_against_oracle(n, nb, eps, tc):
     """MxP map with the FP64 tiles on the int8 tensor cores and the others on
-    the tf32 image engine (both in the k_tc kernel)."""
+    the tf32 image engine (tc=1) or at native width (tc=3: fp16 codes on
+    kind::f16, E4M3 codes on kind::f8f6f4, 3xTF32 for FP32), all in k_tc."""
     xy = w.matern_locations(n, seed=1)
     S = w.matern_cov(xy, 1.0, 0.02627)
     pmap = oracle.plan(S, nb, eps)
     assert np.any(pmap != oracle.FP64)
-    L, info, ld, plan = gpu_factor(S, nb, pmap, attrs=OZ)
+    L, info, ld, plan = gpu_factor(S, nb, pmap, attrs=dict(OZ, tc_engine=tc))
     _check_used(plan)
+    assert plan.get("tc_engine_used") == tc
     Lo, oinfo = oracle.factor(S, nb, pmap)
     assert info == oinfo == 0
     err = np.max(np.abs(L - Lo))
