@@ -99,6 +99,12 @@ typedef enum mxp_attr {
                                        MXP_ATTR_FP64_ENGINE_USED.  Re-sizes the workspace. */
     MXP_ATTR_OZ_SLICES = 13,      /* s for MXP_ATTR_FP64_ENGINE = 1, 4..8 (default 8: 55 bits per operand,
                                      dropped products <= 2^-56 of the row maxima) */
+    MXP_ATTR_COMPACT_POOL = 14,   /* with the native engine (MXP_ATTR_TC_ENGINE_USED = 3): 1 (default) = store every
+                                     tile below FP64 at its precision (codes + a power-of-two scale: 4/2/1 bytes per
+                                     element, "minimum acceptable bytes per word"); its fp64 accumulator slot
+                                     is recycled once the tile is final, so only FP64 tiles keep 8-byte slots.
+                                     mxp_chol_tile_device_ptr then refuses such tiles (MXP_ESTATE); unpack, the
+                                     forward solve and the D2H decode them.  0 = every tile keeps an fp64 slot. */
     MXP_ATTR_GPU_LAUNCHES = 100,  /* (get only) kernels launched by the last factorization */
     MXP_ATTR_H2D_BYTES = 101,     /* (get only) host->device bytes moved by the last factorization */
     MXP_ATTR_D2H_BYTES = 102,     /* (get only) device->host bytes moved by the last factorization */
@@ -106,8 +112,9 @@ typedef enum mxp_attr {
     MXP_ATTR_NT = 104,            /* (get only) Nt = ceil(n/nb) */
     MXP_ATTR_IMAGE_BYTES = 105,   /* (get only) bytes of tcgen05 operand images in the workspace (0: none) */
     MXP_ATTR_FP64_ENGINE_USED = 106, /* (get only) FP64 engine the next factorization uses (0 DMMA, 1 Ozaki) */
-    MXP_ATTR_TC_ENGINE_USED = 107 /* (get only) engine of the tiles below FP64 the next factorization uses
+    MXP_ATTR_TC_ENGINE_USED = 107, /* (get only) engine of the tiles below FP64 the next factorization uses
                                      (-1: all-FP64 map; else as MXP_ATTR_TC_ENGINE) */
+    MXP_ATTR_COMPACT_USED = 108   /* (get only) 1 if the next factorization uses the compact pool */
 } mxp_attr_t;
 
 /*

@@ -107,6 +107,14 @@ struct mxp_plan_s {
     int fp64_engine = 0, oz_slices = 8;
     bool oz_on = false;
     bool nat_on = false;            // tiles below FP64 on the native-width engine (tc_engine 3, k_tc)
+    // compact pool (with the native engine): only FP64 tiles keep a permanent fp64 slot; a tile
+    // stored below FP64 keeps its fp64 accumulator slot from its input until its QUANT (a ring
+    // recycled column by column) and then lives as its storage image (codes at its precision)
+    bool compact = false;
+    int compact_attr = 1;           // MXP_ATTR_COMPACT_POOL
+    int64_t compact_slots = 0;
+    std::vector<long long> sto;     // [T] byte offsets of the storage images in the shadow arena, -1 = none
+    long long* d_sto = nullptr;
     std::vector<long long> oz_img;  // [T] byte offsets of the int8 slice images, -1 = none
     long long* d_oz_img = nullptr;
     double* d_solve = nullptr;      // forward-solve work vectors (r | z | scalars)
@@ -116,7 +124,7 @@ struct mxp_plan_s {
     uint8_t* d_prec = nullptr;
     unsigned long long* d_amax_x = nullptr;
     double* d_amax_s = nullptr;
-    double* d_iscale = nullptr;     // [2T] scales of the native fp16 / E4M3 code images
+    double* d_iscale = nullptr;     // [3T] scales: native fp16 / E4M3 code images, storage image
     SchedArgs* d_args = nullptr;
     SchedArgs h_args{};
     bool host_mode = false;        // task list built for the host-streaming path (PREP tasks)
@@ -296,15 +304,49 @@ void build_task_list(mxp_plan_s* p) {
 // remainder for e = FP32.  Out of core (pool < T) the register-staged engine
 // is used instead (images would be sized by the whole lower triangle).
 int64_t pool_slots(const mxp_plan_s* p);
-// does a workspace of `need` bytes beside the fp64 pool fit in this device's free memory
-// (2 GB headroom; the plan's own current workspace counts as free)
-bool fits_beside_pool(const mxp_plan_s* p, double need) {
+// Compact slot plan (the static schedule is known in advance): walking
+// the columns in schedule order, tile (m, j) takes a slot freed by a tile of a
+// column <= j-2 (those are final before column j's inputs are prepared, and
+// their QUANT tasks come earlier in the task list, so waiting for them cannot
+// deadlock) or a fresh one.  Tiles stored below FP64 (off the diagonal) free
+// their slot when they are final; FP64 tiles keep theirs.  prev[t] = the tile
+// whose death the preparation of t waits for.  Returns the slot count.
+int64_t plan_compact(const mxp_plan_s* p, std::vector<int32_t>& slot, std::vector<int32_t>& prev) {
+    const int64_t Nt = p->Nt, T = p->T;
+    slot.assign(T, -1);
+    prev.assign(T, -1);
+    std::vector<int32_t> owner, freelist;
+    std::vector<std::vector<int32_t>> freed_at(Nt);
+    for (int64_t j = 0; j < Nt; ++j) {
+        if (j >= 2)
+            for (int32_t x : freed_at[j - 2]) freelist.push_back(x);
+        for (int64_t m = j; m < Nt; ++m) {
+            const int64_t t = tile_index(Nt, m, j);
+            int32_t sl;
+            if (!freelist.empty()) {
+                sl = freelist.back();
+                freelist.pop_back();
+            } else {
+                sl = (int32_t)owner.size();
+                owner.push_back(-1);
+            }
+            slot[t] = sl;
+            prev[t] = owner[sl];
+            owner[sl] = (int32_t)t;
+            if (m != j && p->map[t] != MXP_FP64) freed_at[j].push_back(sl);
+        }
+    }
+    return (int64_t)owner.size();
+}
+// does a workspace of `need` bytes beside a pool of `pool_tiles` fp64 slots fit in this device's
+// free memory (2 GB headroom; the plan's own current workspace counts as free)
+bool fits_beside_pool(const mxp_plan_s* p, double need, int64_t pool_tiles = -1) {
     size_t fr = 0, tot = 0;
     int cur = 0;
     bool ok = true;
     cudaGetDevice(&cur);
     if (cudaSetDevice(p->device) == cudaSuccess && cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
-        const double pool = (double)sizeof(double) * p->nb * p->nb * p->T;
+        const double pool = (double)sizeof(double) * p->nb * p->nb * (pool_tiles < 0 ? p->T : pool_tiles);
         ok = pool + need <= (double)fr + (double)p->ws_bytes - 2e9;
     }
     cudaGetLastError();
@@ -313,8 +355,8 @@ bool fits_beside_pool(const mxp_plan_s* p, double need) {
 }
 void plan_images_as(mxp_plan_s* p, bool native);
 void plan_images(mxp_plan_s* p) {
-    const long long key = ((((long long)p->oz_slices * 2 + p->fp64_engine) * 9 + p->nranks) * 4 + p->tc_engine) * 2 +
-                          (pool_slots(p) == p->T ? 1 : 0);
+    const long long key = (((((long long)p->oz_slices * 2 + p->fp64_engine) * 9 + p->nranks) * 4 + p->tc_engine) * 2 +
+                           (pool_slots(p) == p->T ? 1 : 0)) * 2 + p->compact_attr;
     if (key == p->img_key) return;
     p->img_key = key;
     // native-width images (kind::f16 / kind::f8f6f4) run in the tensor-core kernel k_tc, which
@@ -329,10 +371,27 @@ void plan_images_as(mxp_plan_s* p, bool native) {
     const int64_t Nt = p->Nt, T = p->T;
     p->img.assign(4 * T, -1);
     p->oz_img.assign(T, -1);
+    p->sto.assign(T, -1);
     p->oz_on = false;
     p->nat_on = false;
+    p->compact = false;
     p->qtile.assign(T, 0);
     p->shadow_bytes = 0;
+    int64_t ptiles = T;  // fp64 pool slots (native: the compact plan)
+    const bool compact = native && p->compact_attr;
+    if (compact) {
+        std::vector<int32_t> sl, pv;
+        ptiles = plan_compact(p, sl, pv);
+        // storage images (codes at the tile's precision, column-major) of the tiles below FP64
+        for (int64_t j = 0; j < Nt; ++j)
+            for (int64_t i = j + 1; i < Nt; ++i) {
+                const int64_t t = tile_index(Nt, i, j);
+                const int pt = p->map[t];
+                if (pt == MXP_FP64) continue;
+                p->sto[t] = (long long)p->shadow_bytes;
+                p->shadow_bytes += (size_t)p->nb * p->nb * (pt == MXP_FP32 ? 4 : pt == MXP_FP16 ? 2 : 1);
+            }
+    }
     bool images = p->mxp && p->tc_engine != 0 && p->tc_engine != 2 && pool_slots(p) == T;
     const long long img_bytes = (long long)sizeof(float) * p->nb * p->nb;
     if (images) {  // lower bound of the image bytes (each non-FP64 tile at least its own image)
@@ -341,7 +400,7 @@ void plan_images_as(mxp_plan_s* p, bool native) {
             need += p->map[t] == MXP_FP32 ? 2 * img_bytes
                     : p->map[t] == MXP_FP16 ? (native ? img_bytes / 2 : img_bytes)
                     : p->map[t] == MXP_FP8 ? (native ? img_bytes / 4 : img_bytes) : 0;
-        if (!fits_beside_pool(p, (double)need)) images = false;
+        if (!fits_beside_pool(p, (double)need, ptiles)) images = false;
     }
     // Tile t = (i, n) is an operand of the GEMMs of row i (outputs (i, k), n < k < i) and of
     // column i (outputs (m, i), m > i).  tf32 engine: one fp32 image per distinct
@@ -393,7 +452,7 @@ void plan_images_as(mxp_plan_s* p, bool native) {
                 p->qtile[t] = 1;
             }
         p->oz_on = true;
-        if (!fits_beside_pool(p, (double)p->shadow_bytes)) {  // does not fit: DMMA
+        if (!fits_beside_pool(p, (double)p->shadow_bytes, ptiles)) {  // does not fit: DMMA
             p->oz_img.assign(T, -1);
             p->shadow_bytes = before;
             p->oz_on = false;
@@ -407,6 +466,8 @@ void plan_images_as(mxp_plan_s* p, bool native) {
         }
     }
     p->nat_on = native && p->oz_on;
+    p->compact = p->nat_on && compact;
+    p->compact_slots = p->compact ? ptiles : 0;
     if (images && !p->oz_on && !fits_beside_pool(p, (double)p->shadow_bytes)) {
         // full size known now: does not fit -> the register-staged engine
         p->img.assign(4 * T, -1);
@@ -471,6 +532,10 @@ void tile_coords(int64_t Nt, int64_t t, int64_t& m, int64_t& n) {
 // V2 regime, is not implemented: MXP_ENOMEM).
 bool plan_slots(mxp_plan_s* p, int64_t C) {
     const int64_t Nt = p->Nt, T = p->T;
+    if (p->compact) {  // (plan_images decided it: in core, native engine)
+        plan_compact(p, p->slot_plan, p->prev_owner);
+        return true;
+    }
     p->slot_plan.assign(T, -1);
     p->prev_owner.assign(T, -1);
     if (C >= T) {  // in core: every tile keeps its own slot (L stays resident)
@@ -499,7 +564,7 @@ bool plan_slots(mxp_plan_s* p, int64_t C) {
 
 struct Layout {
     size_t slot, prev, epoch, flags, flags_bytes, expected, items, wbuf, stats, prec, amax_x, amax_s, iscale, args,
-        qtile, img, ozimg, solve, shadow, pool, total;
+        qtile, img, ozimg, sto, solve, shadow, pool, total;
 };
 
 Layout layout(const mxp_plan_s* p) {
@@ -530,7 +595,7 @@ Layout layout(const mxp_plan_s* p) {
     L.amax_s = off;
     off += align_up(sizeof(double) * (size_t)p->T, 256);
     L.iscale = off;
-    off += align_up(sizeof(double) * 2 * (size_t)p->T, 256);
+    off += align_up(sizeof(double) * 3 * (size_t)p->T, 256);
     L.args = off;
     off += align_up(sizeof(SchedArgs), 256);
     L.qtile = off;
@@ -539,12 +604,14 @@ Layout layout(const mxp_plan_s* p) {
     off += align_up(sizeof(long long) * 4 * (size_t)p->T, 256);
     L.ozimg = off;
     off += align_up(sizeof(long long) * (size_t)p->T, 256);
+    L.sto = off;
+    off += align_up(sizeof(long long) * (size_t)p->T, 256);
     L.solve = off;  // forward solve: r, z (Nt*nb each) + scalars
     off += align_up(sizeof(double) * (2 * (size_t)p->Nt * p->nb + 8), 256);
     L.shadow = off;
     off += align_up(p->shadow_bytes, 1024);
     L.pool = off;
-    off += sizeof(double) * (size_t)pool_slots(p) * p->nb * p->nb;
+    off += sizeof(double) * (size_t)(p->compact ? p->compact_slots : pool_slots(p)) * p->nb * p->nb;
     L.total = off;
     return L;
 }
@@ -601,6 +668,7 @@ void bind_workspace(mxp_plan_s* p) {
     p->d_qtile = (uint8_t*)(p->ws + L.qtile);
     p->d_img = (long long*)(p->ws + L.img);
     p->d_oz_img = (long long*)(p->ws + L.ozimg);
+    p->d_sto = (long long*)(p->ws + L.sto);
     p->d_solve = (double*)(p->ws + L.solve);
     p->d_shadow = (uint8_t*)(p->ws + L.shadow);
     p->d_amax_x = (unsigned long long*)(p->ws + L.flags + align_up(sizeof(int) * flag_ints(p), 8));
@@ -815,6 +883,18 @@ int64_t last_pushed_tile(const mxp_plan_s* p, int q) {
     return last;
 }
 
+// where the final tiles of the compact pool live (storage images) for unpack / solve
+TileCodes decode_args(const mxp_plan_s* p) {
+    TileCodes d{};
+    if (p->compact) {
+        d.sto = p->d_sto;
+        d.shadow = p->d_shadow;
+        d.prec = p->d_prec;
+        d.scale = p->d_iscale;
+    }
+    return d;
+}
+
 struct GenSource {  // fused on-device generation of the input tiles (N2)
     const double* xy = nullptr;
     double sigma2 = 1.0, range = 1.0, nugget = 0.0;
@@ -865,7 +945,7 @@ std::string sched_timeout_detail(mxp_plan_s* p) {
 }
 
 void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A_host = nullptr,
-                       int64_t lda = 0, const GenSource* gen = nullptr) {
+                       int64_t lda = 0, const GenSource* gen = nullptr, const double* srcA = nullptr) {
     const int64_t Nt = p->Nt, T = p->T;
     if (p->host_mode != host_mode) {
         p->host_mode = host_mode;
@@ -882,6 +962,7 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
         CK(cudaMemcpyAsync(p->d_prec, p->map.data(), (size_t)T, cudaMemcpyHostToDevice, s0));
         CK(cudaMemcpyAsync(p->d_qtile, p->qtile.data(), (size_t)T, cudaMemcpyHostToDevice, s0));
         CK(cudaMemcpyAsync(p->d_img, p->img.data(), sizeof(long long) * 4 * T, cudaMemcpyHostToDevice, s0));
+        CK(cudaMemcpyAsync(p->d_sto, p->sto.data(), sizeof(long long) * T, cudaMemcpyHostToDevice, s0));
         CK(cudaStreamSynchronize(s0));
         p->list_uploaded = true;
     }
@@ -935,7 +1016,11 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     a.col_ready = a.potrf_claim + Nt;
     int* d2h_done = a.col_ready + Nt;
     a.logdet_parts = p->d_logdet_parts;
-    a.loaded = (p->host_mode && !gen) ? loaded : nullptr;
+    a.loaded = (p->host_mode && !gen && !srcA) ? loaded : nullptr;
+    a.src_A = srcA;  // compact device path: PREP copies tile (m, k) from the caller's matrix
+    a.src_lda = lda;
+    a.compact = p->compact ? 1 : 0;
+    a.sto = p->compact ? p->d_sto : nullptr;
     a.n = p->n;
     a.gen_mode = gen ? 1 : 0;
     a.prev_owner = p->d_prev;
@@ -1089,7 +1174,7 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
             }
         });
     if (p->nranks > 1) feed([&] { push_tiles(p, a); });
-    if (host_mode && !gen) try {
+    if (host_mode && !gen && !srcA) try {
         // H2D in schedule (column) order; the GPU front-end publishes loaded[t]
         CK(cudaStreamWaitEvent(p->sH2D, p->ev_start, 0));
         CK(cudaStreamWaitEvent(p->sD2H, p->ev_start, 0));
@@ -1128,11 +1213,17 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
                 double* dst = p->pool + (size_t)p->slot_plan[t] * nb * nb;
                 const double* src = A_host + (size_t)k * nb * lda + (size_t)m * nb;
                 const int32_t prev = p->prev_owner[t];
-                if (prev >= 0) {  // out of core: the slot's previous tile must be dead and written back
+                if (prev >= 0) {  // out of core / compact: the slot's previous tile must be dead and written back
                     int64_t pm = 0, pc = 0;
                     tile_coords(Nt, prev, pm, pc);
-                    if (g_wait32((CUstream)p->sH2D, (CUdeviceptr)(a.col_ready + pm), (cuuint32_t)(Nt - pm),
-                                 CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS ||
+                    // compact: a tile below FP64 dies when it is final (its readers use images);
+                    // out of core: when column pm, its last reader, is final
+                    const bool ok = p->compact
+                        ? g_wait32((CUstream)p->sH2D, (CUdeviceptr)(a.ready + prev), (cuuint32_t)p->epoch,
+                                   CU_STREAM_WAIT_VALUE_GEQ) == CUDA_SUCCESS
+                        : g_wait32((CUstream)p->sH2D, (CUdeviceptr)(a.col_ready + pm), (cuuint32_t)(Nt - pm),
+                                   CU_STREAM_WAIT_VALUE_GEQ) == CUDA_SUCCESS;
+                    if (!ok ||
                         g_wait32((CUstream)p->sH2D, (CUdeviceptr)(d2h_done + prev), 1, CU_STREAM_WAIT_VALUE_GEQ) !=
                             CUDA_SUCCESS)
                         throw CudaError{cudaErrorUnknown};
@@ -1327,6 +1418,17 @@ int mxp_chol_plan_set(mxp_plan_t p, mxp_attr_t key, int64_t v) {
         else p->oz_slices = (int)v;
         p->list_uploaded = false;
         return MXP_OK;
+    case MXP_ATTR_COMPACT_POOL:
+        if (v < 0 || v > 1) return -3;
+        if (p->ws && !p->ws_owned) return MXP_ESTATE;  // changes the workspace layout
+        if (p->ws_owned) {
+            cudaFree(p->ws);
+            p->ws = nullptr;
+            p->ws_owned = false;
+        }
+        p->compact_attr = (int)v;
+        p->list_uploaded = false;
+        return MXP_OK;
     case MXP_ATTR_TC_ENGINE:
         if (v < 0 || v > 3) return -3;
         if (p->ws && !p->ws_owned) return MXP_ESTATE;  // changes the task list / image sizes
@@ -1374,6 +1476,8 @@ int mxp_chol_plan_get(mxp_plan_t p, mxp_attr_t key, int64_t* v) {
     case MXP_ATTR_TC_ENGINE: *v = p->tc_engine; return MXP_OK;
     case MXP_ATTR_FP64_ENGINE: *v = p->fp64_engine; return MXP_OK;
     case MXP_ATTR_OZ_SLICES: *v = p->oz_slices; return MXP_OK;
+    case MXP_ATTR_COMPACT_POOL: *v = p->compact_attr; return MXP_OK;
+    case MXP_ATTR_COMPACT_USED: plan_images(p); *v = p->compact ? 1 : 0; return MXP_OK;
     case MXP_ATTR_FP64_ENGINE_USED: plan_images(p); *v = p->oz_on ? 1 : 0; return MXP_OK;
     case MXP_ATTR_RANK: *v = p->rank; return MXP_OK;
     case MXP_ATTR_NRANKS: *v = p->nranks; return MXP_OK;
@@ -1382,7 +1486,7 @@ int mxp_chol_plan_get(mxp_plan_t p, mxp_attr_t key, int64_t* v) {
     case MXP_ATTR_GPU_LAUNCHES: *v = p->launches; return MXP_OK;
     case MXP_ATTR_H2D_BYTES: *v = p->h2d; return MXP_OK;
     case MXP_ATTR_D2H_BYTES: *v = p->d2h; return MXP_OK;
-    case MXP_ATTR_POOL_SLOTS: *v = pool_slots(p); return MXP_OK;
+    case MXP_ATTR_POOL_SLOTS: plan_images(p); *v = p->compact ? p->compact_slots : pool_slots(p); return MXP_OK;
     case MXP_ATTR_NT: *v = p->Nt; return MXP_OK;
     case MXP_ATTR_IMAGE_BYTES: plan_images(p); *v = (int64_t)p->shadow_bytes; return MXP_OK;
     case MXP_ATTR_TC_ENGINE_USED: {
@@ -1447,27 +1551,37 @@ int mxp_chol_factor_device(mxp_plan_t p, double* A, int64_t lda, int64_t* info) 
         ensure_streams(p);
         bind_workspace(p);
         cudaStream_t s0 = entry_stream(p);
-        // slot table (identity in-core) + info reset, ordered on the user stream
-        p->slot_plan.resize(p->T);
-        p->prev_owner.assign(p->T, -1);
-        for (int64_t t = 0; t < p->T; ++t) p->slot_plan[t] = (int32_t)t;
+        // slot table (identity in core; the compact ring with the native engine) + info reset,
+        // ordered on the user stream
+        if (p->compact) {
+            plan_slots(p, p->T);
+        } else {
+            p->slot_plan.resize(p->T);
+            p->prev_owner.assign(p->T, -1);
+            for (int64_t t = 0; t < p->T; ++t) p->slot_plan[t] = (int32_t)t;
+        }
         CK(cudaMemcpyAsync(p->d_slot, p->slot_plan.data(), sizeof(int32_t) * p->T, cudaMemcpyHostToDevice, s0));
         CK(cudaMemcpyAsync(p->d_prev, p->prev_owner.data(), sizeof(int32_t) * p->T, cudaMemcpyHostToDevice, s0));
         CK(cudaMemsetAsync(p->d_info, 0, sizeof(int64_t), s0));
         prof_reset(p);
-        {
-            Prof pr(p, s0, MXP_KCLASS_OTHER, 0.0);
-            launch_pack_f64(A, lda, p->n, p->pool, p->d_slot, p->Nt, p->nb, 0, p->Nt, s0, p->rank, p->nranks);
-            ++p->launches;
-            dbg(p, s0, "pack");
+        if (p->compact) {
+            // PREP tasks copy each tile from A into its ring slot right before its first use
+            factor_incore_f64(p, s0, true, nullptr, lda, nullptr, A);
+        } else {
+            {
+                Prof pr(p, s0, MXP_KCLASS_OTHER, 0.0);
+                launch_pack_f64(A, lda, p->n, p->pool, p->d_slot, p->Nt, p->nb, 0, p->Nt, s0, p->rank, p->nranks);
+                ++p->launches;
+                dbg(p, s0, "pack");
+            }
+            factor_incore_f64(p, s0, false);
         }
-        factor_incore_f64(p, s0, false);
         CK(cudaEventRecord(p->ev_done, p->sU));
         CK(cudaStreamWaitEvent(s0, p->ev_done, 0));
         finish_pushes(p, s0);
         {
             Prof pr(p, s0, MXP_KCLASS_OTHER, 0.0, 3);
-            launch_unpack_f64(A, lda, p->n, p->pool, p->d_slot, p->Nt, p->nb, 0, p->Nt, s0);
+            launch_unpack_f64(A, lda, p->n, p->pool, p->d_slot, p->Nt, p->nb, 0, p->Nt, s0, decode_args(p));
             launch_logdet_final(p->d_logdet_parts, p->Nt, p->d_logdet, s0);
             p->launches += 2;
             dbg(p, s0, "unpack");
@@ -1911,7 +2025,8 @@ int mxp_chol_get_factor_device(mxp_plan_t p, double* L_dev, int64_t ldl) {
     cudaGetDevice(&cur);
     try {
         CK(cudaSetDevice(p->device));
-        launch_unpack_f64(L_dev, ldl, p->n, p->pool, p->d_slot, p->Nt, p->nb, 0, p->Nt, p->user_stream);
+        launch_unpack_f64(L_dev, ldl, p->n, p->pool, p->d_slot, p->Nt, p->nb, 0, p->Nt, p->user_stream,
+                          decode_args(p));
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(p->user_stream));
     } catch (const CudaError& e) {
@@ -1938,7 +2053,7 @@ int mxp_chol_solve_lower(mxp_plan_t p, const double* y_dev, double* z_dev, doubl
         cudaStream_t s = p->user_stream;
         CK(cudaMemsetAsync(r, 0, sizeof(double) * N, s));
         CK(cudaMemcpyAsync(r, y_dev, sizeof(double) * p->n, cudaMemcpyDeviceToDevice, s));
-        launch_forward_solve(p->pool, p->d_slot, p->d_wbuf, p->Nt, p->nb, r, z, s);
+        launch_forward_solve(p->pool, p->d_slot, p->d_wbuf, p->Nt, p->nb, r, z, s, decode_args(p));
         launch_sumsq(z, p->n, sc, s);
         CK(cudaGetLastError());
         if (z_dev) CK(cudaMemcpyAsync(z_dev, z, sizeof(double) * p->n, cudaMemcpyDeviceToDevice, s));
@@ -1974,6 +2089,7 @@ int mxp_chol_tile_device_ptr(mxp_plan_t p, int64_t i, int64_t j, double** ptr) {
     if (j < 0 || j > i) return -3;
     if (!ptr) return -4;
     if (!p->pool || p->slot_plan.empty() || pool_slots(p) < p->T) return MXP_ESTATE;
+    if (p->compact && p->sto[tile_index(p->Nt, i, j)] >= 0) return MXP_ESTATE;  // stored as codes
     *ptr = p->pool + (size_t)p->slot_plan[tile_index(p->Nt, i, j)] * p->nb * p->nb;
     return MXP_OK;
 }

@@ -97,9 +97,14 @@ struct SchedArgs {
                                //     block, grid, column, taken (host reports it in mxp_last_error)
     // native-width operand images (tc_native.cuh; MXP_ATTR_TC_ENGINE = 3, tensor-core kernel k_tc):
     // img[4t+1] = fp16 codes of cast_FP16(L) for FP16 outputs, img[4t+2] = E4M3 codes of cast_FP8(L)
-    // for FP8 outputs, iscale[2t + kind] = the power-of-two scale of those codes (code = value * scale)
+    // for FP8 outputs, iscale[3t + kind] = the power-of-two scale of those codes (code = value * scale)
     int native;
-    double* iscale;            // [2T]
+    double* iscale;            // [3T]: + [3t+2] = scale of the storage image (code = value * scale)
+    // compact pool (native engine): tiles below FP64 live as storage images after their QUANT
+    int compact;
+    const long long* sto;      // [T] offsets of the storage images in `shadow` (-1: FP64 tile)
+    const double* src_A;       // compact device path: the caller's matrix (PREP copies tiles from it)
+    int64_t src_lda;
     int* sm_claim;             // [256] k_sched CTAs per SM in the Ozaki mode (extras leave at once,
                                //       keeping room for the k_tc CTA of every SM)
     unsigned long long* stats; // optional diagnostics (MXP_ATTR_PROFILE): see STAT_*
@@ -124,10 +129,20 @@ void launch_tc(const SchedArgs* a_dev, int grid, cudaStream_t s);
 int tc_ctas_per_sm();
 void launch_potrf_tile(const SchedArgs& a, int64_t k, cudaStream_t s);
 
+// Final tiles stored as codes (compact pool): value = code / scale[3t+2], code at prec[t]
+// (FP32 float, FP16 binary16, FP8 E4M3), column-major nb x nb at shadow + sto[t];
+// sto == nullptr or sto[t] < 0: the fp64 slot.
+struct TileCodes {
+    const long long* sto;
+    const uint8_t* shadow;
+    const uint8_t* prec;
+    const double* scale;
+};
+
 // ---- forward solve / log-likelihood (solve.cu) -----------
 // z = L^-1 r on the resident factor (r, z: Nt*nb, padded with zeros; r is consumed)
 void launch_forward_solve(const double* pool, const int32_t* slot, const double* wbuf, int64_t Nt, int64_t nb,
-                          double* r, double* z, cudaStream_t s);
+                          double* r, double* z, cudaStream_t s, TileCodes codes = TileCodes{});
 void launch_sumsq(const double* z, int64_t n, double* out, cudaStream_t s);
 
 // ---- layout / utility kernels --------------------------------------------
@@ -136,7 +151,8 @@ void launch_pack_f64(const double* A, int64_t lda, int64_t n, double* pool, cons
                      int64_t Nt, int64_t nb, int64_t col0, int64_t col1, cudaStream_t s, int rank = 0,
                      int nranks = 1);
 void launch_unpack_f64(double* A, int64_t lda, int64_t n, const double* pool, const int32_t* slot,
-                       int64_t Nt, int64_t nb, int64_t col0, int64_t col1, cudaStream_t s);
+                       int64_t Nt, int64_t nb, int64_t col0, int64_t col1, cudaStream_t s,
+                       TileCodes codes = TileCodes{});
 // logdet = 2 sum_k parts[k] in ascending k (parts from the POTRFs; deterministic)
 void launch_logdet_final(const double* parts, int64_t Nt, double* out, cudaStream_t s);
 // planner on a generated Matern covariance: per-tile Frobenius norms computed

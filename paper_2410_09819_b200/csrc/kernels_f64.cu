@@ -5,6 +5,7 @@
 #include <math.h>
 
 #include "dmma_gemm.cuh"
+#include "quant.cuh"
 
 namespace mxp {
 
@@ -29,17 +30,23 @@ __global__ void k_pack(const double* __restrict__ A, int64_t lda, int64_t n, dou
     }
 }
 __global__ void k_unpack(double* __restrict__ A, int64_t lda, int64_t n, const double* pool,
-                         const int32_t* slot, int64_t Nt, int64_t nb, int64_t col0) {
+                         const int32_t* slot, int64_t Nt, int64_t nb, int64_t col0, TileCodes codes) {
     const int64_t j = col0 + blockIdx.y;
     const int64_t i = j + blockIdx.z;
     if (i >= Nt) return;
-    const double* T = pool + (int64_t)slot[tile_index(Nt, i, j)] * nb * nb;
+    const int64_t t = tile_index(Nt, i, j);
+    const double* T = pool + (int64_t)slot[t] * nb * nb;
+    // compact pool: a tile stored below FP64 is decoded from its storage image
+    const bool coded = codes.sto && codes.sto[t] >= 0;
+    const uint8_t* cp = coded ? codes.shadow + codes.sto[t] : nullptr;
+    const int p = coded ? codes.prec[t] : P_FP64;
+    const double inv = coded ? 1.0 / codes.scale[3 * t + 2] : 1.0;
     for (int64_t c = blockIdx.x * 8; c < (int64_t)blockIdx.x * 8 + 8; ++c) {
         int64_t gj = j * nb + c;
         if (gj >= n) return;
         for (int64_t r = threadIdx.x; r < nb; r += blockDim.x) {
             int64_t gi = i * nb + r;
-            if (gi < n && gi >= gj) A[gi + gj * lda] = T[r + c * nb];
+            if (gi < n && gi >= gj) A[gi + gj * lda] = coded ? decode_code(p, cp, r + c * nb, inv) : T[r + c * nb];
         }
     }
 }
@@ -50,10 +57,10 @@ void launch_pack_f64(const double* A, int64_t lda, int64_t n, double* pool, cons
     k_pack<<<grid, 256, 0, s>>>(A, lda, n, pool, slot, Nt, nb, col0, rank, nranks);
 }
 void launch_unpack_f64(double* A, int64_t lda, int64_t n, const double* pool, const int32_t* slot,
-                       int64_t Nt, int64_t nb, int64_t col0, int64_t col1, cudaStream_t s) {
+                       int64_t Nt, int64_t nb, int64_t col0, int64_t col1, cudaStream_t s, TileCodes codes) {
     dim3 grid((unsigned)(nb / 8), (unsigned)(col1 - col0), (unsigned)(Nt - col0));
     MXP_CARVEOUT_MAX(k_unpack);
-    k_unpack<<<grid, 256, 0, s>>>(A, lda, n, pool, slot, Nt, nb, col0);
+    k_unpack<<<grid, 256, 0, s>>>(A, lda, n, pool, slot, Nt, nb, col0, codes);
 }
 
 // -------------------------------------------------------------- log-det

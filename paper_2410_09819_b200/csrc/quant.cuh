@@ -102,6 +102,24 @@ __device__ __forceinline__ double apply_cast(const Cast& c, double x) {
     return quantize_value(c.mode, x, c.s, c.inv_s);
 }
 
+// value of element e of a tile stored as codes at precision p (FP32 float, FP16
+// binary16, FP8 E4M3) with scale s: code / s (exact)
+__device__ __forceinline__ double decode_code(int p, const uint8_t* codes, int64_t e, double inv_s) {
+    if (p == P_FP32) return (double)__ldcg(reinterpret_cast<const float*>(codes) + e);
+    if (p == P_FP16) {
+        const unsigned short h = __ldcg(reinterpret_cast<const unsigned short*>(codes) + e);
+        float f;
+        asm("cvt.f32.f16 %0, %1;" : "=f"(f) : "h"(h));
+        return (double)f * inv_s;
+    }
+    const unsigned short b = (unsigned short)__ldcg(codes + e);
+    unsigned int h2;
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(b));
+    float f;
+    asm("cvt.f32.f16 %0, %1;" : "=f"(f) : "h"((unsigned short)(h2 & 0xFFFFu)));
+    return (double)f * inv_s;
+}
+
 // amax of non-negative doubles via their bit patterns (monotone for x >= 0)
 __device__ __forceinline__ void atomic_max_abs(unsigned long long* slot, double v) {
     atomicMax(slot, (unsigned long long)__double_as_longlong(fabs(v)));

@@ -70,7 +70,7 @@ __device__ __forceinline__ bool skip_column(const SchedArgs& a, int64_t col) {
 
 // streaming modes (host input or generated tiles): tile t has been prepared
 __device__ __forceinline__ bool wait_input(const SchedArgs& a, int64_t t, int64_t col) {
-    return !(a.loaded || a.gen_mode) || wait_flag(a.prep_done + t, 1, a, col);
+    return !(a.loaded || a.gen_mode || a.src_A) || wait_flag(a.prep_done + t, 1, a, col);
 }
 
 // Matern nu = 0.5 covariance entry (Eq. 2 closed form)
@@ -493,7 +493,7 @@ __device__ __noinline__ bool task_gemm_nat(const SchedArgs& a, int64_t m, int64_
         nat::NatTile o;
         o.a = a.shadow + a.img[4 * ta + slot] + nat::chunk_offset(KIND, nb, bi, 0);
         o.b = a.shadow + a.img[4 * tb + slot] + nat::chunk_offset(KIND, nb, bj, 0);
-        nat::inv_scales(__ldcg(a.iscale + 2 * ta + KIND), __ldcg(a.iscale + 2 * tb + KIND), o.inv0, o.inv1);
+        nat::inv_scales(__ldcg(a.iscale + 3 * ta + KIND), __ldcg(a.iscale + 3 * tb + KIND), o.inv0, o.inv1);
         return o;
     };
     double* Ct = tile_ptr(a.pool, a.slot, Nt, nb, m, k) + bi * 128 + bj * 128 * nb;
@@ -687,9 +687,37 @@ __device__ __noinline__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k
             }
         }
         if (tid == 0) {
-            a.iscale[2 * t + 0] = s16;
-            a.iscale[2 * t + 1] = s8;
+            a.iscale[3 * t + 0] = s16;
+            a.iscale[3 * t + 1] = s8;
         }
+    }
+    if (a.sto && a.sto[t] >= 0) {  // compact pool: the tile's storage image (codes, column-major)
+        sync_workers();
+        uint8_t* dst = a.shadow + a.sto[t];
+        for (int64_t idx = threadIdx.x; idx < 16 * nb; idx += CC::NT) {
+            const int q4 = (int)(idx & 15), col = (int)(idx >> 4);
+            const double* q = X + 4 * q4 + (int64_t)col * nb;
+            const double2 v01 = __ldcg(reinterpret_cast<const double2*>(q));
+            const double2 v23 = __ldcg(reinterpret_cast<const double2*>(q + 2));
+            const int64_t e = (int64_t)col * nb + r * 64 + 4 * q4;  // element index in the tile
+            if (p == P_FP32) {
+                __stcg(reinterpret_cast<float4*>(dst + 4 * e),
+                       make_float4((float)v01.x, (float)v01.y, (float)v23.x, (float)v23.y));
+            } else if (p == P_FP16) {
+                const unsigned short h0 = __half_as_ushort(__double2half(v01.x * sc));
+                const unsigned short h1 = __half_as_ushort(__double2half(v01.y * sc));
+                const unsigned short h2 = __half_as_ushort(__double2half(v23.x * sc));
+                const unsigned short h3 = __half_as_ushort(__double2half(v23.y * sc));
+                __stcg(reinterpret_cast<uint2*>(dst + 2 * e),
+                       make_uint2((uint32_t)h0 | ((uint32_t)h1 << 16), (uint32_t)h2 | ((uint32_t)h3 << 16)));
+            } else {
+                unsigned short lo, hi;
+                asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"((float)(v01.y * sc)), "f"((float)(v01.x * sc)));
+                asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"((float)(v23.y * sc)), "f"((float)(v23.x * sc)));
+                __stcg(reinterpret_cast<uint32_t*>(dst + e), (uint32_t)lo | ((uint32_t)hi << 16));
+            }
+        }
+        if (threadIdx.x == 0) a.iscale[3 * t + 2] = sc;
     }
     if (a.oz_img && a.oz_img[t] >= 0) {  // int8 slices of the stored values (FP64 GEMM operands)
         __threadfence_block();
@@ -720,10 +748,12 @@ __device__ __noinline__ bool task_prep(const SchedArgs& a, int64_t m, int64_t k,
     const int64_t t = tile_index(Nt, m, k);
     if (threadIdx.x == 0) {
         bool ok;
-        if (a.gen_mode) {
+        if (a.gen_mode || a.src_A) {
             ok = !skip_column(a, k);
             const int32_t prev = a.prev_owner[t];
-            if (ok && prev >= 0) {  // out of core: the slot's previous tile (pm, .) dies with column pm
+            if (ok && prev >= 0 && a.compact) {  // compact ring: the slot's previous tile dies when final
+                ok = wait_flag(a.ready + prev, a.epoch, a, k);
+            } else if (ok && prev >= 0) {  // out of core: the slot's previous tile (pm, .) dies with column pm
                 int64_t pm = 0, pc = 0, r = prev;
                 while (r >= Nt - pc) { r -= Nt - pc; ++pc; }
                 pm = pc + r;
@@ -743,6 +773,15 @@ __device__ __noinline__ bool task_prep(const SchedArgs& a, int64_t m, int64_t k,
             const int64_t r = e % nb, c = e / nb;
             double v;
             if (r < rr && c < cr) v = matern_entry(a, m * nb + r, k * nb + c);
+            else v = (m == k && r == c) ? 1.0 : 0.0;
+            __stcg(T + e, v);
+        }
+        sync_workers();
+    } else if (a.src_A) {  // compact device path: the tile from the caller's matrix (lower part), padded
+        for (int64_t e = threadIdx.x; e < nb * nb; e += CC::NT) {
+            const int64_t r = e % nb, c = e / nb, gi = m * nb + r, gj = k * nb + c;
+            double v;
+            if (r < rr && c < cr) v = gi >= gj ? __ldcg(a.src_A + gi + gj * a.src_lda) : 0.0;
             else v = (m == k && r == c) ? 1.0 : 0.0;
             __stcg(T + e, v);
         }

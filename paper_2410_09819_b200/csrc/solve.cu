@@ -9,14 +9,35 @@
 // 128-row block).  Every sum runs in a fixed order: the result is bitwise
 // reproducible.
 #include "internal.h"
+#include "quant.cuh"
 
 namespace mxp {
 namespace {
 
 // r[m*nb + rows] -= L(m,k)[rows, :] z_k  for m = k+1 .. Nt-1, 128-row blocks
+template <int P>
+__device__ __forceinline__ double tile_elem(const double* L, const uint8_t* codes, int64_t e, double inv) {
+    if constexpr (P == P_FP64) return __ldcs(L + e);
+    else return decode_code(P, codes, e, inv);
+}
+// one thread's partial dot product over columns [c0, c1) of row `row` of a tile
+template <int P>
+__device__ __forceinline__ double row_dot(const double* L, const uint8_t* codes, double inv, int64_t nb, int64_t row,
+                                          int64_t c0, int64_t c1, const double* sz) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // 4 chains, 8 loads in flight per thread
+#pragma unroll 2
+    for (int64_t c = c0; c < c1; c += 4) {
+        s0 = fma(tile_elem<P>(L, codes, row + c * nb, inv), sz[c], s0);
+        s1 = fma(tile_elem<P>(L, codes, row + (c + 1) * nb, inv), sz[c + 1], s1);
+        s2 = fma(tile_elem<P>(L, codes, row + (c + 2) * nb, inv), sz[c + 2], s2);
+        s3 = fma(tile_elem<P>(L, codes, row + (c + 3) * nb, inv), sz[c + 3], s3);
+    }
+    return (s0 + s1) + (s2 + s3);
+}
+
 __global__ void __launch_bounds__(256) k_trsv_gemv(const double* __restrict__ pool, const int32_t* __restrict__ slot,
                                                    int64_t Nt, int64_t nb, int64_t k, double* r,
-                                                   const double* __restrict__ z) {
+                                                   const double* __restrict__ z, TileCodes codes) {
     extern __shared__ double sz[];  // z_k (nb) + 256 partial sums
     double* part = sz + nb;
     const int64_t RB = nb / 128;
@@ -24,17 +45,21 @@ __global__ void __launch_bounds__(256) k_trsv_gemv(const double* __restrict__ po
     for (int64_t c = threadIdx.x; c < nb; c += blockDim.x) sz[c] = z[k * nb + c];
     __syncthreads();
     const int row = threadIdx.x & 127, h = threadIdx.x >> 7;
-    const double* L = pool + (int64_t)slot[tile_index(Nt, m, k)] * nb * nb + rb * 128 + row;
-    const int64_t c0 = h * (nb / 2), c1 = c0 + nb / 2;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // 4 chains, 8 loads in flight per thread
-#pragma unroll 2
-    for (int64_t c = c0; c < c1; c += 4) {
-        s0 = fma(__ldcs(L + c * nb), sz[c], s0);
-        s1 = fma(__ldcs(L + (c + 1) * nb), sz[c + 1], s1);
-        s2 = fma(__ldcs(L + (c + 2) * nb), sz[c + 2], s2);
-        s3 = fma(__ldcs(L + (c + 3) * nb), sz[c + 3], s3);
+    const int64_t t = tile_index(Nt, m, k);
+    const double* L = pool + (int64_t)slot[t] * nb * nb;
+    const int64_t c0 = h * (nb / 2), c1 = c0 + nb / 2, grow = rb * 128 + row;
+    // compact pool: tiles below FP64 are read at their storage precision (fewer bytes)
+    const int p = (codes.sto && codes.sto[t] >= 0) ? codes.prec[t] : P_FP64;
+    const uint8_t* cp = p != P_FP64 ? codes.shadow + codes.sto[t] : nullptr;
+    const double inv = p != P_FP64 ? 1.0 / codes.scale[3 * t + 2] : 1.0;
+    double dot;
+    switch (p) {
+    case P_FP32: dot = row_dot<P_FP32>(L, cp, inv, nb, grow, c0, c1, sz); break;
+    case P_FP16: dot = row_dot<P_FP16>(L, cp, inv, nb, grow, c0, c1, sz); break;
+    case P_FP8: dot = row_dot<P_FP8>(L, cp, inv, nb, grow, c0, c1, sz); break;
+    default: dot = row_dot<P_FP64>(L, cp, inv, nb, grow, c0, c1, sz); break;
     }
-    part[threadIdx.x] = (s0 + s1) + (s2 + s3);
+    part[threadIdx.x] = dot;
     __syncthreads();
     if (h == 0) r[m * nb + rb * 128 + row] -= part[row] + part[row + 128];
 }
@@ -93,7 +118,7 @@ __global__ void __launch_bounds__(1024) k_sumsq(const double* __restrict__ z, in
 }  // namespace
 
 void launch_forward_solve(const double* pool, const int32_t* slot, const double* wbuf, int64_t Nt, int64_t nb,
-                          double* r, double* z, cudaStream_t s) {
+                          double* r, double* z, cudaStream_t s, TileCodes codes) {
     const size_t sm_diag = sizeof(double) * (nb + 128 + 256), sm_gemv = sizeof(double) * (nb + 256);
     static bool configured = false;
     if (!configured) {
@@ -105,7 +130,7 @@ void launch_forward_solve(const double* pool, const int32_t* slot, const double*
         MXP_CARVEOUT_MAX(k_trsv_diag);
         k_trsv_diag<<<1, 256, sm_diag, s>>>(pool, slot, wbuf, Nt, nb, k, r, z);
         MXP_CARVEOUT_MAX(k_trsv_gemv);
-        if (k + 1 < Nt) k_trsv_gemv<<<(unsigned)((Nt - k - 1) * (nb / 128)), 256, sm_gemv, s>>>(pool, slot, Nt, nb, k, r, z);
+        if (k + 1 < Nt) k_trsv_gemv<<<(unsigned)((Nt - k - 1) * (nb / 128)), 256, sm_gemv, s>>>(pool, slot, Nt, nb, k, r, z, codes);
     }
 }
 
