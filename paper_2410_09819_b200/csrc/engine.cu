@@ -397,7 +397,7 @@ void plan_images_as(mxp_plan_s* p, bool native) {
     if (images) {  // lower bound of the image bytes (each non-FP64 tile at least its own image)
         long long need = 0;
         for (int64_t t = 0; t < T; ++t)
-            need += p->map[t] == MXP_FP32 ? 2 * img_bytes
+            need += p->map[t] == MXP_FP32 ? (native ? img_bytes : 2 * img_bytes)
                     : p->map[t] == MXP_FP16 ? (native ? img_bytes / 2 : img_bytes)
                     : p->map[t] == MXP_FP8 ? (native ? img_bytes / 4 : img_bytes) : 0;
         if (!fits_beside_pool(p, (double)need, ptiles)) images = false;
@@ -421,19 +421,28 @@ void plan_images_as(mxp_plan_s* p, bool native) {
                 for (int64_t m = i + 1; m < Nt; ++m) consumer(p->map[tile_index(Nt, m, i)]);
             }
             bool any = false;
-            for (int e = 1; e <= 3; ++e)
-                if (need[e]) {
-                    any = true;
-                    p->img[4 * t + e - 1] = (long long)p->shadow_bytes;
-                    if (native && e == MXP_FP16) p->shadow_bytes += nat::image_bytes(nat::K_F16, p->nb);
-                    else if (native && e == MXP_FP8) p->shadow_bytes += nat::image_bytes(nat::K_F8, p->nb);
-                    else p->shadow_bytes += img_bytes;
-                    // TF32 remainder: FP32 image of an operand stored at FP32 or finer
-                    if (e == MXP_FP32 && (!native || pt <= MXP_FP32)) {
-                        p->img[4 * t + 3] = (long long)p->shadow_bytes;
+            if (native) {
+                // slot 1: fp16 codes h (FP16 consumers, and the high part for FP32 consumers);
+                // slot 3: fp16 remainders l (FP32 consumers of operands stored at FP32 or finer);
+                // slot 2: E4M3 codes (FP8 consumers)
+                const bool n16 = need[MXP_FP16] || need[MXP_FP32], n8 = need[MXP_FP8];
+                const bool nrem = need[MXP_FP32] && pt <= MXP_FP32;
+                if (n16) p->img[4 * t + 1] = (long long)p->shadow_bytes, p->shadow_bytes += nat::image_bytes(nat::K_F16, p->nb);
+                if (n8) p->img[4 * t + 2] = (long long)p->shadow_bytes, p->shadow_bytes += nat::image_bytes(nat::K_F8, p->nb);
+                if (nrem) p->img[4 * t + 3] = (long long)p->shadow_bytes, p->shadow_bytes += nat::image_bytes(nat::K_F16, p->nb);
+                any = n16 || n8;
+            } else {
+                for (int e = 1; e <= 3; ++e)
+                    if (need[e]) {
+                        any = true;
+                        p->img[4 * t + e - 1] = (long long)p->shadow_bytes;
                         p->shadow_bytes += img_bytes;
+                        if (e == MXP_FP32) {  // TF32 remainder of the FP32 image
+                            p->img[4 * t + 3] = (long long)p->shadow_bytes;
+                            p->shadow_bytes += img_bytes;
+                        }
                     }
-                }
+            }
             p->qtile[t] = (pt != MXP_FP64 || any) ? 1 : 0;
         }
     // Ozaki mode (in core; tiles below FP64 need the image engine): every
@@ -1328,6 +1337,16 @@ int mxp_chol_plan(int64_t n, int64_t nb, const uint8_t* precision_map, int ngpus
                 if (i == j && c != MXP_FP64) return -3;
                 map[tile_index(Nt, i, j)] = c;
             }
+    }
+    {  // every kernel loaded now, before any persistent kernel can be running (CUDA lazy
+       // loading at a first launch can wait for running kernels; co-located ranks deadlock)
+        static std::once_flag once;
+        std::call_once(once, [] {
+            preload_sched();
+            preload_layout();
+            preload_solve();
+            preload_generators();
+        });
     }
     auto* p = new mxp_plan_s();
     p->n = n;

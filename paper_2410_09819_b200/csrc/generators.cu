@@ -108,3 +108,14 @@ extern "C" int mxp_generate_matern_device(int64_t n, const double* xy_dev, doubl
     k_gen_matern<<<g, 256, 0, (cudaStream_t)stream>>>(n, xy_dev, sigma2, range_a, nugget, A, lda);
     return cudaGetLastError() == cudaSuccess ? MXP_OK : MXP_ECUDA;
 }
+
+namespace mxp {
+// (see preload_sched in sched_f64.cu)
+void preload_generators() {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, (const void*)k_gen_plgsy);
+    cudaFuncGetAttributes(&fa, (const void*)k_gen_kms);
+    cudaFuncGetAttributes(&fa, (const void*)k_gen_matern);
+    cudaGetLastError();
+}
+}  // namespace mxp

@@ -119,6 +119,11 @@ enum {
     STAT_POTRF = 16  // + 3k: kernel start, wait done, end
 };
 int sched_ctas_per_sm();
+// load every kernel of the library eagerly (one call per file; see preload_sched)
+void preload_sched();
+void preload_layout();
+void preload_solve();
+void preload_generators();
 // input stage of MxP (a3, O3): per-tile amax, then A^ = deq(q_p(A)) in place
 void launch_input_quantize(double* pool, const int32_t* slot, const uint8_t* prec, int64_t Nt, int64_t nb,
                            unsigned long long* amax_x, double* amax_s, cudaStream_t s, int rank = 0,

@@ -106,4 +106,17 @@ void launch_tile_norms(const double* A, int64_t lda, int64_t n, int64_t nb, doub
     k_tile_norms<<<grid, 256, 0, s>>>(A, lda, n, nb, Nt, norms);
 }
 
+
+// Load every kernel of this file now (CUDA lazy loading would otherwise load a
+// kernel at its first launch, which can wait for running kernels -- with ranks
+// co-located on one GPU those spin on each other: a deadlock).
+void preload_layout() {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, (const void*)k_pack);
+    cudaFuncGetAttributes(&fa, (const void*)k_unpack);
+    cudaFuncGetAttributes(&fa, (const void*)k_logdet_final);
+    cudaFuncGetAttributes(&fa, (const void*)k_tile_norms);
+    cudaGetLastError();
+}
+
 }  // namespace mxp

@@ -486,14 +486,21 @@ __device__ __noinline__ bool task_gemm_nat(const SchedArgs& a, int64_t m, int64_
     }
     __syncthreads();
     if (!*s_flag) return false;
-    const int slot = 1 + KIND;  // img[4t+1]: fp16 codes, img[4t+2]: E4M3 codes
+    // img[4t+1]: fp16 codes (FP16 and FP32 outputs), img[4t+2]: E4M3 codes, img[4t+3]: fp16 remainders
+    constexpr int slot = KIND == nat::K_F8 ? 2 : 1, sk = KIND == nat::K_F8 ? 1 : 0;
     auto src = [&](int i) {
         const int64_t n = n0 + i;
         const int64_t ta = tile_index(Nt, m, n), tb = tile_index(Nt, k, n);
         nat::NatTile o;
         o.a = a.shadow + a.img[4 * ta + slot] + nat::chunk_offset(KIND, nb, bi, 0);
         o.b = a.shadow + a.img[4 * tb + slot] + nat::chunk_offset(KIND, nb, bj, 0);
-        nat::inv_scales(__ldcg(a.iscale + 3 * ta + KIND), __ldcg(a.iscale + 3 * tb + KIND), o.inv0, o.inv1);
+        o.al = o.bl = nullptr;
+        if (KIND == nat::K_F32X2) {
+            const long long ra = a.img[4 * ta + 3], rb = a.img[4 * tb + 3];
+            if (ra >= 0) o.al = a.shadow + ra + nat::chunk_offset(KIND, nb, bi, 0);
+            if (rb >= 0) o.bl = a.shadow + rb + nat::chunk_offset(KIND, nb, bj, 0);
+        }
+        nat::inv_scales(__ldcg(a.iscale + 3 * ta + sk), __ldcg(a.iscale + 3 * tb + sk), o.inv0, o.inv1);
         return o;
     };
     double* Ct = tile_ptr(a.pool, a.slot, Nt, nb, m, k) + bi * 128 + bj * 128 * nb;
@@ -641,7 +648,7 @@ __device__ __noinline__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k
             const uint32_t off = tc::sw_offset(row & 127, col & 15);
 #pragma unroll
             for (int e = 0; e < 3; ++e) {
-                if (!im[e] || (a.native && e > 0)) continue;
+                if (!im[e] || a.native) continue;
                 float f[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) f[i] = (float)apply_cast(ce[e], x[i]);
@@ -659,7 +666,7 @@ __device__ __noinline__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k
             }
         }
     }
-    if (a.native && (im[1] || im[2])) {  // native-width code images (tc_native.cuh) of cast_FP16 / cast_FP8
+    if (a.native && (im[1] || im[2] || im[3])) {  // native-width code images (tc_native.cuh)
         sync_workers();
         // scale of the codes: the stored scale when the tile is stored at or below the image's
         // precision (up-cast: the stored codes themselves, exact in fp16 / E4M3), else the
@@ -679,6 +686,7 @@ __device__ __noinline__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k
                 for (int e = 0; e < 16; ++e) y[e] = apply_cast(c16, x[e]);
                 nat::write_f16_16(im[1], nb, row, (int)k0, y, s16);
             }
+            if (im[3]) nat::write_f16rem_16(im[3], nb, row, (int)k0, x, s16);  // (x stored at FP32 or finer)
             if (im[2]) {
                 double y[16];
 #pragma unroll
@@ -1243,6 +1251,8 @@ __global__ void __launch_bounds__(128, 1) k_tc(const SchedArgs* __restrict__ ap)
             if (threadIdx.x == 0) atomicAdd(a.tdiag + 12, 1);
             if (cp == P_FP64)
                 task_gemm_oz(a, m, k, it.w >> 16, it.w & 0xFFFF, smem_t, tmem, &s_flag);
+            else if (cp == P_FP32 && a.native)
+                task_gemm_nat<nat::K_F32X2>(a, m, k, it.w >> 16, it.w & 0xFFFF, smem_t, tmem, &s_flag);
             else if (cp == P_FP32)
                 task_gemm_img<true, 4>(a, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_t, tmem, &s_flag);
             else if (a.native && cp == P_FP16)
@@ -1409,6 +1419,22 @@ void launch_tc(const SchedArgs* a_dev, int grid, cudaStream_t s) {
 void launch_potrf_tile(const SchedArgs& a, int64_t k, cudaStream_t s) {
     configure_sched();
     k_potrf_tile<<<1, 256, POTRF_SMEM, s>>>(a, k);
+}
+
+
+// Load every kernel of this file now (CUDA lazy loading would otherwise load a
+// kernel at its first launch, which can wait for running kernels -- with ranks
+// co-located on one GPU those spin on each other: a deadlock).
+void preload_sched() {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, (const void*)k_sched<true>);
+    cudaFuncGetAttributes(&fa, (const void*)k_sched<false>);
+    cudaFuncGetAttributes(&fa, (const void*)k_tc);
+    cudaFuncGetAttributes(&fa, (const void*)k_potrf_tile);
+    cudaFuncGetAttributes(&fa, (const void*)k_matern_tile_norms);
+    cudaFuncGetAttributes(&fa, (const void*)k_tile_amax);
+    cudaFuncGetAttributes(&fa, (const void*)k_tile_quantize);
+    cudaGetLastError();
 }
 
 }  // namespace mxp

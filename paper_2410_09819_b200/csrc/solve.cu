@@ -139,4 +139,16 @@ void launch_sumsq(const double* z, int64_t n, double* out, cudaStream_t s) {
     k_sumsq<<<1, 1024, 0, s>>>(z, n, out);
 }
 
+
+// Load every kernel of this file now (CUDA lazy loading would otherwise load a
+// kernel at its first launch, which can wait for running kernels -- with ranks
+// co-located on one GPU those spin on each other: a deadlock).
+void preload_solve() {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, (const void*)k_trsv_diag);
+    cudaFuncGetAttributes(&fa, (const void*)k_trsv_gemv);
+    cudaFuncGetAttributes(&fa, (const void*)k_sumsq);
+    cudaGetLastError();
+}
+
 }  // namespace mxp

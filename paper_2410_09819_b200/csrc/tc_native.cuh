@@ -30,15 +30,21 @@
 namespace mxp {
 namespace nat {
 
-enum { K_F16 = 0, K_F8 = 1 };
+// K_F32X2: FP32 outputs -- each operand as fp16 codes h = RN(x s) plus the
+// remainder l = RN(x s - h) (both in the scale s: 22 bits, like 3xTF32 hi/lo),
+// products h h + h l + l h on kind::f16 (l l, 2^-22 relative, dropped)
+enum { K_F16 = 0, K_F8 = 1, K_F32X2 = 2 };
 constexpr int BM = 128, BN = 128;
 constexpr int CHUNK = 128 * 128;            // bytes per operand chunk
 constexpr int STAGE_BYTES = 2 * CHUNK;      // A | B
 constexpr int NST = 4;                      // stages
 constexpr int SMEM_BYTES = 1024 + NST * STAGE_BYTES + 128;
 
-__host__ __device__ constexpr int ke(int kind) { return kind == K_F16 ? 64 : 128; }  // K per chunk
-__host__ __device__ constexpr int64_t image_bytes(int kind, int64_t nb) { return nb * nb * (kind == K_F16 ? 2 : 1); }
+__host__ __device__ constexpr int ke(int kind) { return kind == K_F8 ? 128 : 64; }  // K per chunk
+__host__ __device__ constexpr int64_t image_bytes(int kind, int64_t nb) { return nb * nb * (kind == K_F8 ? 1 : 2); }
+// stages and chunks per stage: A | B (| A remainder | B remainder for K_F32X2)
+__host__ __device__ constexpr int nstages(int kind) { return kind == K_F32X2 ? 2 : NST; }
+__host__ __device__ constexpr int stage_bytes(int kind) { return (kind == K_F32X2 ? 4 : 2) * CHUNK; }
 __host__ __device__ constexpr int64_t chunk_offset(int kind, int64_t nb, int64_t rb, int64_t kc) {
     return (rb * (nb / ke(kind)) + kc) * CHUNK;
 }
@@ -63,7 +69,7 @@ constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)
 
 template <int KIND>
 __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
-    if constexpr (KIND == K_F16)
+    if constexpr (KIND != K_F8)
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
             "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
@@ -99,6 +105,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
 struct NatTile {
     const uint8_t* a;
     const uint8_t* b;
+    const uint8_t* al;  // K_F32X2: remainder images (nullptr: the operand is exact in fp16 codes)
+    const uint8_t* bl;
     float inv0, inv1;
 };
 
@@ -134,54 +142,66 @@ __device__ __forceinline__ void drain_tile(uint32_t tl, int buf, bool first, con
 // 255-register warp fills one SM sub-partition's register file.
 template <int KIND, class Src>
 __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, int kt, uint8_t* smem, uint32_t tmem) {
+    constexpr int NS = nstages(KIND), SB = stage_bytes(KIND);
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(base + NST * STAGE_BYTES);
-    uint64_t* empty = full + NST;
-    uint64_t* tfull = empty + NST;  // [2] accumulator ready for the drain
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + NS * SB);
+    uint64_t* empty = full + NS;
+    uint64_t* tfull = empty + NS;   // [2] accumulator ready for the drain
     uint64_t* tempty = tfull + 2;   // [2] accumulator drained (4 warps arrive)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int G = ntiles * kt;
     const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
     if (tid == 0) {
-        for (int i = 0; i < NST; ++i) tc::mbar_init(full + i, 1), tc::mbar_init(empty + i, 1);
+        for (int i = 0; i < NS; ++i) tc::mbar_init(full + i, 1), tc::mbar_init(empty + i, 1);
         for (int i = 0; i < 2; ++i) tc::mbar_init(tfull + i, 1), tc::mbar_init(tempty + i, 4);
         tc::fence_mbar_init();
     }
     __syncthreads();
     if (warp == 0) {
-        NatTile cur{};
+        NatTile cur{}, curm{};
         int cur_i = -1;
         auto issue = [&](int g) {  // bulk copies of K step g into its stage (elected lane)
-            const int st = g % NST, i = g / kt, kc = g - i * kt;
+            const int st = g % NS, i = g / kt, kc = g - i * kt;
             if (i != cur_i) cur = src(i), cur_i = i;
-            uint8_t* sa = base + st * STAGE_BYTES;
-            tc::mbar_expect_tx(full + st, (uint32_t)STAGE_BYTES);
-            tc::bulk_g2s(sa, cur.a + (int64_t)kc * CHUNK, CHUNK, full + st);
-            tc::bulk_g2s(sa + CHUNK, cur.b + (int64_t)kc * CHUNK, CHUNK, full + st);
+            uint8_t* sa = base + st * SB;
+            const int64_t o = (int64_t)kc * CHUNK;
+            uint32_t bytes = 2 * CHUNK;
+            if (KIND == K_F32X2) bytes += (cur.al ? CHUNK : 0) + (cur.bl ? CHUNK : 0);
+            tc::mbar_expect_tx(full + st, bytes);
+            tc::bulk_g2s(sa, cur.a + o, CHUNK, full + st);
+            tc::bulk_g2s(sa + CHUNK, cur.b + o, CHUNK, full + st);
+            if (KIND == K_F32X2 && cur.al) tc::bulk_g2s(sa + 2 * CHUNK, cur.al + o, CHUNK, full + st);
+            if (KIND == K_F32X2 && cur.bl) tc::bulk_g2s(sa + 3 * CHUNK, cur.bl + o, CHUNK, full + st);
         };
-        auto refill = [&](int g) {  // stage of step g (its MMAs issued) -> step g + NST
-            if (g >= 0 && g + NST < G) {
-                tc::mbar_wait(empty + (g % NST), (uint32_t)((g / NST) & 1));
-                issue(g + NST);
+        auto refill = [&](int g) {  // stage of step g (its MMAs issued) -> step g + NS
+            if (g >= 0 && g + NS < G) {
+                tc::mbar_wait(empty + (g % NS), (uint32_t)((g / NS) & 1));
+                issue(g + NS);
             }
         };
         if (lane == 0)
-            for (int g = 0; g < NST && g < G; ++g) issue(g);
+            for (int g = 0; g < NS && g < G; ++g) issue(g);
         for (int i = 0; i < ntiles; ++i) {
             const int buf = i & 1;
             if (lane == 0) {
+                if (KIND == K_F32X2) curm = src(i);
                 if (i >= 2) tc::mbar_wait(tempty + buf, (uint32_t)(((i >> 1) - 1) & 1));
                 tc::fence_after();
                 const uint32_t d = tmem + (uint32_t)(buf * BN);
                 for (int kc = 0; kc < kt; ++kc) {
-                    const int g = i * kt + kc, st = g % NST;
-                    tc::mbar_wait(full + st, (uint32_t)((g / NST) & 1));
+                    const int g = i * kt + kc, st = g % NS;
+                    tc::mbar_wait(full + st, (uint32_t)((g / NS) & 1));
                     tc::fence_after();
-                    const uint32_t sa = tc::smem_u32(base + st * STAGE_BYTES);
+                    const uint32_t sa = tc::smem_u32(base + st * SB);
                     const uint64_t ad = make_desc(sa), bd = make_desc(sa + CHUNK);
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)  // 32 bytes of K per MMA: +2 in the 16-byte address field
+                    for (int kk = 0; kk < 4; ++kk) {  // 32 bytes of K per MMA: +2 in the 16-byte address field
                         mma<KIND>(d, ad + 2 * kk, bd + 2 * kk, (kc | kk) ? 1u : 0u);
+                        if (KIND == K_F32X2) {
+                            if (curm.bl) mma<KIND>(d, ad + 2 * kk, make_desc(sa + 3 * CHUNK) + 2 * kk, 1u);
+                            if (curm.al) mma<KIND>(d, make_desc(sa + 2 * CHUNK) + 2 * kk, bd + 2 * kk, 1u);
+                        }
+                    }
                     tc::commit(empty + st);
                     // refill the previous step's stage once its MMAs have read it (this step's
                     // MMAs stay queued behind them); at the last step of a K tile the refill
@@ -248,7 +268,7 @@ __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, i
     }
     __syncthreads();
     if (tid == 0) {
-        for (int i = 0; i < NST; ++i) tc::mbar_inval(full + i), tc::mbar_inval(empty + i);
+        for (int i = 0; i < NS; ++i) tc::mbar_inval(full + i), tc::mbar_inval(empty + i);
         for (int i = 0; i < 2; ++i) tc::mbar_inval(tfull + i), tc::mbar_inval(tempty + i);
     }
 }
@@ -271,6 +291,17 @@ __device__ __forceinline__ void write_f16_16(uint8_t* img, int64_t nb, int row, 
     uint8_t* ch = img + chunk_offset(K_F16, nb, rb, kc);
     __stcg(reinterpret_cast<uint4*>(ch + sw128(row & 127, kb)), make_uint4(w[0], w[1], w[2], w[3]));
     __stcg(reinterpret_cast<uint4*>(ch + sw128(row & 127, kb + 16)), make_uint4(w[4], w[5], w[6], w[7]));
+}
+// fp16 remainders l = RN(x s - RN(x s)) of 16 consecutive K elements (K_F32X2)
+__device__ __forceinline__ void write_f16rem_16(uint8_t* img, int64_t nb, int row, int k0, const double (&x)[16],
+                                                double s) {
+    double r[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        const double y = x[e] * s;
+        r[e] = y - (double)__half2float(__double2half(y));
+    }
+    write_f16_16(img, nb, row, k0, r, 1.0);
 }
 __device__ __forceinline__ void write_f8_16(uint8_t* img, int64_t nb, int row, int k0, const double (&x)[16],
                                             double s) {

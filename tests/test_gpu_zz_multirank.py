@@ -9,7 +9,7 @@ import pytest
 import oracle
 import workloads as w
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.isolated(timeout=240)]
 
 
 def _ranks(n, nb, P, pmap=None, attrs=None):
