@@ -64,7 +64,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-mxp", action="store_true")
     ap.add_argument("--mxp-n", type=int, default=131072)
-    ap.add_argument("--mxp-eps", type=float, nargs="*", default=[1e-8, 1e-5])
+    ap.add_argument("--mxp-eps", type=float, nargs="*", default=[1e-5, 1e-6, 1e-7, 1e-8, 1e-9])
+    ap.add_argument("--kl-n", type=int, default=32768)
+    ap.add_argument("--no-kl", action="store_true")
     ap.add_argument("--no-ooc", action="store_true")
     ap.add_argument("--ooc-n", type=int, default=98304)
     ap.add_argument("--ooc-frac", type=float, default=0.65)
@@ -151,6 +153,47 @@ def cpu_oracle_sample(n=2048, nb=256, seed=42):
                       f"seconds; rate = (n^3/3)/t"}
 
 
+def cpu_baselines(seed=42):
+    """SURVEY 8(d) oracle timing table on the host cores: C1 exactly, FP64 and 4-precision Matern
+    at n = 4096, plus LAPACK dpotrf (numpy/OpenBLAS) at n = 16384 as the optimized-CPU point.
+    Rates in GFLOP/s = (n^3/3)/t; the larger configs are extrapolated by n^3 in DESIGN.md."""
+    import numpy as np
+
+    import oracle
+    import workloads as w
+    oracle.build()
+    out = {"cores": os.cpu_count()}
+
+    def t_oracle(A, nb, pmap=None):
+        t0 = time.perf_counter()
+        _, info = oracle.factor(A, nb, pmap)
+        assert info == 0
+        return time.perf_counter() - t0
+    A = w.kms(1024, 0.5)
+    t = t_oracle(A, 256)
+    out["c1_oracle"] = {"n": 1024, "nb": 256, "s": t, "gflops": 1024 ** 3 / 3 / t / 1e9}
+    A = w.plgsy(4096, seed)
+    t = t_oracle(A, 256)
+    out["oracle_fp64_n4096"] = {"nb": 256, "s": t, "gflops": 4096 ** 3 / 3 / t / 1e9}
+    xy = w.matern_locations(4096, seed=1)
+    S = w.matern_cov(xy, 1.0, 0.02627)
+    pm = oracle.plan(S, 256, 1e-5)
+    t = t_oracle(S, 256, pm)
+    out["oracle_mxp_n4096"] = {"nb": 256, "eps": 1e-5, "s": t, "gflops": 4096 ** 3 / 3 / t / 1e9}
+    A = w.plgsy(16384, seed)
+    t0 = time.perf_counter()
+    np.linalg.cholesky(A)
+    t = time.perf_counter() - t0
+    try:
+        import threadpoolctl
+        th = [x.get("num_threads") for x in threadpoolctl.threadpool_info() if x.get("user_api") == "blas"]
+    except Exception:
+        th = None
+    out["lapack_dpotrf_n16384"] = {"s": t, "gflops": 16384 ** 3 / 3 / t / 1e9, "blas_threads": th,
+                                   "how": "numpy.linalg.cholesky (LAPACK dpotrf via numpy's BLAS)"}
+    return out
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -178,12 +221,14 @@ def run_reference(args):
 
 
 def int8_peak():
-    """Dense int8 tensor peak: MEASURED_PEAKS.json's bf16 dense figure x the nominal int8:bf16 ratio (2)."""
+    """Dense int8 tensor peak: MEASURED_PEAKS.json's sustained bf16 dense figure (k_tc runs for
+    seconds inside the step) x the nominal int8:bf16 ratio (2)."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             pk = json.load(f)
-        return 2.0 * pk["bf16_tflops"], ("2 x MEASURED_PEAKS.json bf16_tflops (burst, %.1f) -- B200 int8:bf16 "
-                                         "dense ratio 2 (4.5 POPS : 2.25 PFLOPS nominal)" % pk["bf16_tflops"])
+        return 2.0 * pk["bf16_tflops_sustained"], (
+            "2 x MEASURED_PEAKS.json bf16_tflops_sustained (%.1f; the kernel runs for seconds) -- B200 "
+            "int8:bf16 dense ratio 2 (4.5 POPS : 2.25 PFLOPS nominal)" % pk["bf16_tflops_sustained"])
     except Exception:
         return 4500.0, "nominal B200 dense int8 4.5 POPS (MEASURED_PEAKS.json absent)"
 
@@ -197,6 +242,256 @@ def load_traffic(nb, engine="dmma"):
         return d.get("dram_bytes_per_launch"), d
     except Exception:
         return None, None
+
+
+def residual_fro(A, B, nbk=4096):
+    """||A - L L^T||_F / ||A||_F, L = tril(B), by block columns (cuBLAS DGEMM; independent
+    of our kernels): the diagonal block once, the blocks below it twice (symmetry)."""
+    import torch
+    n = A.shape[0]
+    ss = 0.0
+    for j0 in range(0, n, nbk):
+        j1 = min(n, j0 + nbk)
+        Lr = torch.tril(B[j0:, :j1], diagonal=j0)           # rows j0.. of L, columns < j1
+        R = A[j0:, j0:j1] - Lr @ Lr[: j1 - j0].T             # block column j of A - L L^T, rows >= j0
+        ss += R[: j1 - j0].norm().item() ** 2 + 2.0 * R[j1 - j0:].norm().item() ** 2
+        del Lr, R
+    return ss ** 0.5 / torch.linalg.matrix_norm(A).item()
+
+
+def mxp_flops_by_precision(pmap, Nt, nb):
+    """Per-precision flops of one factorization (SURVEY 8(d) roofline): GEMM (m,k,n) in p(m,k),
+    SYRK in FP64, TRSM nb^3 in FP64 (DMMA), POTRF nb^3/3.  Returns {"fp64_gemm", "fp32", "fp16",
+    "fp8", "trsm", "potrf"} in flops; they sum to (Nt nb)^3 / 3."""
+    import numpy as np
+    F = {"fp64_gemm": 0.0, "fp32": 0.0, "fp16": 0.0, "fp8": 0.0, "trsm": 0.0, "potrf": 0.0}
+    nb3 = float(nb) ** 3
+    key = {0: "fp64_gemm", 1: "fp32", 2: "fp16", 3: "fp8"}
+    pm = np.asarray(pmap)
+    for k in range(Nt):
+        t0 = k * Nt - k * (k - 1) // 2
+        F["fp64_gemm"] += k * nb3          # SYRK of the diagonal tile
+        F["potrf"] += nb3 / 3
+        for m in range(k + 1, Nt):
+            F[key[int(pm[t0 + m - k])]] += 2.0 * k * nb3
+            F["trsm"] += nb3
+    return F
+
+
+def mxp_roofline(F, peaks):
+    """T_compute = sum_p F_p / peak_p; roof = (n^3/3) / T_compute (TFLOP/s)."""
+    T = sum(F[k] / (peaks[k] * 1e12) for k in F if F[k] > 0)
+    return sum(F.values()) / T / 1e12, T
+
+
+def run_c3(args, m, dev, dev_index, stream, ws, new_plan, allreduce, barrier, dgemm_peak):
+    import gc
+    import math
+
+    import numpy as np
+    import torch
+
+    import workloads as w
+    gc.collect()
+    torch.cuda.empty_cache()
+    nm, nbm, theta = args.mxp_n, args.nb, (1.0, 0.02627, 0.5)
+    Nt = -(-nm // nbm)
+    xy = w.matern_locations(nm, seed=1)
+    xyd = torch.as_tensor(xy, device=dev).contiguous()
+    gz = torch.Generator(device=dev).manual_seed(2)
+    z = torch.randn(nm, dtype=torch.float64, device=dev, generator=gz)
+    flops_m = nm ** 3 / 3
+    out = {"workload": f"C3: Matern nu=0.5 theta=(1, 0.02627, 0.5) (weak), n={nm}, nb={nbm}, Morton-sorted "
+                       f"uniform locations (seed 1), tiles generated on the device inside the schedule",
+           "maps": {}}
+    const = -0.5 * nm * math.log(2 * math.pi)
+
+    # ---- independent FP64 reference: cuSOLVER potrf (upper) on the dense matrix (137 GB), in its
+    #      own process (a cuSOLVER fault must not poison this context); it also returns y = Sigma z
+    y = None
+    cus = None
+    if ws == 1:
+        import subprocess
+        import tempfile
+        gc.collect()
+        torch.cuda.empty_cache()
+        tmp = os.path.join(tempfile.mkdtemp(), "c3_ref.npz")
+        try:
+            r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "cusolver_c3.py"), str(nm), str(theta[1]),
+                                tmp], capture_output=True, text=True, timeout=600)
+            if r.returncode == 0:
+                d = np.load(tmp)
+                meta = json.loads(str(d["meta"]))
+                y = torch.as_tensor(d["y"], device=dev)
+                cus = dict(meta, loglik_y0=const - 0.5 * meta["logdet"],
+                           loglik_y=const - 0.5 * meta["logdet"] - 0.5 * meta["quad_form"],
+                           how="cusolverDnXpotrf (upper, fp64) on the dense generated covariance in a child "
+                               "process; logdet from diag(U); y^T Sigma^-1 y by cusolverDnXpotrs; y = Sigma z, "
+                               "z seeded normal (seed 2), computed before the factorization")
+            else:
+                cus = {"error": (r.stderr or r.stdout)[-300:]}
+        except Exception as e:  # noqa -- a library baseline must not abort our measurement
+            cus = {"error": repr(e)[:300]}
+    out["cusolver_fp64"] = cus
+    if y is None:
+        y = torch.randn(nm, dtype=torch.float64, device=dev, generator=torch.Generator(device=dev).manual_seed(3))
+
+    def run(pmap, reps, fp64_engine=None):
+        pl = new_plan(nm, nbm, pmap, engine=fp64_engine)
+        pl.set("profile", 0)
+        ts = []
+        for i in range(reps):
+            torch.cuda.synchronize()
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            inf = pl.factor_matern(xyd, theta[0], theta[1])
+            e1.record(stream)
+            torch.cuda.synchronize()
+            assert inf == 0, inf
+            ts.append(allreduce(e0.elapsed_time(e1) / 1e3, "max"))
+        r = {"t": min(ts[1:] if len(ts) > 1 else ts), "logdet": pl.logdet(),
+             "ws_gb": pl.workspace_size() / 1e9, "img_gb": pl.get("image_bytes") / 1e9,
+             "fp64_engine": "ozaki" if pl.get("fp64_engine_used") == 1 else "dmma",
+             "tc_engine": pl.get("tc_engine_used"), "compact": pl.get("compact_used")}
+        if ws == 1:
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r["loglik_y"] = pl.loglik(y)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            r["solve_ms"] = e0.elapsed_time(e1)
+        pl.close()
+        del pl
+        gc.collect()
+        torch.cuda.empty_cache()
+        return r
+
+    reps = 2  # one warm-up + one timed factorization per configuration (bounded bench time)
+    r64 = run(None, reps)
+    ll64 = const - 0.5 * r64["logdet"]
+    out["fp64"] = {"tflops": flops_m / r64["t"] / 1e12, "ms": r64["t"] * 1e3, "logdet": r64["logdet"],
+                   "engine": r64["fp64_engine"], "loglik_y0": ll64, "loglik_y": r64.get("loglik_y")}
+    if r64.get("solve_ms"):
+        lower_bytes = Nt * (Nt + 1) // 2 * nbm * nbm * 8
+        out["fp64"]["forward_solve"] = {
+            "ms": r64["solve_ms"], "gbs": lower_bytes / (r64["solve_ms"] / 1e3) / 1e9,
+            "how": "mxp_chol_loglik(y): forward solve L z = y (every lower tile read once) + ||z||^2"}
+    if cus and "logdet" in cus:
+        out["fp64"]["loglik_y0_rel_err_vs_cusolver"] = abs(ll64 - cus["loglik_y0"]) / abs(cus["loglik_y0"])
+        if r64.get("loglik_y") is not None:
+            out["fp64"]["loglik_y_rel_err_vs_cusolver"] = abs(r64["loglik_y"] - cus["loglik_y"]) / abs(cus["loglik_y"])
+    best_fp64 = max(out["fp64"]["tflops"], (cus or {}).get("tflops") or 0.0)
+    # measured sustained peaks for the per-precision roofline (SURVEY 8(d)): FP64 GEMM/SYRK on
+    # the int8 pipe (36 products) or DMMA; FP32 = 3 fp16 products (h h + h l + l h); FP16 = bf16
+    # dense; FP8 = 2x; TRSM / POTRF on DMMA (live DGEMM)
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            bf16 = json.load(f)["bf16_tflops_sustained"]
+    except Exception:
+        bf16 = 2250.0 * 0.6
+    peaks = {"fp64_gemm": 2 * bf16 / 36, "fp32": bf16 / 3, "fp16": bf16, "fp8": 2 * bf16, "trsm": dgemm_peak,
+             "potrf": dgemm_peak}
+    g16 = {}
+    for eps in args.mxp_eps:
+        pmap, _ = m.precision_map_matern_device(xyd, nbm, eps, theta[0], theta[1])
+        r = run(pmap, reps)
+        llm = const - 0.5 * r["logdet"]
+        F = mxp_flops_by_precision(pmap, Nt, nbm)
+        pk = dict(peaks)
+        if r["fp64_engine"] == "dmma":
+            pk["fp64_gemm"] = dgemm_peak
+        roof, _ = mxp_roofline(F, pk)
+        tfl = flops_m / r["t"] / 1e12
+        e = {"tflops": tfl, "ms": r["t"] * 1e3, "speedup_vs_fp64": out["fp64"]["tflops"] and tfl / out["fp64"]["tflops"],
+             "speedup_vs_best_fp64": tfl / best_fp64,
+             "engines": {"fp64": r["fp64_engine"], "below_fp64": {3: "native (kind::f16/f8f6f4)", 1: "tf32 images",
+                                                                  2: "tf32 registers", 0: "dmma"}.get(r["tc_engine"])},
+             "compact_pool": bool(r["compact"]), "workspace_gb": round(r["ws_gb"], 2),
+             "image_gb": round(r["img_gb"], 2),
+             "tile_fractions_fp64_fp32_fp16_fp8": [round(float(np.mean(pmap == c)), 4) for c in range(4)],
+             "flop_fractions": {k: round(v / flops_m, 4) for k, v in F.items()},
+             "roofline": {"roof_tflops": roof, "frac": tfl / roof,
+                          "how": "roof = (n^3/3) / sum_p F_p/peak_p; peaks: FP64 GEMM = 2 x bf16 sustained / 36 "
+                                 "(Ozaki) or live DGEMM, FP32 = bf16/3, FP16 = bf16, FP8 = 2 x bf16, TRSM/POTRF = DGEMM"},
+             "loglik_y0_rel_err": abs(llm - ll64) / abs(ll64), "logdet_abs_diff": abs(r["logdet"] - r64["logdet"]),
+             "kl_eq3": ll64 - llm}
+        if r.get("loglik_y") is not None and r64.get("loglik_y") is not None:
+            e["loglik_y_rel_err"] = abs(r["loglik_y"] - r64["loglik_y"]) / abs(r64["loglik_y"])
+        if cus and "logdet" in cus:
+            e["loglik_y0_rel_err_vs_cusolver"] = abs(llm - cus["loglik_y0"]) / abs(cus["loglik_y0"])
+            if r.get("loglik_y") is not None:
+                e["loglik_y_rel_err_vs_cusolver"] = abs(r["loglik_y"] - cus["loglik_y"]) / abs(cus["loglik_y"])
+        ok = e["loglik_y0_rel_err"] <= 1e-6 and e.get("loglik_y_rel_err", 0.0) <= 1e-6
+        e["meets_g16"] = ok
+        if ok:
+            g16[eps] = e
+        out["maps"][f"{eps:g}"] = e
+    if g16:
+        eps_best = max(g16)
+        out["largest_eps_meeting_g16"] = {"eps": eps_best, "tflops": g16[eps_best]["tflops"],
+                                          "speedup_vs_best_fp64": g16[eps_best]["speedup_vs_best_fp64"],
+                                          "g16": "|l_MxP - l_FP64| / |l_FP64| <= 1e-6 at y = 0 and y = Sigma z"}
+    out["note"] = ("TFLOP/s = (n^3/3)/t, t = one factorization incl. fused generation (1 warm-up + 1 timed); "
+                   "loglik vs our FP64 run of the same pipeline and vs cuSOLVER")
+    return out
+
+
+def run_kl_sweep(args, m, dev, new_plan):
+    """N1: Eq. 3 KL = l_FP64(theta;0) - l_MxP(theta;0) and l at y = Sigma z over the
+    three correlations x eps at n = args.kl_n (the C3 size is the eps sweep of run_c3)."""
+    import gc
+    import math
+
+    import torch
+
+    import workloads as w
+    n, nb = args.kl_n, args.nb
+    xy = w.matern_locations(n, seed=1)
+    xyd = torch.as_tensor(xy, device=dev).contiguous()
+    z = torch.randn(n, dtype=torch.float64, device=dev, generator=torch.Generator(device=dev).manual_seed(2))
+    const = -0.5 * n * math.log(2 * math.pi)
+    rows = []
+    for name, a in (("weak", 0.02627), ("medium", 0.078809), ("strong", 0.210158)):
+        A = torch.empty((n, n), dtype=torch.float64, device=dev).T
+        m.generate_matern_device(A, xyd, 1.0, a)
+        y = A @ z
+        del A
+        torch.cuda.empty_cache()
+        res = {}
+        for eps in [None] + list(args.mxp_eps):
+            pmap = None if eps is None else m.precision_map_matern_device(xyd, nb, eps, 1.0, a)[0]
+            pl = new_plan(n, nb, pmap)
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record()
+            info = pl.factor_matern(xyd, 1.0, a)
+            t1.record()
+            torch.cuda.synchronize()
+            res[eps] = (info, pl.logdet() if info == 0 else None, pl.loglik(y) if info == 0 else None,
+                        t0.elapsed_time(t1))
+            pl.close()
+            gc.collect()
+            torch.cuda.empty_cache()
+        i64, ld64, lly64, _ = res[None]
+        l0 = const - 0.5 * ld64
+        for eps in args.mxp_eps:
+            info, ld, lly, ms = res[eps]
+            if info != 0:
+                rows.append({"theta": name, "range_a": a, "eps": eps, "info": info})
+                continue
+            la = const - 0.5 * ld
+            kl = l0 - la
+            rows.append({"theta": name, "range_a": a, "eps": eps, "kl_eq3": kl,
+                         "log10_abs_kl": math.log10(abs(kl)) if kl else None,
+                         "loglik_y0_rel_err": abs(la - l0) / abs(l0),
+                         "loglik_y_rel_err": abs(lly - lly64) / abs(lly64), "ms": ms})
+    return {"n": n, "nb": nb, "rows": rows,
+            "how": "Eq. 3 KL = l0(theta;0) - la(theta;0) (G17, signed), l0 = FP64 factorization, la = MxP map "
+                   "at eps; l(y) at y = Sigma z; tiles generated in the schedule"}
 
 
 def run_ours(args):
@@ -288,13 +583,16 @@ def run_ours(args):
     value = flops / t_step / 1e12  # one n x n factorization per step, over all ranks
 
     progress("C2 timed")
-    # correctness probe on the last factor: ||(A - L L^T) x|| / (||A||_F ||x||)
+    # accuracy of the last factor: the full backward error ||A - L L^T||_F / ||A||_F (blockwise
+    # cuBLAS DGEMM, independent of our kernels) and the randomized probe ||(A - L L^T) x|| / ||A x||
+    backward_error = residual_fro(A, B) if ws == 1 else None
     L = torch.tril(B)
     g = torch.Generator(device=dev)
     g.manual_seed(7)
     x = torch.randn(n, 4, dtype=torch.float64, device=dev, generator=g)
-    probe = ((A @ x - L @ (L.T @ x)).norm() / (torch.linalg.matrix_norm(A) * x.norm())).item()
-    del L, x
+    Ax = A @ x
+    probe = ((Ax - L @ (L.T @ x)).norm() / Ax.norm()).item()
+    del L, x, Ax
     logdet = plan.logdet()
     sched = plan.sched_diagnostics()
     if sched:
@@ -307,8 +605,8 @@ def run_ours(args):
 
     progress("probe")
     # the other FP64 engine on the same input (same step, fewer reps)
-    engines = {engine_used: {"tflops": value, "ms": t_step * 1e3, "backward_error_probe": probe,
-                             "logdet": logdet}}
+    engines = {engine_used: {"tflops": value, "ms": t_step * 1e3, "backward_error_fro": backward_error,
+                             "backward_error_probe": probe, "logdet": logdet}}
     if not args.no_engine_compare:
         other = "dmma" if engine_used == "ozaki" else "ozaki"
         pl2 = new_plan(n, nb, engine=other)
@@ -326,13 +624,15 @@ def run_ours(args):
             assert inf == 0, inf
             if i:
                 ts.append(allreduce(e0.elapsed_time(e1) / 1e3, "max"))
+        be2 = residual_fro(A, B) if ws == 1 else None
         L2 = torch.tril(B)
         x2 = torch.randn(n, 4, dtype=torch.float64, device=dev, generator=torch.Generator(device=dev).manual_seed(7))
-        pr2 = ((A @ x2 - L2 @ (L2.T @ x2)).norm() / (torch.linalg.matrix_norm(A) * x2.norm())).item()
-        del L2, x2
+        Ax2 = A @ x2
+        pr2 = ((Ax2 - L2 @ (L2.T @ x2)).norm() / Ax2.norm()).item()
+        del L2, x2, Ax2
         used2 = "ozaki" if pl2.get("fp64_engine_used") == 1 else "dmma"
-        engines[used2] = {"tflops": flops / min(ts) / 1e12, "ms": min(ts) * 1e3, "backward_error_probe": pr2,
-                          "logdet": pl2.logdet()}
+        engines[used2] = {"tflops": flops / min(ts) / 1e12, "ms": min(ts) * 1e3, "backward_error_fro": be2,
+                          "backward_error_probe": pr2, "logdet": pl2.logdet()}
         pl2.close()
         del pl2
         torch.cuda.empty_cache()
@@ -465,91 +765,20 @@ def run_ours(args):
     torch.cuda.empty_cache()
 
     progress("e2e")
-    # C3 (BASELINE configs[2]): Matern nu=0.5 weak correlation, 4-precision map,
-    # n = 131072, generated tile by tile on the device inside the schedule;
-    # log-likelihood at y = 0 (Eq. 3 convention, G16) vs the FP64 factorization
+    # C3 (BASELINE configs[2]): Matern nu=0.5 weak correlation, n = 131072, 4-precision maps
+    # over eps in {1e-5 ... 1e-9}, tiles generated on the device inside the schedule.  FP64
+    # references: our FP64 run and cuSOLVER potrf on the dense 137 GB matrix (independent).
+    # Log-likelihood (Eq. 1) at y = 0 (Eq. 3 convention) and at y = Sigma z (z seeded normal), for
+    # which y^T Sigma^-1 y = y^T z exactly (G16).
     mxp = None
     if not args.no_mxp:
-        import math
-
-        import numpy as np
-
-        import workloads as w
-        import gc
-        gc.collect()
-        torch.cuda.empty_cache()
-        free_gb = torch.cuda.mem_get_info()[0] / 1e9
-        nm, nbm, theta = args.mxp_n, args.nb, (1.0, 0.02627, 0.5)
-        xy = w.matern_locations(nm, seed=1)
-        xyd = torch.as_tensor(xy, device=dev).contiguous()
-        yd = torch.randn(nm, dtype=torch.float64, device=dev, generator=torch.Generator(device=dev).manual_seed(3))
-        flops_m = nm ** 3 / 3
-
-        def run(pmap, reps):
-            pl = new_plan(nm, nbm, pmap)
-            pl.set("profile", 0)
-            ts = []
-            for i in range(reps):
-                torch.cuda.synchronize()
-                barrier()
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                inf = pl.factor_matern(xyd, theta[0], theta[1])
-                e1.record(stream)
-                torch.cuda.synchronize()
-                assert inf == 0, inf
-                ts.append(allreduce(e0.elapsed_time(e1) / 1e3, "max"))
-            ld_ = pl.logdet()
-            # N1: Eq. 1 log-likelihood at a seeded y (forward solve on the resident factor)
-            run.ll_y = None
-            if ws == 1:
-                torch.cuda.synchronize()
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                run.ll_y = pl.loglik(yd)
-                e1.record(stream)
-                torch.cuda.synchronize()
-                run.solve_ms = e0.elapsed_time(e1)
-            run.ws_gb = pl.workspace_size() / 1e9
-            run.img_gb = pl.get("image_bytes") / 1e9
-            pl.close()
-            del pl
-            gc.collect()
-            torch.cuda.empty_cache()
-            return min(ts[1:] if len(ts) > 1 else ts), ld_
-
-        t64, ld64 = run(None, 1 + max(1, args.steps // 3))
-        ll64 = -0.5 * nm * math.log(2 * math.pi) - 0.5 * ld64
-        mxp = {"workload": f"C3: Matern nu=0.5 theta=(1, 0.02627, 0.5) (weak), n={nm}, nb={nbm}, Morton-sorted "
-                           f"uniform locations (seed 1), tiles generated on the device inside the schedule",
-               "fp64": {"tflops": flops_m / t64 / 1e12, "ms": t64 * 1e3, "logdet": ld64}, "maps": {},
-               "fp64_engine": args.fp64_engine,
-               "device_free_gb_at_start": round(free_gb, 1)}
-        ll64_y = run.ll_y
-        if ll64_y is not None:
-            lower_bytes = (nm // nbm) * (nm // nbm + 1) // 2 * nbm * nbm * 8
-            mxp["fp64"]["loglik_y"] = ll64_y
-            mxp["fp64"]["forward_solve"] = {
-                "ms": run.solve_ms, "gbs": lower_bytes / (run.solve_ms / 1e3) / 1e9,
-                "how": "mxp_chol_loglik(y): forward solve L z = y (every lower tile read once) + ||z||^2, "
-                       "CUDA events; GB/s = lower-triangle bytes / time (HBM roofline: MEASURED_PEAKS hbm_gbs)"}
-        for eps in args.mxp_eps:
-            pmap, _ = m.precision_map_matern_device(xyd, nbm, eps, theta[0], theta[1])
-            tm, ldm = run(pmap, 1 + max(1, args.steps // 3))
-            llm = -0.5 * nm * math.log(2 * math.pi) - 0.5 * ldm
-            mxp["maps"][f"{eps:g}"] = {
-                "tflops": flops_m / tm / 1e12, "ms": tm * 1e3, "speedup_vs_fp64": t64 / tm,
-                "workspace_gb": round(run.ws_gb, 2), "operand_images_gb": round(run.img_gb, 2),
-                "tile_fractions_fp64_fp32_fp16_fp8": [round(float(np.mean(pmap == c)), 4) for c in range(4)],
-                "loglik_y0_rel_err": abs(llm - ll64) / abs(ll64), "logdet_abs_diff": abs(ldm - ld64),
-                "loglik_y_rel_err": (abs(run.ll_y - ll64_y) / abs(ll64_y)) if ll64_y is not None else None,
-                "kl_eq3": ll64 - llm}
-        mxp["note"] = ("value/units: TFLOP/s = (n^3/3)/t, t = factorization incl. fused generation; loglik at "
-                       "y=0 vs the FP64 run of the same pipeline (G16); 1 warm-up + timed reps, best")
+        mxp = run_c3(args, m, dev, dev_index, stream, ws, new_plan, allreduce, barrier, dgemm_peak)
 
     progress("C3")
+    kl = None
+    if not args.no_kl and ws == 1:
+        kl = run_kl_sweep(args, m, dev, new_plan)
+        progress("KL sweep")
     # Out of core (a5/a9; C4's mode at a size this box's host RAM holds): the
     # host matrix streamed through a pool capped at ooc_frac of the lower
     # triangle (dead-tile slot recycling) vs the same host-streaming call
@@ -612,9 +841,14 @@ def run_ours(args):
         gc.collect()
 
     cpu = None
+    cpu_table = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         cpu = cpu_oracle_sample(2048, 256, args.seed)
         cpu.pop("seconds", None)
+        try:
+            cpu_table = cpu_baselines(args.seed)
+        except Exception as e:  # noqa
+            cpu_table = {"error": repr(e)[:200]}
 
     if rank == 0:
         line = {
@@ -633,11 +867,14 @@ def run_ours(args):
                                                              "a functional run, not a scaling number]" if coloc else "")},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": ck,
-            "baselines": {"cusolver_potrf": cusolver},
+            "baselines": {"cusolver_potrf": cusolver, "cpu": cpu_table},
             "mxp_c3": mxp,
+            "kl_sweep": kl,
             "ooc": ooc,
             "sched": sched,
-            "check": {"backward_error_probe": probe, "logdet": logdet},
+            "check": {"backward_error_fro": backward_error, "backward_error_probe": probe, "logdet": logdet,
+                      "how": "||A - L L^T||_F / ||A||_F by block columns of cuBLAS DGEMM (bar 1e-13, north_star); "
+                             "probe = ||(A - L L^T) x|| / ||A x||, x: 4 seeded normal columns"},
             "fp64_engines": engines,
             "kernels": kstats,
         }

@@ -65,3 +65,14 @@ class Potrf:
     def close(self):
         self.L.cusolverDnDestroyParams(self.p)
         self.L.cusolverDnDestroy(self.h)
+
+
+def potrs(h_potrf: "Potrf", A_ptr: int, B_ptr: int, nrhs: int = 1) -> None:
+    """cusolverDnXpotrs on the factor left in A by Potrf (same uplo): B <- A^-1 B."""
+    L = h_potrf.L
+    L.cusolverDnXpotrs.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                                   ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
+                                   ctypes.c_int64, ctypes.c_void_p]
+    rc = L.cusolverDnXpotrs(h_potrf.h, h_potrf.p, h_potrf.uplo, h_potrf.n, nrhs, 1, ctypes.c_void_p(A_ptr),
+                            h_potrf.lda, 1, ctypes.c_void_p(B_ptr), h_potrf.n, ctypes.c_void_p(h_potrf.info.data_ptr()))
+    assert rc == 0, rc
