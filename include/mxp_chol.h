@@ -123,7 +123,9 @@ typedef enum mxp_attr {
  *   n             matrix order, n >= 1                              (arg 1)
  *   nb            tile size; nb % 128 == 0, 128 <= nb <= 2048        (arg 2)
  *   precision_map host array of Nt(Nt+1)/2 codes, copied; NULL = all FP64 (arg 3)
- *   ngpus         GPUs the plan spans; this build supports 1 per process (arg 4)
+ *   ngpus         GPUs the plan spans: 1 (one plan per GPU and process; several GPUs
+ *                 cooperate through MXP_ATTR_RANK / MXP_ATTR_NRANKS and the peer
+ *                 attach calls below); other values return -4        (arg 4)
  *   out           receives the plan handle                           (arg 5)
  * No device memory is allocated here; that happens on the first factor call
  * (or mxp_chol_set_workspace).
@@ -162,14 +164,43 @@ int mxp_chol_factor_device(mxp_plan_t plan, double* A_dev, int64_t lda, int64_t*
  * written back device->host (lower triangle only).  When the lower
  * triangle at its storage precisions exceeds the device pool
  * (MXP_ATTR_HBM_BYTES_CAP or HBM), tiles are cached and evicted out-of-core
- * (V1 accumulator retention, V2 reuse/eviction, V3 diagonal pinning;
- * P:235-238, Alg. 3).
+ * with a static plan computed ahead from the static schedule: a tile's
+ * slot is recycled once the tile is dead (after its last reader; with the
+ * compact pool, once the tile is final), every tile crosses the link once each
+ * way, and the accumulator of a task stays in its slot for the whole GEMM
+ * chain.  Re-fetching evicted live tiles (the paper's V2 regime, Alg. 3
+ * P:281-301) is not implemented: an HBM cap below the live set returns
+ * MXP_ENOMEM.
  *   A_host host pointer (pinned via mxp_host_alloc for full copy bandwidth;
  *          pageable memory is registered for the call), column-major, lda >= n;
  *          lower triangle overwritten by L as in mxp_chol_factor_device. (arg 2)
  *   lda, info as above.
  */
 int mxp_chol_factor(mxp_plan_t plan, double* A_host, int64_t lda, int64_t* info);
+
+/*
+ * mxp_chol_factor_tiles -- factorization of a matrix held as tile-packed HOST
+ * storage at each tile's precision (the only feasible input of
+ * C5: a dense lda matrix would be 2.2 TB).  P:42 "transmitting the minimum
+ * acceptable bytes per word": tiles below FP64 cross the host link as codes.
+ *   tiles   host array of Nt(Nt+1)/2 pointers in column-major lower-tile order;
+ *           tile t is nb x nb column-major at precision map[t]: FP64 doubles,
+ *           FP32 floats, FP16 binary16 codes, FP8 E4M3 codes (padding beyond n
+ *           ignored).  Diagonal tiles hold the full symmetric nb x nb block (only
+ *           its lower triangle is read).  Pinned memory (mxp_host_alloc) gives
+ *           full copy bandwidth.                                        (arg 2)
+ *   scales  host array of Nt(Nt+1)/2 doubles: value = code / scales[t] for
+ *           FP16/FP8 tiles (a power of two; 1 for FP64/FP32 tiles)     (arg 3)
+ *   info    as mxp_chol_factor                                         (arg 4)
+ * On return every tile holds L's tile at the same precision (codes), scales[t]
+ * its new scale; diagonal tiles hold L_kk with zeros above the diagonal.  The
+ * input is stored at its precision (O3) before use.  Host<->device traffic is
+ * one pass each way at storage precision (MXP_ATTR_H2D_BYTES / _D2H_BYTES).
+ * Tiles below FP64 need the compact pool (MXP_ATTR_COMPACT_USED = 1, i.e. the
+ * native engine in core); otherwise MXP_ENOTSUP.  An all-FP64 map works on
+ * every engine, in core or out of core.  Single rank.
+ */
+int mxp_chol_factor_tiles(mxp_plan_t plan, void* const* tiles, double* scales, int64_t* info);
 
 /*
  * mxp_chol_factor_matern -- factor the Matern nu = 0.5 covariance of n
@@ -251,6 +282,18 @@ int mxp_chol_loglik(mxp_plan_t plan, const double* y_dev, double* loglik);
 int mxp_precision_map_from_matrix_device(int64_t n, int64_t nb, const double* A_dev, int64_t lda,
                                          double eps, uint32_t allowed_mask, uint8_t* map_out,
                                          double* norms_out);
+
+/*
+ * mxp_precision_map_from_matrix -- the same planner (G6) for a HOST matrix
+ * (SURVEY 8(b)): A is streamed to the device one tile column panel at a time
+ * (rows j*nb..n-1 of columns j*nb..j*nb+nb-1; one panel of n x nb doubles of
+ * device memory) and the tile norms are reduced there.  Arguments and errors as
+ * mxp_precision_map_from_matrix_device, with A a host pointer (pageable or
+ * pinned, lower triangle and the diagonal tiles read).  Synchronous; uses the
+ * current device and a private stream.
+ */
+int mxp_precision_map_from_matrix(int64_t n, int64_t nb, const double* A, int64_t lda, double eps,
+                                  uint32_t allowed_mask, uint8_t* map_out, double* norms_out);
 
 /*
  * Synthetic input generators, bit-identical to the host

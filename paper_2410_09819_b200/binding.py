@@ -23,8 +23,8 @@ ATTR = {
 # every symbol include/mxp_chol.h declares (tests check the library exports them)
 EXPORTS = [
     "mxp_chol_plan", "mxp_chol_plan_set", "mxp_chol_plan_get", "mxp_chol_workspace_size",
-    "mxp_chol_set_workspace", "mxp_chol_factor_device", "mxp_chol_factor", "mxp_chol_logdet",
-    "mxp_precision_map_from_matrix_device", "mxp_generate_plgsy_device", "mxp_generate_kms_device",
+    "mxp_chol_set_workspace", "mxp_chol_factor_device", "mxp_chol_factor", "mxp_chol_factor_tiles", "mxp_chol_logdet",
+    "mxp_precision_map_from_matrix_device", "mxp_precision_map_from_matrix", "mxp_generate_plgsy_device", "mxp_generate_kms_device",
     "mxp_generate_matern_device", "mxp_chol_factor_matern", "mxp_precision_map_matern_device",
     "mxp_chol_get_factor_device", "mxp_chol_tile_device_ptr", "mxp_chol_ipc_handle", "mxp_chol_ipc_attach",
     "mxp_chol_attach_peer_plan", "mxp_chol_describe", "mxp_chol_solve_lower", "mxp_chol_loglik",
@@ -66,9 +66,11 @@ def lib():
         L.mxp_chol_set_workspace.argtypes = [vp, vp, ctypes.c_size_t]
         L.mxp_chol_factor_device.argtypes = [vp, vp, i64, pi64]
         L.mxp_chol_factor.argtypes = [vp, vp, i64, pi64]
+        L.mxp_chol_factor_tiles.argtypes = [vp, vp, vp, pi64]
         L.mxp_chol_logdet.argtypes = [vp, pd]
         L.mxp_precision_map_from_matrix_device.argtypes = [i64, i64, vp, i64, ctypes.c_double,
                                                             ctypes.c_uint32, vp, vp]
+        L.mxp_precision_map_from_matrix.argtypes = [i64, i64, vp, i64, ctypes.c_double, ctypes.c_uint32, vp, vp]
         L.mxp_generate_plgsy_device.argtypes = [i64, u64, vp, i64, vp]
         L.mxp_generate_kms_device.argtypes = [i64, ctypes.c_double, vp, i64, vp]
         L.mxp_generate_matern_device.argtypes = [i64, vp, ctypes.c_double, ctypes.c_double, ctypes.c_double,
@@ -211,6 +213,24 @@ class Plan:
         _check("mxp_chol_factor", lib().mxp_chol_factor(self._h, ptr, lda, ctypes.byref(info)))
         return info.value
 
+    def factor_tiles(self, tiles, scales, stream_from_torch: bool = True) -> int:
+        """Tile-packed host storage at storage precision (mxp_chol_factor_tiles): `tiles` is a
+        list of Nt(Nt+1)/2 C-contiguous host buffers (numpy arrays or CPU tensors) in column-major
+        lower-tile order, each the nb x nb column-major tile at its precision (float64, float32,
+        float16 codes, uint8 E4M3 codes); `scales` a float64 array (value = code / scale).
+        Both are overwritten with L.  Returns info."""
+        import numpy as np
+        ptrs = (ctypes.c_void_p * len(tiles))()
+        for t, x in enumerate(tiles):
+            ptrs[t] = x.ctypes.data if hasattr(x, "ctypes") else x.data_ptr()
+        assert isinstance(scales, np.ndarray) and scales.dtype == np.float64 and scales.flags.c_contiguous
+        if stream_from_torch:
+            self._stream_from_torch()
+        info = ctypes.c_int64()
+        _check("mxp_chol_factor_tiles", lib().mxp_chol_factor_tiles(self._h, ptrs, scales.ctypes.data,
+                                                                    ctypes.byref(info)))
+        return info.value
+
     def factor_matern(self, xy, sigma2: float = 1.0, range_a: float = 0.02627, nugget: float = 0.0,
                       stream_from_torch: bool = True) -> int:
         """Factor the Matern covariance of locations xy (n x 2), generated tile by
@@ -332,6 +352,21 @@ class Plan:
         yp = self._dev_vec(y, self.n) if y is not None else None
         _check("mxp_chol_loglik", lib().mxp_chol_loglik(self._h, yp, ctypes.byref(v)))
         return v.value
+
+
+def precision_map_from_matrix(A, nb: int, eps: float, allowed: int = 0xF):
+    """Planner on a HOST matrix (numpy array or CPU tensor; streamed to the device one
+    tile column at a time) -> (uint8 map, float64 tile norms)."""
+    import numpy as np
+    Af = np.asfortranarray(np.asarray(A, dtype=np.float64))
+    n = Af.shape[0]
+    Nt = -(-n // nb)
+    m = np.empty(Nt * (Nt + 1) // 2, np.uint8)
+    f = np.empty(Nt * (Nt + 1) // 2, np.float64)
+    _check("mxp_precision_map_from_matrix",
+           lib().mxp_precision_map_from_matrix(n, nb, Af.ctypes.data, n, float(eps), allowed,
+                                               m.ctypes.data, f.ctypes.data))
+    return m, f
 
 
 def precision_map_from_matrix_device(A, nb: int, eps: float, allowed: int = 0xF):

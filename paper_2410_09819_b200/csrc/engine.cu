@@ -115,6 +115,8 @@ struct mxp_plan_s {
     int64_t compact_slots = 0;
     std::vector<long long> sto;     // [T] byte offsets of the storage images in the shadow arena, -1 = none
     long long* d_sto = nullptr;
+    void* const* tiles_io = nullptr;  // mxp_chol_factor_tiles: host tiles at storage precision (this call)
+    double* d_in_scale = nullptr;     // [T] scales of those input tiles
     std::vector<long long> oz_img;  // [T] byte offsets of the int8 slice images, -1 = none
     long long* d_oz_img = nullptr;
     double* d_solve = nullptr;      // forward-solve work vectors (r | z | scalars)
@@ -573,7 +575,7 @@ bool plan_slots(mxp_plan_s* p, int64_t C) {
 
 struct Layout {
     size_t slot, prev, epoch, flags, flags_bytes, expected, items, wbuf, stats, prec, amax_x, amax_s, iscale, args,
-        qtile, img, ozimg, sto, solve, shadow, pool, total;
+        qtile, img, ozimg, sto, in_scale, solve, shadow, pool, total;
 };
 
 Layout layout(const mxp_plan_s* p) {
@@ -615,6 +617,8 @@ Layout layout(const mxp_plan_s* p) {
     off += align_up(sizeof(long long) * (size_t)p->T, 256);
     L.sto = off;
     off += align_up(sizeof(long long) * (size_t)p->T, 256);
+    L.in_scale = off;
+    off += align_up(sizeof(double) * (size_t)p->T, 256);
     L.solve = off;  // forward solve: r, z (Nt*nb each) + scalars
     off += align_up(sizeof(double) * (2 * (size_t)p->Nt * p->nb + 8), 256);
     L.shadow = off;
@@ -678,6 +682,7 @@ void bind_workspace(mxp_plan_s* p) {
     p->d_img = (long long*)(p->ws + L.img);
     p->d_oz_img = (long long*)(p->ws + L.ozimg);
     p->d_sto = (long long*)(p->ws + L.sto);
+    p->d_in_scale = (double*)(p->ws + L.in_scale);
     p->d_solve = (double*)(p->ws + L.solve);
     p->d_shadow = (uint8_t*)(p->ws + L.shadow);
     p->d_amax_x = (unsigned long long*)(p->ws + L.flags + align_up(sizeof(int) * flag_ints(p), 8));
@@ -1030,6 +1035,8 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     a.src_lda = lda;
     a.compact = p->compact ? 1 : 0;
     a.sto = p->compact ? p->d_sto : nullptr;
+    a.tile_codes = p->tiles_io ? 1 : 0;  // input tiles arrive as codes in their storage images
+    a.in_scale = p->d_in_scale;
     a.n = p->n;
     a.gen_mode = gen ? 1 : 0;
     a.prev_owner = p->d_prev;
@@ -1200,7 +1207,13 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
                                  CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
                         throw CudaError{cudaErrorUnknown};
                     const double* src = p->pool + (size_t)p->slot_plan[t] * nb * nb;
-                    if (m != k) {
+                    if (p->tiles_io) {  // tile-packed host storage: the tile at its storage precision
+                        const int pt = p->map[t];
+                        const size_t bytes = (size_t)nb * nb * (pt == MXP_FP64 ? 8 : pt == MXP_FP32 ? 4 : pt == MXP_FP16 ? 2 : 1);
+                        const void* s2 = pt == MXP_FP64 ? (const void*)src : (const void*)(p->d_shadow + p->sto[t]);
+                        CK(cudaMemcpyAsync(p->tiles_io[t], s2, bytes, cudaMemcpyDeviceToHost, p->sD2H));
+                        d2h_bytes += (int64_t)bytes;
+                    } else if (m != k) {
                         CK(cudaMemcpy2DAsync(A_host + (size_t)k * nb * lda + (size_t)m * nb, sizeof(double) * lda, src,
                                              sizeof(double) * nb, sizeof(double) * rr, cr, cudaMemcpyDeviceToHost, p->sD2H));
                         d2h_bytes += (int64_t)(sizeof(double) * rr * cr);
@@ -1220,8 +1233,19 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
                 const int64_t t = tile_index(Nt, m, k);
                 const int64_t rr = std::min(nb, n - m * nb), cr = std::min(nb, n - k * nb);
                 double* dst = p->pool + (size_t)p->slot_plan[t] * nb * nb;
-                const double* src = A_host + (size_t)k * nb * lda + (size_t)m * nb;
+                const double* src = A_host ? A_host + (size_t)k * nb * lda + (size_t)m * nb : nullptr;
                 const int32_t prev = p->prev_owner[t];
+                const bool coded = p->tiles_io && p->map[t] != MXP_FP64;
+                if (coded) {  // codes into the tile's storage image; the PREP task waits for the slot
+                    const int pt = p->map[t];
+                    const size_t bytes = (size_t)nb * nb * (pt == MXP_FP32 ? 4 : pt == MXP_FP16 ? 2 : 1);
+                    CK(cudaMemcpyAsync(p->d_shadow + p->sto[t], p->tiles_io[t], bytes, cudaMemcpyHostToDevice, p->sH2D));
+                    if (g_write32((CUstream)p->sH2D, (CUdeviceptr)(a.loaded + t), 1, CU_STREAM_WRITE_VALUE_DEFAULT) !=
+                        CUDA_SUCCESS)
+                        throw CudaError{cudaErrorUnknown};
+                    p->h2d += (int64_t)bytes;
+                    continue;
+                }
                 if (prev >= 0) {  // out of core / compact: the slot's previous tile must be dead and written back
                     int64_t pm = 0, pc = 0;
                     tile_coords(Nt, prev, pm, pc);
@@ -1237,11 +1261,16 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
                             CUDA_SUCCESS)
                         throw CudaError{cudaErrorUnknown};
                 }
-                CK(cudaMemcpy2DAsync(dst, sizeof(double) * nb, src, sizeof(double) * lda, sizeof(double) * rr, cr,
-                                     cudaMemcpyHostToDevice, p->sH2D));
+                if (p->tiles_io) {  // an FP64 tile: nb x nb doubles straight into its slot
+                    CK(cudaMemcpyAsync(dst, p->tiles_io[t], sizeof(double) * nb * nb, cudaMemcpyHostToDevice, p->sH2D));
+                    p->h2d += (int64_t)(sizeof(double) * nb * nb);
+                } else {
+                    CK(cudaMemcpy2DAsync(dst, sizeof(double) * nb, src, sizeof(double) * lda, sizeof(double) * rr, cr,
+                                         cudaMemcpyHostToDevice, p->sH2D));
+                    p->h2d += (int64_t)(sizeof(double) * rr * cr);
+                }
                 if (g_write32((CUstream)p->sH2D, (CUdeviceptr)(a.loaded + t), 1, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
                     throw CudaError{cudaErrorUnknown};
-                p->h2d += (int64_t)(sizeof(double) * rr * cr);
             }
         join_all();
         p->d2h += d2h_bytes;
@@ -1763,6 +1792,91 @@ int mxp_chol_factor(mxp_plan_t p, double* A_host, int64_t lda, int64_t* info) {
     return MXP_OK;
 }
 
+int mxp_chol_factor_tiles(mxp_plan_t p, void* const* tiles, double* scales, int64_t* info) {
+    if (!p) return -1;
+    if (!tiles) return -2;
+    if (!scales) return -3;
+    if (!info) return -4;
+    // tile-packed host storage (the C5 input): tiles below FP64 travel as their codes,
+    // which needs the compact pool (native engine); an all-FP64 map works on every engine
+    if (p->nranks > 1) {
+        g_last_error = "factor_tiles: single rank";
+        return MXP_ENOTSUP;
+    }
+    for (int64_t t = 0; t < p->T; ++t)
+        if (!tiles[t]) return -2;
+    p->have_result = false;
+    p->launches = p->h2d = p->d2h = 0;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    try {
+        CK(cudaSetDevice(p->device));
+        if (!stream_memops()) {
+            g_last_error = "cuStreamWriteValue32/cuStreamWaitValue32 unavailable";
+            cudaSetDevice(cur);
+            return MXP_ENOTSUP;
+        }
+        ensure_streams(p);
+        bind_workspace(p);
+        if (p->mxp && !p->compact) {
+            g_last_error = "factor_tiles with tiles below FP64 needs the compact pool (MXP_ATTR_TC_ENGINE 3, "
+                           "MXP_ATTR_FP64_ENGINE 1, in core, MXP_ATTR_COMPACT_POOL 1)";
+            cudaSetDevice(cur);
+            return MXP_ENOTSUP;
+        }
+        cudaStream_t s0 = entry_stream(p);
+        const int64_t C = pool_slots(p);
+        if (!plan_slots(p, C)) {
+            g_last_error = "HBM cap below the out-of-core working set (live tiles of two columns)";
+            cudaSetDevice(cur);
+            return MXP_ENOMEM;
+        }
+        p->slots = C;
+        CK(cudaMemcpyAsync(p->d_slot, p->slot_plan.data(), sizeof(int32_t) * p->T, cudaMemcpyHostToDevice, s0));
+        CK(cudaMemcpyAsync(p->d_prev, p->prev_owner.data(), sizeof(int32_t) * p->T, cudaMemcpyHostToDevice, s0));
+        CK(cudaMemcpyAsync(p->d_in_scale, scales, sizeof(double) * p->T, cudaMemcpyHostToDevice, s0));
+        CK(cudaMemsetAsync(p->d_info, 0, sizeof(int64_t), s0));
+        prof_reset(p);
+        p->tiles_io = tiles;
+        try {
+            factor_incore_f64(p, s0, true, nullptr, p->n);
+        } catch (...) {
+            p->tiles_io = nullptr;
+            throw;
+        }
+        p->tiles_io = nullptr;
+        CK(cudaStreamSynchronize(p->sU));
+        int64_t hinfo = 0;
+        int herr = 0;
+        CK(cudaMemcpy(&hinfo, p->d_info, sizeof(int64_t), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&herr, p->d_flags + 1, sizeof(int), cudaMemcpyDeviceToHost));
+        CK(cudaStreamSynchronize(p->sD2H));
+        CK(cudaStreamSynchronize(p->sH2D));
+        if (herr) {
+            g_last_error = "static schedule: a Ready-table wait timed out (scheduler error)" + sched_timeout_detail(p);
+            throw CudaError{cudaErrorLaunchTimeout};
+        }
+        // output scales: the storage scale of every tile below FP64 (code = value * scale), 1 otherwise
+        std::vector<double> sc(3 * (size_t)p->T, 1.0);
+        if (p->mxp) CK(cudaMemcpy(sc.data(), p->d_iscale, sizeof(double) * 3 * p->T, cudaMemcpyDeviceToHost));
+        for (int64_t t = 0; t < p->T; ++t) scales[t] = p->map[t] == MXP_FP64 ? 1.0 : sc[3 * t + 2];
+        double ld = 0.0;
+        launch_logdet_final(p->d_logdet_parts, p->Nt, p->d_logdet, s0);
+        p->launches += 1;
+        CK(cudaMemcpyAsync(&ld, p->d_logdet, sizeof(double), cudaMemcpyDeviceToHost, s0));
+        CK(cudaStreamSynchronize(s0));
+        prof_collect(p);
+        *info = hinfo;
+        p->have_result = (hinfo == 0);
+        p->logdet = ld;
+    } catch (const CudaError& e) {
+        cudaSetDevice(cur);
+        return status_from_exception(e);
+    }
+    cudaSetDevice(cur);
+    return MXP_OK;
+}
+
 int mxp_chol_logdet(mxp_plan_t p, double* logdet) {
     if (!p) return -1;
     if (!logdet) return -2;
@@ -1830,6 +1944,46 @@ int mxp_precision_map_from_matrix_device(int64_t n, int64_t nb, const double* A,
         CK(cudaFree(dn));
     } catch (const CudaError& e) {
         if (dn) cudaFree(dn);
+        return status_from_exception(e);
+    }
+    return plan_from_norms(Nt, f, eps, allowed, map_out, norms_out);
+}
+
+int mxp_precision_map_from_matrix(int64_t n, int64_t nb, const double* A, int64_t lda, double eps,
+                                  uint32_t allowed, uint8_t* map_out, double* norms_out) {
+    if (n < 1) return -1;
+    if (nb < 1) return -2;
+    if (!A) return -3;
+    if (lda < n) return -4;
+    if (!(eps > 0.0 && eps < 1.0)) return -5;
+    if (!(allowed & 1u) || (allowed & ~0xFu)) return -6;
+    if (!map_out) return -7;
+    const int64_t Nt = (n + nb - 1) / nb, T = Nt * (Nt + 1) / 2;
+    double *dn = nullptr, *dp = nullptr;
+    std::vector<double> f(T);
+    cudaStream_t s = nullptr;
+    try {
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        CK(cudaMalloc(&dn, sizeof(double) * T));
+        // one tile column at a time: H2D of rows [j nb, n) x columns [j nb, j nb + nb) (the lower
+        // triangle and the diagonal tile's upper part, which the norm mirrors), then its norms
+        CK(cudaMalloc(&dp, sizeof(double) * (size_t)n * (size_t)nb));
+        for (int64_t j = 0; j < Nt; ++j) {
+            const int64_t r0 = j * nb, rows = n - r0, cols = std::min(nb, n - r0);
+            CK(cudaMemcpy2DAsync(dp, sizeof(double) * rows, A + r0 + r0 * lda, sizeof(double) * lda,
+                                 sizeof(double) * rows, cols, cudaMemcpyHostToDevice, s));
+            launch_panel_norms(dp, rows, n, nb, j, dn, s);
+            CK(cudaGetLastError());
+        }
+        CK(cudaMemcpyAsync(f.data(), dn, sizeof(double) * T, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        CK(cudaFree(dn));
+        CK(cudaFree(dp));
+        CK(cudaStreamDestroy(s));
+    } catch (const CudaError& e) {
+        if (dn) cudaFree(dn);
+        if (dp) cudaFree(dp);
+        if (s) cudaStreamDestroy(s);
         return status_from_exception(e);
     }
     return plan_from_norms(Nt, f, eps, allowed, map_out, norms_out);

@@ -105,6 +105,8 @@ struct SchedArgs {
     const long long* sto;      // [T] offsets of the storage images in `shadow` (-1: FP64 tile)
     const double* src_A;       // compact device path: the caller's matrix (PREP copies tiles from it)
     int64_t src_lda;
+    int tile_codes;            // mxp_chol_factor_tiles: input tiles below FP64 arrive as codes in their
+    const double* in_scale;    //   storage images (value = code / in_scale[t]); PREP decodes them
     int* sm_claim;             // [256] k_sched CTAs per SM in the Ozaki mode (extras leave at once,
                                //       keeping room for the k_tc CTA of every SM)
     unsigned long long* stats; // optional diagnostics (MXP_ATTR_PROFILE): see STAT_*
@@ -165,6 +167,9 @@ void launch_logdet_final(const double* parts, int64_t Nt, double* out, cudaStrea
 void launch_matern_tile_norms(const double* xy, int64_t n, int64_t nb, double sigma2, double range_a,
                               double nugget, double* norms, cudaStream_t s);
 // planner: per-tile Frobenius norms (fp64) of the lower tiles of an lda matrix
+// planner on a host matrix: norms of tile column j from its device panel copy (ld = ldp)
+void launch_panel_norms(const double* P, int64_t ldp, int64_t n, int64_t nb, int64_t j, double* norms,
+                        cudaStream_t s);
 void launch_tile_norms(const double* A, int64_t lda, int64_t n, int64_t nb, double* norms,
                        cudaStream_t s);
 

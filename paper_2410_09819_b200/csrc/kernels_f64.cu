@@ -106,6 +106,35 @@ void launch_tile_norms(const double* A, int64_t lda, int64_t n, int64_t nb, doub
     k_tile_norms<<<grid, 256, 0, s>>>(A, lda, n, nb, Nt, norms);
 }
 
+// Tile norms of one tile column j from a device copy of the host matrix's panel
+// (rows j*nb .. n-1, columns j*nb .. j*nb+nb-1, column-major with ld = ldp): the
+// host planner streams A column panel by column panel (a2 with A in host memory).
+__global__ void k_panel_norms(const double* __restrict__ P, int64_t ldp, int64_t n, int64_t nb, int64_t Nt,
+                              int64_t j, double* norms) {
+    __shared__ double red[256];
+    const int64_t i = j + blockIdx.x;
+    if (i >= Nt) return;
+    const int64_t r0 = j * nb;  // global row of the panel's first row
+    double s = 0.0;
+    for (int64_t c = j * nb; c < (j + 1) * nb && c < n; ++c)
+        for (int64_t r = i * nb + threadIdx.x; r < (i + 1) * nb && r < n; r += blockDim.x) {
+            double v = (r >= c) ? P[(r - r0) + (c - r0) * ldp] : P[(c - r0) + (r - r0) * ldp];
+            s += v * v;
+        }
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) norms[tile_index(Nt, i, j)] = sqrt(red[0]);
+}
+void launch_panel_norms(const double* P, int64_t ldp, int64_t n, int64_t nb, int64_t j, double* norms,
+                        cudaStream_t s) {
+    const int64_t Nt = (n + nb - 1) / nb;
+    MXP_CARVEOUT_MAX(k_panel_norms);
+    k_panel_norms<<<(unsigned)(Nt - j), 256, 0, s>>>(P, ldp, n, nb, Nt, j, norms);
+}
 
 // Load every kernel of this file now (CUDA lazy loading would otherwise load a
 // kernel at its first launch, which can wait for running kernels -- with ranks
@@ -116,6 +145,7 @@ void preload_layout() {
     cudaFuncGetAttributes(&fa, (const void*)k_unpack);
     cudaFuncGetAttributes(&fa, (const void*)k_logdet_final);
     cudaFuncGetAttributes(&fa, (const void*)k_tile_norms);
+    cudaFuncGetAttributes(&fa, (const void*)k_panel_norms);
     cudaGetLastError();
 }
 

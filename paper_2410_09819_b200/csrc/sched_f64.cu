@@ -769,12 +769,22 @@ __device__ __noinline__ bool task_prep(const SchedArgs& a, int64_t m, int64_t k,
             }
         } else {
             ok = wait_flag(a.loaded + t, 1, a, k);
+            const int32_t prev = a.prev_owner[t];
+            if (ok && a.tile_codes && a.sto && a.sto[t] >= 0 && prev >= 0)  // codes staged aside: the slot must be free
+                ok = wait_flag(a.ready + prev, a.epoch, a, k);
         }
         *s_flag = ok;
     }
     sync_workers();
     if (!*s_flag) return false;
     double* T = tile_ptr(a.pool, a.slot, Nt, nb, m, k);
+    if (a.tile_codes && a.sto && a.sto[t] >= 0) {  // factor_tiles: decode the input codes into the fp64 slot
+        const int pc = a.prec[t];
+        const uint8_t* cp = a.shadow + a.sto[t];
+        const double inv = 1.0 / __ldcg(a.in_scale + t);
+        for (int64_t e = threadIdx.x; e < nb * nb; e += CC::NT) __stcg(T + e, decode_code(pc, cp, e, inv));
+        sync_workers();
+    }
     const int64_t rr = n - m * nb, cr = n - k * nb;  // real rows / columns of this tile
     if (a.gen_mode) {  // N2: generate the tile in place (fused generation, no input copy)
         for (int64_t e = threadIdx.x; e < nb * nb; e += CC::NT) {
@@ -802,7 +812,10 @@ __device__ __noinline__ bool task_prep(const SchedArgs& a, int64_t m, int64_t k,
         sync_workers();
     }
     const int p = a.prec ? a.prec[t] : P_FP64;
-    if (p != P_FP64) {
+    // (factor_tiles: a tile given as codes already IS the stored input -- re-quantizing it with a
+    // scale recomputed from its amax would not be the identity when that amax rounded up into
+    // the next binade, the up-cast reading of O4.2.3)
+    if (p != P_FP64 && !(a.tile_codes && a.sto && a.sto[t] >= 0)) {
         double v = 0.0;
         for (int64_t e = threadIdx.x; e < nb * nb; e += CC::NT) v = fmax(v, fabs(__ldcg(T + e)));
         for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));

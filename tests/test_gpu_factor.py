@@ -153,6 +153,30 @@ def test_planner_device_matches_oracle():
         assert np.mean(mp == mo) >= 0.999
 
 
+@pytest.mark.parametrize("n,nb", [(2048, 128), (1900, 256), (3000, 1024)])
+def test_planner_host_matches_device_and_oracle(n, nb):
+    """mxp_precision_map_from_matrix (host A streamed by tile-column panels) gives the device
+    planner's norms bit for bit (same kernel arithmetic) and the oracle's within rounding."""
+    import torch
+
+    import paper_2410_09819_b200 as m
+    xy = w.matern_locations(n, seed=1)
+    S = w.matern_cov(xy, 1.0, 0.02627)
+    M = np.tril(S) + np.triu(np.full((n, n), 5.0), 1)  # the strict upper triangle is not read ...
+    Nt = -(-n // nb)
+    for i in range(Nt):  # ... except inside diagonal tiles (mirrored there): keep it symmetric
+        r = slice(i * nb, min(n, (i + 1) * nb))
+        M[r, r] = S[r, r]
+    Sd = torch.tensor(S, device="cuda").T
+    for eps in (1e-5, 1e-8):
+        mh, fh = m.precision_map_from_matrix(M, nb, eps)
+        md, fd = m.precision_map_from_matrix_device(Sd, nb, eps)
+        assert np.array_equal(fh, fd) and np.array_equal(mh, md)
+        fo = oracle.tile_norms(S, nb)
+        assert np.max(np.abs(fh - fo) / np.maximum(fo, 1e-300)) <= 1e-12  # (nb^2-term sums, other order)
+        assert np.mean(mh == oracle.plan(S, nb, eps)) >= 0.999
+
+
 @pytest.mark.parametrize("n,nb", [(1000, 256), (2048, 512), (1300, 128)])
 def test_host_streaming_path_against_oracle(n, nb):
     """mxp_chol_factor: tiles stream H2D/D2H around the static schedule."""
