@@ -354,7 +354,8 @@ def run_c3(args, m, dev, dev_index, stream, ws, new_plan, allreduce, barrier, dg
         r = {"t": min(ts[1:] if len(ts) > 1 else ts), "logdet": pl.logdet(),
              "ws_gb": pl.workspace_size() / 1e9, "img_gb": pl.get("image_bytes") / 1e9,
              "fp64_engine": "ozaki" if pl.get("fp64_engine_used") == 1 else "dmma",
-             "tc_engine": pl.get("tc_engine_used"), "compact": pl.get("compact_used")}
+             "tc_engine": pl.get("tc_engine_used"), "compact": pl.get("compact_used"),
+             "slots": pl.get("pool_slots")}
         if ws == 1:
             torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True)
@@ -410,7 +411,8 @@ def run_c3(args, m, dev, dev_index, stream, ws, new_plan, allreduce, barrier, dg
              "speedup_vs_best_fp64": tfl / best_fp64,
              "engines": {"fp64": r["fp64_engine"], "below_fp64": {3: "native (kind::f16/f8f6f4)", 1: "tf32 images",
                                                                   2: "tf32 registers", 0: "dmma"}.get(r["tc_engine"])},
-             "compact_pool": bool(r["compact"]), "workspace_gb": round(r["ws_gb"], 2),
+             "compact_pool": bool(r["compact"]), "fp64_pool_slots": r["slots"], "tiles": Nt * (Nt + 1) // 2,
+             "workspace_gb": round(r["ws_gb"], 2),
              "image_gb": round(r["img_gb"], 2),
              "tile_fractions_fp64_fp32_fp16_fp8": [round(float(np.mean(pmap == c)), 4) for c in range(4)],
              "flop_fractions": {k: round(v / flops_m, 4) for k, v in F.items()},
