@@ -72,7 +72,7 @@ def parse():
     ap.add_argument("--ooc-frac", type=float, default=0.65)
     ap.add_argument("--fp64-engine", default="ozaki", choices=["dmma", "ozaki"],
                     help="GEMM/SYRK engine of FP64 tiles: FP64 tensor pipe (DMMA) or Ozaki-I on int8 tcgen05")
-    ap.add_argument("--oz-slices", type=int, default=8)
+    ap.add_argument("--oz-slices", type=int, default=7)
     ap.add_argument("--no-engine-compare", action="store_true")
     return ap.parse_args()
 
@@ -387,14 +387,15 @@ def run_c3(args, m, dev, dev_index, stream, ws, new_plan, allreduce, barrier, dg
             out["fp64"]["loglik_y_rel_err_vs_cusolver"] = abs(r64["loglik_y"] - cus["loglik_y"]) / abs(cus["loglik_y"])
     best_fp64 = max(out["fp64"]["tflops"], (cus or {}).get("tflops") or 0.0)
     # measured sustained peaks for the per-precision roofline: FP64 GEMM/SYRK on
-    # the int8 pipe (36 products) or DMMA; FP32 = 3 fp16 products (h h + h l + l h); FP16 = bf16
+    # the int8 pipe (s(s+1)/2 products) or DMMA; FP32 = 3 fp16 products (h h + h l + l h); FP16 = bf16
     # dense; FP8 = 2x; TRSM / POTRF on DMMA (live DGEMM)
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             bf16 = json.load(f)["bf16_tflops_sustained"]
     except Exception:
         bf16 = 2250.0 * 0.6
-    peaks = {"fp64_gemm": 2 * bf16 / 36, "fp32": bf16 / 3, "fp16": bf16, "fp8": 2 * bf16, "trsm": dgemm_peak,
+    npairs = args.oz_slices * (args.oz_slices + 1) // 2
+    peaks = {"fp64_gemm": 2 * bf16 / npairs, "fp32": bf16 / 3, "fp16": bf16, "fp8": 2 * bf16, "trsm": dgemm_peak,
              "potrf": dgemm_peak}
     g16 = {}
     for eps in args.mxp_eps:
@@ -417,8 +418,8 @@ def run_c3(args, m, dev, dev_index, stream, ws, new_plan, allreduce, barrier, dg
              "tile_fractions_fp64_fp32_fp16_fp8": [round(float(np.mean(pmap == c)), 4) for c in range(4)],
              "flop_fractions": {k: round(v / flops_m, 4) for k, v in F.items()},
              "roofline": {"roof_tflops": roof, "frac": tfl / roof,
-                          "how": "roof = (n^3/3) / sum_p F_p/peak_p; peaks: FP64 GEMM = 2 x bf16 sustained / 36 "
-                                 "(Ozaki) or live DGEMM, FP32 = bf16/3, FP16 = bf16, FP8 = 2 x bf16, TRSM/POTRF = DGEMM"},
+                          "how": "roof = (n^3/3) / sum_p F_p/peak_p; peaks: FP64 GEMM = 2 x bf16 sustained / "
+                                 f"{npairs} (Ozaki, s={args.oz_slices}) or live DGEMM, FP32 = bf16/3, FP16 = bf16, FP8 = 2 x bf16, TRSM/POTRF = DGEMM"},
              "loglik_y0_rel_err": abs(llm - ll64) / abs(ll64), "logdet_abs_diff": abs(r["logdet"] - r64["logdet"]),
              "kl_eq3": ll64 - llm}
         if r.get("loglik_y") is not None and r64.get("loglik_y") is not None:

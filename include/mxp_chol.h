@@ -91,14 +91,20 @@ typedef enum mxp_attr {
                                      0 (default) = FP64 tensor pipe (DMMA, mma.sync.m8n8k4.f64);
                                      1 = Ozaki scheme I on the int8 tensor cores (tcgen05 kind::i8): every
                                        off-diagonal tile is split once, exactly, into s int8 slices with a
-                                       power-of-two scale per row (7s - 1 bits), the s(s+1)/2 slice products
-                                       of weight >= 2^-7(s-1) are accumulated exactly in int32 TMEM, and the
+                                       power-of-two scale per row (8s - 2 bits + sign, balanced base-256
+                                       digits), the s(s+1)/2 slice products of weight >= 2^-8(s-1) are
+                                       accumulated exactly in int32 TMEM, and the
                                        levels are combined in fp64 after every tile of K (fp64 accumulation
-                                       across tiles).  In core, single rank; otherwise (or if the s bytes per
-                                       element of slice images do not fit in HBM) it behaves as 0 -- see
-                                       MXP_ATTR_FP64_ENGINE_USED.  Re-sizes the workspace. */
-    MXP_ATTR_OZ_SLICES = 13,      /* s for MXP_ATTR_FP64_ENGINE = 1, 4..8 (default 8: 55 bits per operand,
-                                     dropped products <= 2^-56 of the row maxima) */
+                                       across tiles).  Single rank.  In core the pool keeps every fp64 tile
+                                       beside the slice images.  Out of core (FP64 map, HBM cap below the
+                                       lower triangle; mxp_chol_factor / _factor_tiles / _factor_matern) an
+                                       fp64 tile lives in a ring slot only while it is computed and a final
+                                       off-diagonal tile lives on as its slice image (s bytes per element) in
+                                       an arena whose slots are recycled when the tile's row dies; ring +
+                                       arena must fit under the cap (MXP_ATTR_OZ_IMAGE_SLOTS).  Otherwise it
+                                       behaves as 0 -- see MXP_ATTR_FP64_ENGINE_USED.  Re-sizes the workspace. */
+    MXP_ATTR_OZ_SLICES = 13,      /* s for MXP_ATTR_FP64_ENGINE = 1, 4..8 (default 7: 54 bits per operand,
+                                     28 int8 products; dropped products <= 6 * 2^-52 of the row maxima) */
     MXP_ATTR_COMPACT_POOL = 14,   /* with the native engine (MXP_ATTR_TC_ENGINE_USED = 3): 1 (default) = store every
                                      tile below FP64 at its precision (codes + a power-of-two scale: 4/2/1 bytes per
                                      element, "minimum acceptable bytes per word"); its fp64 accumulator slot
@@ -114,7 +120,9 @@ typedef enum mxp_attr {
     MXP_ATTR_FP64_ENGINE_USED = 106, /* (get only) FP64 engine the next factorization uses (0 DMMA, 1 Ozaki) */
     MXP_ATTR_TC_ENGINE_USED = 107, /* (get only) engine of the tiles below FP64 the next factorization uses
                                      (-1: all-FP64 map; else as MXP_ATTR_TC_ENGINE) */
-    MXP_ATTR_COMPACT_USED = 108   /* (get only) 1 if the next factorization uses the compact pool */
+    MXP_ATTR_COMPACT_USED = 108,  /* (get only) 1 if the next factorization uses the compact pool */
+    MXP_ATTR_OZ_IMAGE_SLOTS = 109 /* (get only) slice-image slots of the out-of-core Ozaki mode (the peak live
+                                     set of final off-diagonal tiles, ~Nt^2/4); 0 when that mode is off */
 } mxp_attr_t;
 
 /*

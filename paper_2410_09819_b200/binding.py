@@ -17,7 +17,7 @@ ATTR = {
     "debug_sync": 5, "profile": 6, "tc_engine": 7, "rank": 8, "nranks": 9, "sm_first": 10,
     "sm_count": 11, "fp64_engine": 12, "oz_slices": 13, "gpu_launches": 100, "h2d_bytes": 101, "d2h_bytes": 102,
     "pool_slots": 103, "nt": 104, "image_bytes": 105, "fp64_engine_used": 106, "tc_engine_used": 107, "compact_pool": 14,
-    "compact_used": 108,
+    "compact_used": 108, "oz_image_slots": 109,
 }
 
 # every symbol include/mxp_chol.h declares (tests check the library exports them)

@@ -104,7 +104,7 @@ struct mxp_plan_s {
     uint8_t* d_shadow = nullptr;
     // FP64 engine (MXP_ATTR_FP64_ENGINE): 0 DMMA, 1 Ozaki int8 on tcgen05 (in core);
     // oz_on = the engine actually used by the current image plan
-    int fp64_engine = 0, oz_slices = 8;
+    int fp64_engine = 0, oz_slices = 7;
     bool oz_on = false;
     bool nat_on = false;            // tiles below FP64 on the native-width engine (tc_engine 3, k_tc)
     // compact pool (with the native engine): only FP64 tiles keep a permanent fp64 slot; a tile
@@ -119,6 +119,14 @@ struct mxp_plan_s {
     double* d_in_scale = nullptr;     // [T] scales of those input tiles
     std::vector<long long> oz_img;  // [T] byte offsets of the int8 slice images, -1 = none
     long long* d_oz_img = nullptr;
+    // Ozaki out of core (FP64 maps, one rank, HBM cap below the lower triangle): every tile keeps an
+    // fp64 slot only while it is computed (a ring recycled column by column, plan_compact(all)),
+    // and a final off-diagonal tile lives on as its slice image in an arena whose slots are
+    // recycled when the tile's row dies (plan_oz_ooc; DESIGN 5.4)
+    bool oz_ooc = false;
+    int64_t ring_slots = 0, oz_img_slots = 0;
+    std::vector<int32_t> ring_slot, ring_prev, img_prev;
+    int32_t* d_img_prev = nullptr;
     double* d_solve = nullptr;      // forward-solve work vectors (r | z | scalars)
     std::vector<int4> items2;       // GEMM list of k_tc (Ozaki mode)
     cudaStream_t sT = 0;
@@ -313,7 +321,7 @@ int64_t pool_slots(const mxp_plan_s* p);
 // deadlock) or a fresh one.  Tiles stored below FP64 (off the diagonal) free
 // their slot when they are final; FP64 tiles keep theirs.  prev[t] = the tile
 // whose death the preparation of t waits for.  Returns the slot count.
-int64_t plan_compact(const mxp_plan_s* p, std::vector<int32_t>& slot, std::vector<int32_t>& prev) {
+int64_t plan_compact(const mxp_plan_s* p, std::vector<int32_t>& slot, std::vector<int32_t>& prev, bool all = false) {
     const int64_t Nt = p->Nt, T = p->T;
     slot.assign(T, -1);
     prev.assign(T, -1);
@@ -335,7 +343,42 @@ int64_t plan_compact(const mxp_plan_s* p, std::vector<int32_t>& slot, std::vecto
             slot[t] = sl;
             prev[t] = owner[sl];
             owner[sl] = (int32_t)t;
-            if (m != j && p->map[t] != MXP_FP64) freed_at[j].push_back(sl);
+            // all (Ozaki out of core): every tile frees its slot -- off the diagonal once final
+            // (its readers use the slice image), on the diagonal once its column is final
+            if (all || (m != j && p->map[t] != MXP_FP64)) freed_at[j].push_back(sl);
+        }
+    }
+    return (int64_t)owner.size();
+}
+
+// Slice-image arena of the Ozaki out-of-core mode: the image of tile (i, n)
+// (i > n) is written by its QUANT (iteration n) and read by the GEMMs of row i
+// (A side, columns n+1..i) and column i (B side): it dies with column i.  So
+// the images born in column j take slots freed by rows <= j-1 (final before
+// the QUANTs of column j, which wait for them; those tasks are earlier in the
+// list: no deadlock).  prev[t] = the previous owner of t's image slot.
+// Returns the slot count (the peak live set, ~Nt^2/4 tiles).
+int64_t plan_oz_images(const mxp_plan_s* p, std::vector<int32_t>& slot, std::vector<int32_t>& prev) {
+    const int64_t Nt = p->Nt, T = p->T;
+    slot.assign(T, -1);
+    prev.assign(T, -1);
+    std::vector<int32_t> owner, freelist;
+    for (int64_t j = 0; j < Nt; ++j) {
+        if (j >= 1)  // row j-1 died with column j-1
+            for (int64_t n = 0; n < j - 1; ++n) freelist.push_back(slot[tile_index(Nt, j - 1, n)]);
+        for (int64_t m = j + 1; m < Nt; ++m) {
+            const int64_t t = tile_index(Nt, m, j);
+            int32_t sl;
+            if (!freelist.empty()) {
+                sl = freelist.back();
+                freelist.pop_back();
+            } else {
+                sl = (int32_t)owner.size();
+                owner.push_back(-1);
+            }
+            slot[t] = sl;
+            prev[t] = owner[sl];
+            owner[sl] = (int32_t)t;
         }
     }
     return (int64_t)owner.size();
@@ -358,7 +401,8 @@ bool fits_beside_pool(const mxp_plan_s* p, double need, int64_t pool_tiles = -1)
 void plan_images_as(mxp_plan_s* p, bool native);
 void plan_images(mxp_plan_s* p) {
     const long long key = (((((long long)p->oz_slices * 2 + p->fp64_engine) * 9 + p->nranks) * 4 + p->tc_engine) * 2 +
-                           (pool_slots(p) == p->T ? 1 : 0)) * 2 + p->compact_attr;
+                           (pool_slots(p) == p->T ? 1 : 0)) * 2 + p->compact_attr +
+                          1000003LL * (p->hbm_cap >> 20);  // (the out-of-core Ozaki plan depends on the cap)
     if (key == p->img_key) return;
     p->img_key = key;
     // native-width images (kind::f16 / kind::f8f6f4) run in the tensor-core kernel k_tc, which
@@ -375,6 +419,9 @@ void plan_images_as(mxp_plan_s* p, bool native) {
     p->oz_img.assign(T, -1);
     p->sto.assign(T, -1);
     p->oz_on = false;
+    p->oz_ooc = false;
+    p->ring_slots = p->oz_img_slots = 0;
+    p->img_prev.clear();
     p->nat_on = false;
     p->compact = false;
     p->qtile.assign(T, 0);
@@ -476,6 +523,26 @@ void plan_images_as(mxp_plan_s* p, bool native) {
             for (int64_t k = 0; k < Nt; ++k) p->qtile[tile_index(Nt, k, k)] = 0;
         }
     }
+    // Ozaki out of core (FP64 map, one rank, cap below the fp64 lower triangle): an fp64 ring for
+    // the tiles being computed + a slice-image arena sized by the live set; both under the cap
+    if (!p->oz_on && p->fp64_engine == 1 && !p->mxp && p->nranks == 1 && pool_slots(p) < T) {
+        const long long ob = oz::image_bytes(p->oz_slices, p->nb);
+        std::vector<int32_t> islot, iprev;
+        const int64_t ring = plan_compact(p, p->ring_slot, p->ring_prev, true);
+        const int64_t ni = plan_oz_images(p, islot, iprev);
+        const double need = (double)ring * sizeof(double) * p->nb * p->nb + (double)ni * ob;
+        if (need <= (double)p->hbm_cap && fits_beside_pool(p, (double)ni * ob, ring)) {
+            for (int64_t t = 0; t < T; ++t) {
+                p->oz_img[t] = islot[t] >= 0 ? (long long)islot[t] * ob : -1;
+                p->qtile[t] = islot[t] >= 0 ? 1 : 0;
+            }
+            p->img_prev = iprev;
+            p->shadow_bytes = (size_t)ni * ob;
+            p->oz_on = p->oz_ooc = true;
+            p->ring_slots = ring;
+            p->oz_img_slots = ni;
+        }
+    }
     p->nat_on = native && p->oz_on;
     p->compact = p->nat_on && compact;
     p->compact_slots = p->compact ? ptiles : 0;
@@ -547,6 +614,11 @@ bool plan_slots(mxp_plan_s* p, int64_t C) {
         plan_compact(p, p->slot_plan, p->prev_owner);
         return true;
     }
+    if (p->oz_ooc) {  // Ozaki out of core: the fp64 ring (plan_images)
+        p->slot_plan = p->ring_slot;
+        p->prev_owner = p->ring_prev;
+        return true;
+    }
     p->slot_plan.assign(T, -1);
     p->prev_owner.assign(T, -1);
     if (C >= T) {  // in core: every tile keeps its own slot (L stays resident)
@@ -575,7 +647,7 @@ bool plan_slots(mxp_plan_s* p, int64_t C) {
 
 struct Layout {
     size_t slot, prev, epoch, flags, flags_bytes, expected, items, wbuf, stats, prec, amax_x, amax_s, iscale, args,
-        qtile, img, ozimg, sto, in_scale, solve, shadow, pool, total;
+        qtile, img, ozimg, imgprev, sto, in_scale, solve, shadow, pool, total;
 };
 
 Layout layout(const mxp_plan_s* p) {
@@ -615,6 +687,8 @@ Layout layout(const mxp_plan_s* p) {
     off += align_up(sizeof(long long) * 4 * (size_t)p->T, 256);
     L.ozimg = off;
     off += align_up(sizeof(long long) * (size_t)p->T, 256);
+    L.imgprev = off;
+    off += align_up(sizeof(int32_t) * (size_t)p->T, 256);
     L.sto = off;
     off += align_up(sizeof(long long) * (size_t)p->T, 256);
     L.in_scale = off;
@@ -624,7 +698,8 @@ Layout layout(const mxp_plan_s* p) {
     L.shadow = off;
     off += align_up(p->shadow_bytes, 1024);
     L.pool = off;
-    off += sizeof(double) * (size_t)(p->compact ? p->compact_slots : pool_slots(p)) * p->nb * p->nb;
+    off += sizeof(double) * (size_t)(p->oz_ooc ? p->ring_slots : p->compact ? p->compact_slots : pool_slots(p)) *
+           p->nb * p->nb;
     L.total = off;
     return L;
 }
@@ -681,6 +756,7 @@ void bind_workspace(mxp_plan_s* p) {
     p->d_qtile = (uint8_t*)(p->ws + L.qtile);
     p->d_img = (long long*)(p->ws + L.img);
     p->d_oz_img = (long long*)(p->ws + L.ozimg);
+    p->d_img_prev = (int32_t*)(p->ws + L.imgprev);
     p->d_sto = (long long*)(p->ws + L.sto);
     p->d_in_scale = (double*)(p->ws + L.in_scale);
     p->d_solve = (double*)(p->ws + L.solve);
@@ -972,6 +1048,8 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
             CK(cudaMemcpyAsync(p->d_items + p->items.size(), p->items2.data(), sizeof(int4) * p->items2.size(),
                                cudaMemcpyHostToDevice, s0));
         CK(cudaMemcpyAsync(p->d_oz_img, p->oz_img.data(), sizeof(long long) * T, cudaMemcpyHostToDevice, s0));
+        if (p->oz_ooc)
+            CK(cudaMemcpyAsync(p->d_img_prev, p->img_prev.data(), sizeof(int32_t) * T, cudaMemcpyHostToDevice, s0));
         CK(cudaMemcpyAsync(p->d_expected, p->expected.data(), sizeof(int) * T, cudaMemcpyHostToDevice, s0));
         CK(cudaMemcpyAsync(p->d_prec, p->map.data(), (size_t)T, cudaMemcpyHostToDevice, s0));
         CK(cudaMemcpyAsync(p->d_qtile, p->qtile.data(), (size_t)T, cudaMemcpyHostToDevice, s0));
@@ -1049,6 +1127,8 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     a.prec = (p->mxp || p->oz_on) ? p->d_prec : nullptr;
     a.oz_img = p->oz_on ? p->d_oz_img : nullptr;
     a.oz_slices = p->oz_slices;
+    a.img_prev = p->oz_ooc ? p->d_img_prev : nullptr;
+    a.ring_all = p->oz_ooc ? 1 : 0;
     a.items2 = p->d_items + p->items.size();
     a.nitems2 = (int)p->items2.size();
     a.counter2 = p->d_flags + flag_ints(p) - 1;
@@ -1249,13 +1329,14 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
                 if (prev >= 0) {  // out of core / compact: the slot's previous tile must be dead and written back
                     int64_t pm = 0, pc = 0;
                     tile_coords(Nt, prev, pm, pc);
-                    // compact: a tile below FP64 dies when it is final (its readers use images);
-                    // out of core: when column pm, its last reader, is final
-                    const bool ok = p->compact
+                    // compact / Ozaki ring: an off-diagonal tile dies when it is final (its readers
+                    // use images); out of core, and a diagonal tile of the Ozaki ring (read by the
+                    // TRSMs of its column): when column pm is final
+                    const bool ok = (p->compact || p->oz_ooc) && pm != pc
                         ? g_wait32((CUstream)p->sH2D, (CUdeviceptr)(a.ready + prev), (cuuint32_t)p->epoch,
                                    CU_STREAM_WAIT_VALUE_GEQ) == CUDA_SUCCESS
-                        : g_wait32((CUstream)p->sH2D, (CUdeviceptr)(a.col_ready + pm), (cuuint32_t)(Nt - pm),
-                                   CU_STREAM_WAIT_VALUE_GEQ) == CUDA_SUCCESS;
+                        : g_wait32((CUstream)p->sH2D, (CUdeviceptr)(a.col_ready + (p->oz_ooc ? pc : pm)),
+                                   (cuuint32_t)(Nt - (p->oz_ooc ? pc : pm)), CU_STREAM_WAIT_VALUE_GEQ) == CUDA_SUCCESS;
                     if (!ok ||
                         g_wait32((CUstream)p->sH2D, (CUdeviceptr)(d2h_done + prev), 1, CU_STREAM_WAIT_VALUE_GEQ) !=
                             CUDA_SUCCESS)
@@ -1526,6 +1607,7 @@ int mxp_chol_plan_get(mxp_plan_t p, mxp_attr_t key, int64_t* v) {
     case MXP_ATTR_OZ_SLICES: *v = p->oz_slices; return MXP_OK;
     case MXP_ATTR_COMPACT_POOL: *v = p->compact_attr; return MXP_OK;
     case MXP_ATTR_COMPACT_USED: plan_images(p); *v = p->compact ? 1 : 0; return MXP_OK;
+    case MXP_ATTR_OZ_IMAGE_SLOTS: plan_images(p); *v = p->oz_ooc ? p->oz_img_slots : 0; return MXP_OK;
     case MXP_ATTR_FP64_ENGINE_USED: plan_images(p); *v = p->oz_on ? 1 : 0; return MXP_OK;
     case MXP_ATTR_RANK: *v = p->rank; return MXP_OK;
     case MXP_ATTR_NRANKS: *v = p->nranks; return MXP_OK;
@@ -1534,7 +1616,10 @@ int mxp_chol_plan_get(mxp_plan_t p, mxp_attr_t key, int64_t* v) {
     case MXP_ATTR_GPU_LAUNCHES: *v = p->launches; return MXP_OK;
     case MXP_ATTR_H2D_BYTES: *v = p->h2d; return MXP_OK;
     case MXP_ATTR_D2H_BYTES: *v = p->d2h; return MXP_OK;
-    case MXP_ATTR_POOL_SLOTS: plan_images(p); *v = p->compact ? p->compact_slots : pool_slots(p); return MXP_OK;
+    case MXP_ATTR_POOL_SLOTS:
+        plan_images(p);
+        *v = p->oz_ooc ? p->ring_slots : p->compact ? p->compact_slots : pool_slots(p);
+        return MXP_OK;
     case MXP_ATTR_NT: *v = p->Nt; return MXP_OK;
     case MXP_ATTR_IMAGE_BYTES: plan_images(p); *v = (int64_t)p->shadow_bytes; return MXP_OK;
     case MXP_ATTR_TC_ENGINE_USED: {

@@ -89,6 +89,10 @@ struct SchedArgs {
     const long long* oz_img;   // [T] byte offset of the tile's int8 slice image in `shadow` (-1: none);
                                //     nullptr: the Ozaki engine is off
     int oz_slices;             // s (slices per operand, 1..8)
+    const int32_t* img_prev;   // Ozaki out of core: [T] previous owner of t's slice-image slot (its QUANT
+                               //     waits until that tile's row died: column complete); nullptr in core
+    int ring_all;              // Ozaki out of core: every tile's fp64 slot is a ring slot (diagonal tiles
+                               //     die with their column, the others when final)
     const int4* items2;        // k_tc's list: the WHOLE static list (k_tc alone can finish the
     int nitems2;               //   schedule, e.g. when a profiler serializes the kernels); k_sched
     int* counter2;             //   takes the non-GEMM subsequence (items); both claim non-GEMM tasks

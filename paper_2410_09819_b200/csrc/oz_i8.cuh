@@ -7,28 +7,33 @@
 // columns) is split row by row, exactly, into s int8 slices:
 //
 //   E_r = exponent with max_c |X_rc| < 2^E_r          (frexp of the row max)
-//   y = X_rc 2^-E_r in (-1, 1);  d_1 = rint(64 y), rem = 64 y - d_1,
-//   d_t = rint(128 rem), rem = 128 rem - d_t   (t = 2..s)   -- all exact in fp64
-//   X_rc = 2^(E_r - 6) sum_t d_t 2^(-7(t-1))  +  O(2^(E_r - 7s))
+//   M = rint(X_rc 2^(8s-2-E_r))                        (|M| <= 2^(8s-2): 8s-2 bits + sign)
+//   balanced base-256 digits of M from the low end: d_{s-1}, ..., d_1 in [-128, 127]
+//   (d = ((M + 128) mod 256) - 128, M <- (M - d) / 256, exact integer steps), d_0 = the rest
+//   X_rc ~= 2^(E_r - 6) sum_t d_t 2^(-8t)             (|d_0| <= 64; error <= 2^(E_r - 8s + 1))
 //
-// with |d_t| <= 64.  A product of two tiles is then a sum of int8 GEMMs with
-// exact int32 accumulation; pairs of equal weight (t + u = c) share one TMEM
-// accumulator ("level" c), and pairs below the s-th level are dropped
-// (t + u <= s + 1: s(s+1)/2 int8 GEMMs):
+// A product of two tiles is then a sum of int8 GEMMs with exact int32
+// accumulation; pairs of equal weight (t + u = c) share one TMEM accumulator
+// ("level" c), and the pairs of weight below 2^-8(s-1) are dropped
+// (t + u <= s - 1: s(s+1)/2 int8 GEMMs):
 //
-//   (A B^T)_rj ~= sA_r sB_j sum_{c=2}^{s+1} 2^(-7(c-2)) ACC_c[r][j],
+//   (A B^T)_rj ~= sA_r sB_j sum_{c=0}^{s-1} 2^(-8c) ACC_c[r][j],
 //   ACC_c = sum_{t+u=c} D^A_t D^B_u^T,   sA_r = 2^(EA_r - 6),  sB_j = 2^(EB_j - 6).
 //
 // Each tile of K carries its own row scales, so the levels are drained (int32
 // -> fp64, scaled) after every tile of K into an fp64 register accumulator:
-// the accumulation across tiles is FP64, as in a DGEMM.  s = 8 gives 55 bits
-// per operand (vs 53 for FP64); the dropped pairs weigh <= 2^-56 relative to the
-// row maxima.  |ACC_c| <= 8 * 64^2 * nb < 2^31 for nb <= 65536: no overflow.
+// the accumulation across tiles is FP64, as in a DGEMM.  s = 7 (default) gives
+// 54 bits per operand (vs 53 for FP64) with 28 products; the dropped pairs weigh
+// <= (s-1) 2^(14-8s) of the product of the two row maxima' scales (~1e-15 worst
+// case, random-signed in practice).  |ACC_c| <= s * 2^14 * nb < 2^31 for
+// nb <= 16384: no overflow.  (Round 1 used base-128 digits |d| <= 64, s = 8:
+// 36 products for 55 bits; the full int8 range carries one more bit per slice.)
 //
 // Block shape: 128 (M, rows of A) x 64 (N, rows of B).  s levels x 64 int32
 // columns live in TMEM (s <= 8 -> <= 512 columns: the whole TMEM of the SM;
 // one such CTA per SM), level c at columns [64c, 64c+64).  Stacking B slices
-// along N maps onto consecutive levels, so one MMA of N = 64m covers m pairs.
+// along N maps onto consecutive levels, so one MMA of N = 64m covers m pairs
+// (s = 7: 10 MMAs per 32-K step).
 //
 // Operand image of a tile (written once by the tile's QUANT tasks): for slice
 // t (0-based), 128-row block rb, 32-column K chunk kc, a 4 KB chunk at
@@ -108,16 +113,21 @@ __device__ __forceinline__ double i2d(int x) {
 }
 
 // ---------------------------------------------------------------- slicing
-// The s int8 digits of y = x * 2^-E in (-1, 1) (see the header comment).
+// The s int8 digits of y = x * 2^-E in (-1, 1) (see the header comment):
+// M = rint(y 2^(8s-2)) then balanced base-256 digits, every step exact.
 __device__ __forceinline__ void slice_digits(double y, int s, int (&d)[MAX_S]) {
-    double r = y * 64.0;
+    long long M = __double2ll_rn(y * __longlong_as_double((long long)(1023 + 8 * s - 2) << 52));
 #pragma unroll
-    for (int t = 0; t < MAX_S; ++t) {
-        if (t > 0) r *= 128.0;
-        const double q = rint(r);
-        d[t] = t < s ? (int)q : 0;
-        r -= q;
+    for (int t = MAX_S - 1; t >= 1; --t) {
+        if (t < s) {
+            const int dt = (int)((M + 128) & 255) - 128;  // in [-128, 127]
+            d[t] = dt;
+            M = (M - dt) >> 8;  // exact: M - dt is a multiple of 256
+        } else {
+            d[t] = 0;
+        }
     }
+    d[0] = (int)M;  // |d_0| <= 64
 }
 // 2^(E-6) for the row max m (E: m < 2^E, from frexp); m = 0 -> scale 1 (all digits 0)
 __device__ __forceinline__ double row_scale(double m, double& inv) {
@@ -183,7 +193,7 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int* v) {
 }
 
 // C(128 x 64, fp64, column-major ldc) -= sum over ntiles tiles of A_n B_n^T,
-// each tile of K = 32 * kt (kt = nb / 32) emulated with S slices.
+// each tile of K = 32 * kt (kt = nb / 32) emulated with S slices (kt * 32 <= 16384).
 // smem: >= SMEM_BYTES dynamic shared memory; tmem: 512 allocated columns.
 // All 128 threads call; thread 0 issues the bulk copies and the MMAs (S
 // compile-time: the S(S+1)/2 MMAs of a K step are straight-line code on
@@ -293,8 +303,8 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
             for (int j = 0; j < 8; ++j) {
                 double v = 0.0;
 #pragma unroll
-                for (int c = S - 1; c >= 0; --c)  // smallest weight first; 2^(-7c) exact
-                    v = fma(i2d(x[c][j]), __longlong_as_double((long long)(1023 - 7 * c) << 52), v);
+                for (int c = S - 1; c >= 0; --c)  // smallest weight first; 2^(-8c) exact
+                    v = fma(i2d(x[c][j]), __longlong_as_double((long long)(1023 - 8 * c) << 52), v);
                 acc[g8 * 8 + j] = fma(v * sa_r, s_sb[g8 * 8 + j], acc[g8 * 8 + j]);
             }
         }

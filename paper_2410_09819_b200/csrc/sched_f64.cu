@@ -728,8 +728,20 @@ __device__ __noinline__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k
         if (threadIdx.x == 0) a.iscale[3 * t + 2] = sc;
     }
     if (a.oz_img && a.oz_img[t] >= 0) {  // int8 slices of the stored values (FP64 GEMM operands)
+        if (a.img_prev && threadIdx.x == 0) {  // out of core: the image slot's previous tile (pm, .) has died
+            const int32_t prev = a.img_prev[t];
+            bool ok = true;
+            if (prev >= 0) {
+                int64_t pc = 0, r = prev;
+                while (r >= Nt - pc) { r -= Nt - pc; ++pc; }
+                const int64_t pm = pc + r;
+                ok = wait_flag(a.col_ready + pm, (int)(Nt - pm), a, k);
+            }
+            *s_flag = ok;
+        }
         __threadfence_block();
         sync_workers();
+        if (!*s_flag) return false;
         oz_slice_rows(a, X, r, a.shadow + a.oz_img[t], red);
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");  // images are read by bulk copies
@@ -759,12 +771,18 @@ __device__ __noinline__ bool task_prep(const SchedArgs& a, int64_t m, int64_t k,
         if (a.gen_mode || a.src_A) {
             ok = !skip_column(a, k);
             const int32_t prev = a.prev_owner[t];
-            if (ok && prev >= 0 && a.compact) {  // compact ring: the slot's previous tile dies when final
-                ok = wait_flag(a.ready + prev, a.epoch, a, k);
-            } else if (ok && prev >= 0) {  // out of core: the slot's previous tile (pm, .) dies with column pm
-                int64_t pm = 0, pc = 0, r = prev;
+            int64_t pm = 0, pc = 0;
+            if (prev >= 0) {
+                int64_t r = prev;
                 while (r >= Nt - pc) { r -= Nt - pc; ++pc; }
                 pm = pc + r;
+            }
+            if (ok && prev >= 0 && (a.compact || a.ring_all) && pm != pc) {
+                // compact / Ozaki ring: an off-diagonal tile's slot is free once the tile is final
+                ok = wait_flag(a.ready + prev, a.epoch, a, k);
+            } else if (ok && prev >= 0) {
+                // out of core: the slot's previous tile (pm, .) dies with column pm; a diagonal
+                // tile of the Ozaki ring with its own column (pm = pc)
                 ok = wait_flag(a.col_ready + pm, (int)(Nt - pm), a, k);
             }
         } else {
