@@ -284,6 +284,26 @@ def mxp_roofline(F, peaks):
     return sum(F.values()) / T / 1e12, T
 
 
+def ooc_timeline_summary(tl, t_total):
+    """The paper's Fig. 7 rows (C2G, G2C, Work) as per-column event times of a
+    profiled out-of-core run, plus what they say about overlap: a column's loads finishing
+    after the previous column's POTRF would stall the schedule on the host link."""
+    import numpy as np
+    if not tl:
+        return None
+    h2d, d2h, work = tl["h2d"], tl["d2h"], tl["work"]
+    nt = len(work)
+    late = [k for k in range(1, nt) if h2d[k] >= 0 and work[k - 1] >= 0 and h2d[k] > work[k - 1]]
+    lag = [d2h[k] - work[k] for k in range(nt) if d2h[k] >= 0 and work[k] >= 0]
+    return {"columns": nt, "run_ms": t_total * 1e3,
+            "h2d_done_ms": [round(x, 3) for x in h2d], "d2h_done_ms": [round(x, 3) for x in d2h],
+            "work_done_ms": [round(x, 3) for x in work],
+            "columns_loaded_after_previous_potrf": len(late),
+            "h2d_all_done_ms": max(h2d), "d2h_lag_after_potrf_ms_median": float(np.median(lag)) if lag else None,
+            "how": "CUDA events after each column's H2D loads (C2G), D2H write-backs (G2C) and POTRF (Work), "
+                   "ms since the factorization start (mxp_chol_timeline, MXP_ATTR_PROFILE=1)"}
+
+
 def run_c3(args, m, dev, dev_index, stream, ws, new_plan, allreduce, barrier, dgemm_peak):
     import gc
     import math
@@ -783,9 +803,11 @@ def run_ours(args):
         kl = run_kl_sweep(args, m, dev, new_plan)
         progress("KL sweep")
     # Out of core (a5/a9; C4's mode at a size this box's host RAM holds): the
-    # host matrix streamed through a pool capped at ooc_frac of the lower
-    # triangle (dead-tile slot recycling) vs the same host-streaming call
-    # with every tile resident; plgsy FP64, nb as C2.
+    # host matrix streamed through HBM capped at ooc_frac of the lower
+    # triangle vs the same host-streaming call with every tile resident, with
+    # the C2 FP64 engine (Ozaki: fp64 ring + slice images recycled when their
+    # row dies; DMMA: dead-tile slot recycling); plgsy FP64, nb as C2.  A third,
+    # profiled out-of-core run records the per-column C2G / G2C / Work timeline.
     ooc = None
     if not args.no_ooc and ws == 1:
         import gc
@@ -804,14 +826,18 @@ def run_ours(args):
             torch.cuda.synchronize()
             torch.cuda.empty_cache()
 
-        def run_ooc(cap):
-            ts, hb, db, slots = [], 0, 0, 0
-            for i in range(2):  # first call: warm-up (plan workspace, pinned stage)
+        def run_ooc(cap, profile=False):
+            ts, hb, db, slots, extra = [], 0, 0, 0, {}
+            for i in range(1 if profile else 2):  # first call: warm-up (plan workspace, pinned stage)
                 fresh()
                 pl = m.Plan(no, nbo)
                 pl.set("device", dev_index)
+                pl.set("fp64_engine", ENG[args.fp64_engine])
+                pl.set("oz_slices", args.oz_slices)
                 if cap:
                     pl.set("hbm_bytes_cap", cap)
+                if profile:
+                    pl.set("profile", 1)
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
@@ -821,23 +847,31 @@ def run_ours(args):
                 assert inf == 0, inf
                 ts.append(e0.elapsed_time(e1) / 1e3)
                 hb, db, slots = pl.get("h2d_bytes"), pl.get("d2h_bytes"), pl.get("pool_slots")
+                extra = {"fp64_engine": "ozaki" if pl.get("fp64_engine_used") == 1 else "dmma",
+                         "oz_image_slots": pl.get("oz_image_slots")}
+                if profile:
+                    extra["timeline"] = pl.timeline()
                 pl.close()
                 del pl
                 gc.collect()
                 torch.cuda.empty_cache()
-            return ts[-1], hb, db, slots
+            return ts[-1], hb, db, slots, extra
 
-        t_in, hb_in, db_in, s_in = run_ooc(0)
+        t_in, hb_in, db_in, s_in, x_in = run_ooc(0)
         cap = int(args.ooc_frac * lower)
-        t_oc, hb_oc, db_oc, s_oc = run_ooc(cap)
+        t_oc, hb_oc, db_oc, s_oc, x_oc = run_ooc(cap)
+        t_pr, _, _, _, x_pr = run_ooc(cap, profile=True)
         fl = no ** 3 / 3
         ooc = {"workload": f"plgsy n={no} nb={nbo} FP64 from pinned host memory (mxp_chol_factor)",
                "lower_triangle_gb": round(lower / 1e9, 2),
-               "in_core": {"tflops": fl / t_in / 1e12, "ms": t_in * 1e3, "pool_slots": s_in,
-                           "h2d_bytes": hb_in, "d2h_bytes": db_in},
-               "out_of_core": {"tflops": fl / t_oc / 1e12, "ms": t_oc * 1e3, "pool_slots": s_oc,
-                               "hbm_cap_gb": round(cap / 1e9, 2), "h2d_bytes": hb_oc, "d2h_bytes": db_oc},
+               "in_core": dict({"tflops": fl / t_in / 1e12, "ms": t_in * 1e3, "pool_slots": s_in,
+                                "h2d_bytes": hb_in, "d2h_bytes": db_in}, **x_in),
+               "out_of_core": dict({"tflops": fl / t_oc / 1e12, "ms": t_oc * 1e3, "pool_slots": s_oc,
+                                    "hbm_cap_gb": round(cap / 1e9, 2), "h2d_bytes": hb_oc, "d2h_bytes": db_oc},
+                                   **x_oc),
                "ooc_over_in_core": t_in / t_oc,
+               "ooc_over_c2_device_in_core": (fl / t_oc / 1e12) / value,
+               "timeline": ooc_timeline_summary(x_pr.get("timeline"), t_pr),
                "note": "C4 (n=262144, 276 GB lower triangle) exceeds this box's 196 GB host RAM; the same "
                        "streaming/recycling path is timed with the pool capped below the lower triangle"}
         del Ah

@@ -336,6 +336,19 @@ int mxp_chol_kernel_stats(mxp_plan_t plan, int kernel_class, int64_t* launches, 
                           double* flops);
 
 /*
+ * Copy/compute timeline of the last host-streaming factorization (mxp_chol_factor /
+ * mxp_chol_factor_tiles) run with MXP_ATTR_PROFILE = 1 -- the paper's C2G / G2C / Work rows
+ * (Fig. 7): for each tile column k, three times in milliseconds since the start of
+ * the factorization (CUDA events): [3k] the H2D loads of column k are complete, [3k+1] its D2H
+ * write-backs are complete, [3k+2] its POTRF has finished; -1 where none was recorded.
+ *   ms       host array of `count` doubles (may be NULL when count = 0)  (arg 2)
+ *   count    capacity of ms                                            (arg 3)
+ *   written  receives the number of entries available (3 Nt)            (arg 4)
+ * Returns MXP_ESTATE when no such run exists.
+ */
+int mxp_chol_timeline(mxp_plan_t plan, double* ms, int64_t count, int64_t* written);
+
+/*
  * Scheduler diagnostics of the last factorization when MXP_ATTR_PROFILE is 1
  * (%globaltimer nanoseconds, summed over CTAs): [0] GEMM busy, [1] GEMM wait,
  * [2] TRSM busy, [3] TRSM wait, [4] #GEMM tasks, [5] #TRSM tasks, [6] first

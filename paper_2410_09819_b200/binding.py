@@ -29,7 +29,7 @@ EXPORTS = [
     "mxp_chol_get_factor_device", "mxp_chol_tile_device_ptr", "mxp_chol_ipc_handle", "mxp_chol_ipc_attach",
     "mxp_chol_attach_peer_plan", "mxp_chol_describe", "mxp_chol_solve_lower", "mxp_chol_loglik",
     "mxp_chol_plan_destroy", "mxp_host_alloc", "mxp_host_free", "mxp_strerror", "mxp_last_error",
-    "mxp_chol_abi_version", "mxp_chol_kernel_stats", "mxp_chol_sched_diagnostics",
+    "mxp_chol_abi_version", "mxp_chol_kernel_stats", "mxp_chol_timeline", "mxp_chol_sched_diagnostics",
 ]
 KCLASS = {"chain": 0, "potrf": 1, "trsm": 2, "other": 3}
 
@@ -85,6 +85,7 @@ def lib():
         L.mxp_last_error.restype = ctypes.c_char_p
         L.mxp_chol_abi_version.argtypes = []
         L.mxp_chol_kernel_stats.argtypes = [vp, i32, pi64, pd, pd]
+        L.mxp_chol_timeline.argtypes = [vp, pd, i64, pi64]
         L.mxp_chol_factor_matern.argtypes = [vp, vp, ctypes.c_double, ctypes.c_double, ctypes.c_double, pi64]
         L.mxp_precision_map_matern_device.argtypes = [i64, i64, vp, ctypes.c_double, ctypes.c_double,
                                                       ctypes.c_double, ctypes.c_double, ctypes.c_uint32, vp, vp]
@@ -305,6 +306,16 @@ class Plan:
                 self._h, c, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(fl)))
             out[name] = (n.value, ms.value, fl.value)
         return out
+
+    def timeline(self) -> dict:
+        """Per-column copy/compute timeline of the last host-streaming factorization with
+        profile=1 (ms since its start): {"h2d": [...], "d2h": [...], "work": [...]}, -1 = none."""
+        n = ctypes.c_int64()
+        _check("mxp_chol_timeline", lib().mxp_chol_timeline(self._h, None, 0, ctypes.byref(n)))
+        buf = (ctypes.c_double * n.value)()
+        _check("mxp_chol_timeline", lib().mxp_chol_timeline(self._h, buf, n.value, ctypes.byref(n)))
+        v = list(buf)
+        return {"h2d": v[0::3], "d2h": v[1::3], "work": v[2::3]}
 
     def sched_diagnostics(self) -> dict:
         """Device-side scheduler timing of the last factorization (profile=1)."""

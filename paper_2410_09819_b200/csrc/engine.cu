@@ -171,6 +171,13 @@ struct mxp_plan_s {
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
+    // copy/compute timeline of the last host-streaming factorization with MXP_ATTR_PROFILE = 1
+    // (the paper's C2G / G2C / Work rows): per column k, events after its H2D loads,
+    // after its D2H write-backs and after its POTRF; tl_ms = ms since the factorization start
+    std::vector<cudaEvent_t> ev_tl;
+    std::vector<char> tl_rec;
+    std::vector<double> tl_ms;
+    bool tl_on = false;
     int64_t st_launch[4] = {0, 0, 0, 0};
     double st_ms[4] = {0, 0, 0, 0}, st_flops[4] = {0, 0, 0, 0};
     bool have_result = false;
@@ -187,6 +194,7 @@ mxp_plan_s::~mxp_plan_s() {
     for (auto e : ev_panel) cudaEventDestroy(e);
     for (auto e : ev_bulk) cudaEventDestroy(e);
     for (auto e : ev_pool) cudaEventDestroy(e);
+    for (auto e : ev_tl) cudaEventDestroy(e);
     if (ev_start) cudaEventDestroy(ev_start);
     if (ev_done) cudaEventDestroy(ev_done);
     if (sU) cudaStreamDestroy(sU);
@@ -327,9 +335,13 @@ int64_t plan_compact(const mxp_plan_s* p, std::vector<int32_t>& slot, std::vecto
     prev.assign(T, -1);
     std::vector<int32_t> owner, freelist;
     std::vector<std::vector<int32_t>> freed_at(Nt);
+    // all (Ozaki out of core): slots freed by columns <= j-3 -- the tiles of column j are
+    // loaded during iteration j-2 (for the lookahead GEMMs of iteration j-1), while column
+    // j-2's tiles become final and stream back (D2H) about one column later (measured)
+    const int64_t lag = all ? 3 : 2;
     for (int64_t j = 0; j < Nt; ++j) {
-        if (j >= 2)
-            for (int32_t x : freed_at[j - 2]) freelist.push_back(x);
+        if (j >= lag)
+            for (int32_t x : freed_at[j - lag]) freelist.push_back(x);
         for (int64_t m = j; m < Nt; ++m) {
             const int64_t t = tile_index(Nt, m, j);
             int32_t sl;
@@ -354,9 +366,10 @@ int64_t plan_compact(const mxp_plan_s* p, std::vector<int32_t>& slot, std::vecto
 // Slice-image arena of the Ozaki out-of-core mode: the image of tile (i, n)
 // (i > n) is written by its QUANT (iteration n) and read by the GEMMs of row i
 // (A side, columns n+1..i) and column i (B side): it dies with column i.  So
-// the images born in column j take slots freed by rows <= j-1 (final before
-// the QUANTs of column j, which wait for them; those tasks are earlier in the
-// list: no deadlock).  prev[t] = the previous owner of t's image slot.
+// the images born in column j take slots freed by rows <= j-2 (complete
+// before the QUANTs of column j, which wait for them; those tasks are earlier
+// in the list: no deadlock; one row of slack so a QUANT of column j rarely
+// waits for the last QUANTs of column j-1).  prev[t] = the previous owner of t's image slot.
 // Returns the slot count (the peak live set, ~Nt^2/4 tiles).
 int64_t plan_oz_images(const mxp_plan_s* p, std::vector<int32_t>& slot, std::vector<int32_t>& prev) {
     const int64_t Nt = p->Nt, T = p->T;
@@ -364,8 +377,8 @@ int64_t plan_oz_images(const mxp_plan_s* p, std::vector<int32_t>& slot, std::vec
     prev.assign(T, -1);
     std::vector<int32_t> owner, freelist;
     for (int64_t j = 0; j < Nt; ++j) {
-        if (j >= 1)  // row j-1 died with column j-1
-            for (int64_t n = 0; n < j - 1; ++n) freelist.push_back(slot[tile_index(Nt, j - 1, n)]);
+        if (j >= 2)  // row j-2 died with column j-2
+            for (int64_t n = 0; n < j - 2; ++n) freelist.push_back(slot[tile_index(Nt, j - 2, n)]);
         for (int64_t m = j + 1; m < Nt; ++m) {
             const int64_t t = tile_index(Nt, m, j);
             int32_t sl;
@@ -844,6 +857,35 @@ struct Prof {
         }
     }
 };
+void timeline_begin(mxp_plan_s* p) {
+    const size_t need = 3 * (size_t)p->Nt + 1;  // + [3 Nt]: the start (timing event beside ev_start)
+    while (p->ev_tl.size() < need) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        p->ev_tl.push_back(e);
+    }
+    p->tl_rec.assign(need, 0);
+    p->tl_ms.clear();
+    p->tl_on = true;
+}
+void timeline_mark(mxp_plan_s* p, int64_t k, int row, cudaStream_t s) {  // row 0 H2D, 1 D2H, 2 POTRF
+    if (!p->tl_on) return;
+    CK(cudaEventRecord(p->ev_tl[3 * k + row], s));
+    p->tl_rec[3 * k + row] = 1;
+}
+void timeline_collect(mxp_plan_s* p) {  // after every stream of the run has been synchronized
+    if (!p->tl_on) return;
+    p->tl_on = false;
+    const size_t n3 = 3 * (size_t)p->Nt;
+    p->tl_ms.assign(n3, -1.0);
+    if (!p->tl_rec[n3]) return;
+    for (size_t i = 0; i < n3; ++i)
+        if (p->tl_rec[i]) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, p->ev_tl[n3], p->ev_tl[i]));
+            p->tl_ms[i] = ms;
+        }
+}
 void prof_reset(mxp_plan_s* p) {
     p->recs.clear();
     p->ev_used = 0;
@@ -1072,6 +1114,10 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
         p->ready_dirty = true;
     }
     CK(cudaEventRecord(p->ev_start, s0));
+    if (p->tl_on) {  // timeline origin (ev_start has timing disabled)
+        CK(cudaEventRecord(p->ev_tl[3 * Nt], s0));
+        p->tl_rec[3 * Nt] = 1;
+    }
     CK(cudaStreamWaitEvent(p->sU, p->ev_start, 0));
     CK(cudaStreamWaitEvent(p->sP, p->ev_start, 0));
     if (p->oz_on) {
@@ -1190,6 +1236,8 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     } else {
         // Ozaki mode: the GEMM kernel (one CTA per SM, all TMEM) on sT beside
         // one k_sched CTA per SM (TRSM / QUANT / PREP / POTRF fallback) on sU
+        // (measured: k_tc alone with a 5-stage ring and the TRSM / QUANT tasks
+        // in its own list order ran C2 at 60.7 TF/s vs 65.0 co-scheduled)
         double trsm_flops = 0.0;
         for (int64_t m = p->rank; m < Nt; m += p->nranks) trsm_flops += (double)m * nb3;
         p->h_args = a;
@@ -1217,6 +1265,7 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
             for (int64_t k = p->rank; k < Nt; k += p->nranks) {  // diagonal tiles this rank owns
                 launch_potrf_tile(a, k, p->sP);
                 ++p->launches;
+                timeline_mark(p, k, 2, p->sP);
             }
         }
         CK(cudaGetLastError());
@@ -1278,7 +1327,7 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
         feed([&, nb, n] {
             // D2H of each finished tile as soon as Ready(t) flips (lower triangle only);
             // diagonal tiles go to a pinned stage and only their lower triangle is merged
-            for (int64_t k = 0; k < Nt; ++k)
+            for (int64_t k = 0; k < Nt; ++k) {
                 for (int64_t m = k; m < Nt; ++m) {
                     if (m % p->nranks != p->rank) continue;
                     const int64_t t = tile_index(Nt, m, k);
@@ -1306,8 +1355,10 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
                         CUDA_SUCCESS)
                         throw CudaError{cudaErrorUnknown};
                 }
+                timeline_mark(p, k, 1, p->sD2H);
+            }
         });
-        for (int64_t k = 0; k < Nt; ++k)
+        for (int64_t k = 0; k < Nt; ++k) {
             for (int64_t m = k; m < Nt; ++m) {
                 if (m % p->nranks != p->rank) continue;  // peers stream their own rows
                 const int64_t t = tile_index(Nt, m, k);
@@ -1353,6 +1404,8 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
                 if (g_write32((CUstream)p->sH2D, (CUdeviceptr)(a.loaded + t), 1, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
                     throw CudaError{cudaErrorUnknown};
             }
+            timeline_mark(p, k, 0, p->sH2D);
+        }
         join_all();
         p->d2h += d2h_bytes;
     } catch (...) {
@@ -1579,6 +1632,17 @@ int mxp_chol_sched_diagnostics(mxp_plan_t p, uint64_t* out, int64_t count, int64
     int64_t n = std::min<int64_t>(count, (int64_t)p->h_stats.size());
     for (int64_t i = 0; i < n; ++i) out[i] = p->h_stats[i];
     if (written) *written = (int64_t)p->h_stats.size();
+    return MXP_OK;
+}
+
+int mxp_chol_timeline(mxp_plan_t p, double* ms, int64_t count, int64_t* written) {
+    if (!p) return -1;
+    if (!ms && count > 0) return -2;
+    if (count < 0) return -3;
+    if (p->tl_ms.empty()) return MXP_ESTATE;
+    const int64_t w = std::min<int64_t>(count, (int64_t)p->tl_ms.size());
+    for (int64_t i = 0; i < w; ++i) ms[i] = p->tl_ms[i];
+    if (written) *written = (int64_t)p->tl_ms.size();
     return MXP_OK;
 }
 
@@ -1809,6 +1873,7 @@ int mxp_chol_factor(mxp_plan_t p, double* A_host, int64_t lda, int64_t* info) {
         CK(cudaMemcpyAsync(p->d_prev, p->prev_owner.data(), sizeof(int32_t) * p->T, cudaMemcpyHostToDevice, s0));
         CK(cudaMemsetAsync(p->d_info, 0, sizeof(int64_t), s0));
         prof_reset(p);
+        if (p->profile) timeline_begin(p);
         factor_incore_f64(p, s0, true, A_host, lda);
         finish_pushes(p, s0);  // several ranks: drain / await the tile exchange
         // the schedule (U) and the POTRFs (P) end first; on failure the later
@@ -1828,6 +1893,8 @@ int mxp_chol_factor(mxp_plan_t p, double* A_host, int64_t lda, int64_t* info) {
         }
         CK(cudaStreamSynchronize(p->sD2H));
         CK(cudaStreamSynchronize(p->sH2D));
+        CK(cudaStreamSynchronize(p->sP));
+        timeline_collect(p);
         if (herr) {
             g_last_error = "static schedule: a Ready-table wait timed out (scheduler error)" + sched_timeout_detail(p);
             throw CudaError{cudaErrorLaunchTimeout};
@@ -1924,6 +1991,7 @@ int mxp_chol_factor_tiles(mxp_plan_t p, void* const* tiles, double* scales, int6
         prof_reset(p);
         p->tiles_io = tiles;
         try {
+            if (p->profile) timeline_begin(p);
             factor_incore_f64(p, s0, true, nullptr, p->n);
         } catch (...) {
             p->tiles_io = nullptr;
@@ -1937,6 +2005,8 @@ int mxp_chol_factor_tiles(mxp_plan_t p, void* const* tiles, double* scales, int6
         CK(cudaMemcpy(&herr, p->d_flags + 1, sizeof(int), cudaMemcpyDeviceToHost));
         CK(cudaStreamSynchronize(p->sD2H));
         CK(cudaStreamSynchronize(p->sH2D));
+        CK(cudaStreamSynchronize(p->sP));
+        timeline_collect(p);
         if (herr) {
             g_last_error = "static schedule: a Ready-table wait timed out (scheduler error)" + sched_timeout_detail(p);
             throw CudaError{cudaErrorLaunchTimeout};

@@ -172,7 +172,7 @@ def _oz_ooc_cap(n, nb, frac, s=7):
     return int(frac * Nt * (Nt + 1) // 2 * nb * nb * 8)
 
 
-@pytest.mark.parametrize("n,nb,frac", [(4096, 256, 0.8), (3000, 256, 0.9), (4096, 512, 0.95), (12288, 256, 0.6)])
+@pytest.mark.parametrize("n,nb,frac", [(4096, 256, 0.9), (3000, 256, 0.97), (8192, 512, 0.9), (12288, 256, 0.62)])
 def test_ozaki_out_of_core_bitwise_equals_in_core(n, nb, frac):
     """HBM cap below the lower triangle with the Ozaki engine: fp64 tiles live in a
     ring only while computed, final tiles as slice images whose slots are recycled
@@ -207,7 +207,7 @@ def test_ozaki_out_of_core_repeat_and_kms():
     A = w.kms(n, rho)
     plan = m.Plan(n, nb)
     plan.set("fp64_engine", 1)
-    plan.set("hbm_bytes_cap", _oz_ooc_cap(n, nb, 0.8))
+    plan.set("hbm_bytes_cap", _oz_ooc_cap(n, nb, 0.9))
     assert plan.get("oz_image_slots") > 0
     L1, i1, ld1, _ = gpu_factor(A, nb, host=True, plan=plan)
     L2, i2, ld2, _ = gpu_factor(A, nb, host=True, plan=plan)
@@ -248,7 +248,7 @@ def test_ozaki_out_of_core_not_pd_does_not_hang(j):
     del Ad
     plan = m.Plan(n, nb)
     plan.set("fp64_engine", 1)
-    plan.set("hbm_bytes_cap", _oz_ooc_cap(n, nb, 0.6))
+    plan.set("hbm_bytes_cap", _oz_ooc_cap(n, nb, 0.62))
     assert plan.get("oz_image_slots") > 0
     assert plan.factor(Ah.T) == j + 1
 
@@ -266,7 +266,28 @@ def test_ozaki_out_of_core_generated_matern_fp64():
     assert pin.factor_matern(xy, 1.0, 0.078809) == 0
     pl = m.Plan(n, nb)
     pl.set("fp64_engine", 1)
-    pl.set("hbm_bytes_cap", _oz_ooc_cap(n, nb, 0.8))
+    pl.set("hbm_bytes_cap", _oz_ooc_cap(n, nb, 0.9))
     assert pl.get("oz_image_slots") > 0
     assert pl.factor_matern(xy, 1.0, 0.078809) == 0
     assert pl.logdet() == pin.logdet()
+
+
+def test_out_of_core_timeline():
+    """mxp_chol_timeline (profile=1): per column, the loads complete in column order and
+    before the column's write-backs; its POTRF completes before its last write-back."""
+    import paper_2410_09819_b200 as m
+    n, nb = 4096, 256
+    A = w.plgsy(n, seed=8)
+    for eng, frac in ((1, 0.9), (0, 0.62)):
+        plan = m.Plan(n, nb)
+        plan.set("fp64_engine", eng)
+        plan.set("hbm_bytes_cap", _oz_ooc_cap(n, nb, frac))
+        plan.set("profile", 1)
+        L, info, _, _ = gpu_factor(A, nb, host=True, plan=plan)
+        assert info == 0 and plan.get("fp64_engine_used") == eng
+        tl = plan.timeline()
+        Nt = n // nb
+        assert len(tl["h2d"]) == len(tl["d2h"]) == len(tl["work"]) == Nt
+        for k in range(Nt):
+            assert 0 <= tl["h2d"][k] <= tl["d2h"][k] and 0 <= tl["work"][k] <= tl["d2h"][k] + 1e-3, (k, tl)
+            assert k == 0 or tl["h2d"][k - 1] <= tl["h2d"][k] + 1e-3
