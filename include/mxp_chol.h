@@ -105,6 +105,8 @@ typedef enum mxp_attr {
                                        behaves as 0 -- see MXP_ATTR_FP64_ENGINE_USED.  Re-sizes the workspace. */
     MXP_ATTR_OZ_SLICES = 13,      /* s for MXP_ATTR_FP64_ENGINE = 1, 4..8 (default 7: 54 bits per operand,
                                      28 int8 products; dropped products <= 6 * 2^-52 of the row maxima) */
+    MXP_ATTR_OZ_PREFETCH = 15,    /* Ozaki engine: L2 prefetch (cp.async.bulk.prefetch.L2) of the operand chunks
+                                     this many 32-K steps ahead of the shared-memory ring, 0..64 (0 = off) */
     MXP_ATTR_COMPACT_POOL = 14,   /* with the native engine (MXP_ATTR_TC_ENGINE_USED = 3): 1 (default) = store every
                                      tile below FP64 at its precision (codes + a power-of-two scale: 4/2/1 bytes per
                                      element, "minimum acceptable bytes per word"); its fp64 accumulator slot
@@ -131,9 +133,20 @@ typedef enum mxp_attr {
  *   n             matrix order, n >= 1                              (arg 1)
  *   nb            tile size; nb % 128 == 0, 128 <= nb <= 2048        (arg 2)
  *   precision_map host array of Nt(Nt+1)/2 codes, copied; NULL = all FP64 (arg 3)
- *   ngpus         GPUs the plan spans: 1 (one plan per GPU and process; several GPUs
- *                 cooperate through MXP_ATTR_RANK / MXP_ATTR_NRANKS and the peer
- *                 attach calls below); other values return -4        (arg 4)
+ *   ngpus         GPUs the plan spans, 1..8 (other values return -4)    (arg 4)
+ *                 1: one plan per GPU and process; several processes cooperate through
+ *                    MXP_ATTR_RANK / MXP_ATTR_NRANKS and the peer attach calls below.
+ *                 > 1: a group plan in this process (SURVEY 8(e), row-cyclic P x 1):
+ *                    one sub-plan per rank r on device r mod cudaGetDeviceCount(), tile row
+ *                    m owned by rank m mod ngpus, finished tiles pushed to the peers over
+ *                    P2P; the factor calls run every rank from its own host thread and
+ *                    return when all are done.  Ranks that share a device split its SMs.
+ *                    Attributes apply to every rank (MXP_ATTR_DEVICE / RANK / NRANKS /
+ *                    SM_FIRST / SM_COUNT: MXP_ENOTSUP; MXP_ATTR_STREAM orders rank 0);
+ *                    mxp_chol_factor_device reads A from its device (peers by P2P) and
+ *                    rank 0 writes L back; results, log-det and solves come from rank 0;
+ *                    the *_BYTES / GPU_LAUNCHES getters sum over ranks.  Out-of-core
+ *                    streaming and mxp_chol_factor_tiles stay single-rank (MXP_ENOTSUP).
  *   out           receives the plan handle                           (arg 5)
  * No device memory is allocated here; that happens on the first factor call
  * (or mxp_chol_set_workspace).
@@ -347,6 +360,25 @@ int mxp_chol_kernel_stats(mxp_plan_t plan, int kernel_class, int64_t* launches, 
  * Returns MXP_ESTATE when no such run exists.
  */
 int mxp_chol_timeline(mxp_plan_t plan, double* ms, int64_t count, int64_t* written);
+
+/*
+ * Host-link byte ledger of the paper's out-of-core variants (P:202-206 sync /
+ * async, P:235 V1, Alg. 3 P:281-303 V2, P:303 V3, volumes P:496-508) replayed over the static
+ * left-looking task sequence of Alg. 2 (tasks (m, k) column by column, dealt 1-D cyclically to
+ * `streams` streams that advance in lockstep) with a tile cache of hbm_bytes / (8 nb^2) FP64
+ * tiles.  Pure host computation (no GPU); the engine itself runs variant 5.
+ *   n, nb      problem size and tile size                                  (args 1, 2)
+ *   variant    0 sync, 1 async (no cache: every update loads its accumulator and operands and
+ *              writes the accumulator back), 2 V1 (accumulator resident per task), 3 V2 (+ LRU
+ *              cache table of operands and final tiles), 4 V3 (V2 + L_kk pinned until the last
+ *              TRSM of its column), 5 static dead-tile plan (each tile once each way; needs the
+ *              live set), 6 MIN (Belady's optimal eviction for this sequence)      (arg 3)
+ *   streams    1..64 concurrent task streams (the paper's multi-stream async)  (arg 4)
+ *   hbm_bytes  device memory for tiles; 0 = unlimited                          (arg 5)
+ *   out        [4]: host->device bytes, device->host bytes, tile loads, peak resident tiles
+ * Returns MXP_ENOMEM when the capacity cannot hold the variant's minimum working set.
+ */
+int mxp_ooc_variant_volume(int64_t n, int64_t nb, int variant, int streams, int64_t hbm_bytes, int64_t* out);
 
 /*
  * Scheduler diagnostics of the last factorization when MXP_ATTR_PROFILE is 1

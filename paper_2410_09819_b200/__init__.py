@@ -32,13 +32,14 @@ from .binding import (  # noqa: F401
     host_free,
     lib,
     lib_path,
+    ooc_variant_volume,
     precision_map_from_matrix,
     precision_map_from_matrix_device,
     precision_map_matern_device,
 )
 
 __all__ = [
-    "FP64", "FP32", "FP16", "FP8", "MxpError", "Plan", "abi_version", "lib", "lib_path",
+    "FP64", "FP32", "FP16", "FP8", "MxpError", "Plan", "abi_version", "lib", "lib_path", "ooc_variant_volume",
     "precision_map_from_matrix", "precision_map_from_matrix_device", "generate_plgsy_device", "generate_kms_device",
     "generate_matern_device", "precision_map_matern_device",
     "host_alloc", "host_free",

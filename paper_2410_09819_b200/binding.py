@@ -15,7 +15,7 @@ _lock = threading.Lock()
 ATTR = {
     "device": 0, "stream": 1, "hbm_bytes_cap": 2, "splitk_tiles": 3, "lookahead": 4,
     "debug_sync": 5, "profile": 6, "tc_engine": 7, "rank": 8, "nranks": 9, "sm_first": 10,
-    "sm_count": 11, "fp64_engine": 12, "oz_slices": 13, "gpu_launches": 100, "h2d_bytes": 101, "d2h_bytes": 102,
+    "sm_count": 11, "fp64_engine": 12, "oz_slices": 13, "oz_prefetch": 15, "gpu_launches": 100, "h2d_bytes": 101, "d2h_bytes": 102,
     "pool_slots": 103, "nt": 104, "image_bytes": 105, "fp64_engine_used": 106, "tc_engine_used": 107, "compact_pool": 14,
     "compact_used": 108, "oz_image_slots": 109,
 }
@@ -29,7 +29,7 @@ EXPORTS = [
     "mxp_chol_get_factor_device", "mxp_chol_tile_device_ptr", "mxp_chol_ipc_handle", "mxp_chol_ipc_attach",
     "mxp_chol_attach_peer_plan", "mxp_chol_describe", "mxp_chol_solve_lower", "mxp_chol_loglik",
     "mxp_chol_plan_destroy", "mxp_host_alloc", "mxp_host_free", "mxp_strerror", "mxp_last_error",
-    "mxp_chol_abi_version", "mxp_chol_kernel_stats", "mxp_chol_timeline", "mxp_chol_sched_diagnostics",
+    "mxp_chol_abi_version", "mxp_chol_kernel_stats", "mxp_chol_timeline", "mxp_ooc_variant_volume", "mxp_chol_sched_diagnostics",
 ]
 KCLASS = {"chain": 0, "potrf": 1, "trsm": 2, "other": 3}
 
@@ -86,6 +86,7 @@ def lib():
         L.mxp_chol_abi_version.argtypes = []
         L.mxp_chol_kernel_stats.argtypes = [vp, i32, pi64, pd, pd]
         L.mxp_chol_timeline.argtypes = [vp, pd, i64, pi64]
+        L.mxp_ooc_variant_volume.argtypes = [i64, i64, i32, i32, i64, pi64]
         L.mxp_chol_factor_matern.argtypes = [vp, vp, ctypes.c_double, ctypes.c_double, ctypes.c_double, pi64]
         L.mxp_precision_map_matern_device.argtypes = [i64, i64, vp, ctypes.c_double, ctypes.c_double,
                                                       ctypes.c_double, ctypes.c_double, ctypes.c_uint32, vp, vp]
@@ -394,6 +395,21 @@ def precision_map_from_matrix_device(A, nb: int, eps: float, allowed: int = 0xF)
            lib().mxp_precision_map_from_matrix_device(n, nb, ptr, lda, float(eps), allowed,
                                                       m.ctypes.data, f.ctypes.data))
     return m, f
+
+
+OOC_VARIANTS = {"sync": 0, "async": 1, "V1": 2, "V2": 3, "V3": 4, "static": 5, "MIN": 6}
+
+
+def ooc_variant_volume(n: int, nb: int, variant: str, hbm_bytes: int = 0, streams: int = 1):
+    """Host-link ledger of one of the paper's OOC variants over the static schedule
+    (mxp_ooc_variant_volume): {"h2d_bytes", "d2h_bytes", "loads", "peak_tiles"}, or None
+    when the capacity cannot hold the variant's working set."""
+    out = (ctypes.c_int64 * 4)()
+    rc = lib().mxp_ooc_variant_volume(int(n), int(nb), OOC_VARIANTS[variant], int(streams), int(hbm_bytes), out)
+    if rc == -1002:
+        return None
+    _check("mxp_ooc_variant_volume", rc)
+    return {"h2d_bytes": out[0], "d2h_bytes": out[1], "loads": out[2], "peak_tiles": out[3]}
 
 
 def precision_map_matern_device(xy, nb: int, eps: float, sigma2: float = 1.0, range_a: float = 0.02627,

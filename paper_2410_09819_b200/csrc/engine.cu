@@ -105,6 +105,7 @@ struct mxp_plan_s {
     // FP64 engine (MXP_ATTR_FP64_ENGINE): 0 DMMA, 1 Ozaki int8 on tcgen05 (in core);
     // oz_on = the engine actually used by the current image plan
     int fp64_engine = 0, oz_slices = 7;
+    int oz_prefetch = 0;            // MXP_ATTR_OZ_PREFETCH
     bool oz_on = false;
     bool nat_on = false;            // tiles below FP64 on the native-width engine (tc_engine 3, k_tc)
     // compact pool (with the native engine): only FP64 tiles keep a permanent fp64 slot; a tile
@@ -182,11 +183,16 @@ struct mxp_plan_s {
     double st_ms[4] = {0, 0, 0, 0}, st_flops[4] = {0, 0, 0, 0};
     bool have_result = false;
     double logdet = 0.0;
+    // single-process multi-GPU (mxp_chol_plan with ngpus > 1): the group plan owns one sub-plan
+    // per GPU (rank r, device r mod #devices) and runs them from one host thread each
+    std::vector<mxp_plan_s*> group;
+    bool in_group = false;  // a sub-plan: only rank 0 writes the factor back (factor_device)
 
     ~mxp_plan_s();
 };
 
 mxp_plan_s::~mxp_plan_s() {
+    for (auto* c : group) delete c;
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(device);
@@ -1173,6 +1179,7 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     a.prec = (p->mxp || p->oz_on) ? p->d_prec : nullptr;
     a.oz_img = p->oz_on ? p->d_oz_img : nullptr;
     a.oz_slices = p->oz_slices;
+    a.oz_prefetch = p->oz_prefetch;
     a.img_prev = p->oz_ooc ? p->d_img_prev : nullptr;
     a.ring_all = p->oz_ooc ? 1 : 0;
     a.items2 = p->d_items + p->items.size();
@@ -1462,6 +1469,49 @@ int status_from_exception(const CudaError& e) {
 
 }  // namespace
 
+// ---- single-process multi-GPU (a group plan: one sub-plan per GPU) ----------
+bool is_group(const mxp_plan_s* p) { return p && !p->group.empty(); }
+// attach every sub-plan to every other (in-process peer pools; re-done before
+// every run: a sub-plan whose workspace was re-sized has dropped its peers)
+int group_attach(mxp_plan_s* g) {
+    const int P = (int)g->group.size();
+    for (int r = 0; r < P; ++r)
+        for (int q = 0; q < P; ++q)
+            if (q != r) {
+                const int rc = mxp_chol_attach_peer_plan(g->group[r], q, g->group[q]);
+                if (rc != MXP_OK) return rc;
+            }
+    return MXP_OK;
+}
+// fn(sub-plan, &info) on every sub-plan, each from its own host thread (the
+// sub-plans' schedules wait on each other's pushed tiles); first error wins
+template <class F>
+int group_run(mxp_plan_s* g, int64_t* info, F fn) {
+    g->have_result = false;
+    int rc = group_attach(g);
+    if (rc != MXP_OK) return rc;
+    const int P = (int)g->group.size();
+    std::vector<int> st(P, MXP_OK);
+    std::vector<int64_t> inf(P, 0);
+    std::vector<std::string> err(P);
+    std::vector<std::thread> th;
+    for (int r = 0; r < P; ++r)
+        th.emplace_back([&, r] {
+            st[r] = fn(g->group[r], &inf[r]);
+            if (st[r] != MXP_OK) err[r] = g_last_error;
+        });
+    for (auto& t : th) t.join();
+    for (int r = 0; r < P; ++r)
+        if (st[r] != MXP_OK) {
+            g_last_error = "rank " + std::to_string(r) + ": " + err[r];
+            return st[r];
+        }
+    *info = inf[0];  // (a failed pivot is propagated to every rank)
+    g->have_result = g->group[0]->have_result;
+    g->logdet = g->group[0]->logdet;
+    return MXP_OK;
+}
+
 // =========================================================================
 extern "C" {
 
@@ -1486,8 +1536,60 @@ const char* mxp_last_error(void) { return g_last_error.c_str(); }
 int mxp_chol_plan(int64_t n, int64_t nb, const uint8_t* precision_map, int ngpus, mxp_plan_t* out) {
     if (n < 1) return -1;
     if (nb < 128 || nb > 2048 || nb % 128 != 0) return -2;
-    if (ngpus != 1) return -4;
+    if (ngpus < 1 || ngpus > MAX_RANKS) return -4;
     if (!out) return -5;
+    if (ngpus > 1) {
+        // Single-process multi-GPU: one sub-plan per GPU in the row-cyclic
+        // distribution (rank r = GPU r mod #devices, tile row m on rank m mod ngpus), attached
+        // to each other in process (peer access).  With fewer devices than ranks the ranks
+        // sharing a device split its SMs (the co-located test setup).
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+            cudaGetLastError();
+            g_last_error = "ngpus > 1: no CUDA device";
+            return MXP_ECUDA;
+        }
+        std::vector<mxp_plan_s*> kids;
+        for (int r = 0; r < ngpus; ++r) {
+            mxp_plan_t c = nullptr;
+            const int rc = mxp_chol_plan(n, nb, precision_map, 1, &c);
+            if (rc != MXP_OK) {
+                for (auto* k : kids) delete k;
+                return rc;
+            }
+            c->rank = r;
+            c->nranks = ngpus;
+            c->device = r % ndev;
+            c->in_group = true;
+            kids.push_back(c);
+        }
+        for (int r = 0; r < ngpus; ++r) {  // SM partitions of co-located ranks
+            int share = 0, idx = 0;
+            for (int q = 0; q < ngpus; ++q)
+                if (kids[q]->device == kids[r]->device) idx += (q < r), ++share;
+            if (share > 1) {
+                // one SM stays outside every partition: a device-to-device copy between two
+                // pools on the same GPU runs as a copy kernel, which must find an SM that the
+                // persistent schedules do not hold (on separate GPUs the copy engines move it)
+                int nsm = 0;
+                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, kids[r]->device);
+                cudaGetLastError();
+                kids[r]->sm_first = idx * ((nsm - 1) / share);
+                kids[r]->sm_count = (nsm - 1) / share;
+            }
+        }
+        auto* g = new mxp_plan_s();
+        g->n = n;
+        g->nb = nb;
+        g->Nt = kids[0]->Nt;
+        g->T = kids[0]->T;
+        g->map = kids[0]->map;
+        g->mxp = kids[0]->mxp;
+        g->device = kids[0]->device;
+        g->group = std::move(kids);
+        *out = g;
+        return MXP_OK;
+    }
     int64_t Nt = (n + nb - 1) / nb;
     int64_t T = Nt * (Nt + 1) / 2;
     if (T > INT32_MAX) return -1;
@@ -1525,6 +1627,17 @@ int mxp_chol_plan(int64_t n, int64_t nb, const uint8_t* precision_map, int ngpus
 
 int mxp_chol_plan_set(mxp_plan_t p, mxp_attr_t key, int64_t v) {
     if (!p) return -1;
+    if (is_group(p)) {  // the group places its ranks itself; the user stream orders rank 0
+        if (key == MXP_ATTR_DEVICE || key == MXP_ATTR_RANK || key == MXP_ATTR_NRANKS || key == MXP_ATTR_SM_FIRST ||
+            key == MXP_ATTR_SM_COUNT)
+            return MXP_ENOTSUP;
+        if (key == MXP_ATTR_STREAM) return mxp_chol_plan_set(p->group[0], key, v);
+        for (auto* c : p->group) {
+            const int rc = mxp_chol_plan_set(c, key, v);
+            if (rc != MXP_OK) return rc;
+        }
+        return MXP_OK;
+    }
     switch (key) {
     case MXP_ATTR_DEVICE:
         if (p->ws || p->streams_ready) return MXP_ESTATE;
@@ -1600,6 +1713,10 @@ int mxp_chol_plan_set(mxp_plan_t p, mxp_attr_t key, int64_t v) {
         else p->oz_slices = (int)v;
         p->list_uploaded = false;
         return MXP_OK;
+    case MXP_ATTR_OZ_PREFETCH:
+        if (v < 0 || v > 64) return -3;
+        p->oz_prefetch = (int)v;
+        return MXP_OK;
     case MXP_ATTR_COMPACT_POOL:
         if (v < 0 || v > 1) return -3;
         if (p->ws && !p->ws_owned) return MXP_ESTATE;  // changes the workspace layout
@@ -1627,6 +1744,7 @@ int mxp_chol_plan_set(mxp_plan_t p, mxp_attr_t key, int64_t v) {
 }
 
 int mxp_chol_sched_diagnostics(mxp_plan_t p, uint64_t* out, int64_t count, int64_t* written) {
+    if (is_group(p)) return mxp_chol_sched_diagnostics(p->group[0], out, count, written);
     if (!p) return -1;
     if (!out && count) return -2;
     int64_t n = std::min<int64_t>(count, (int64_t)p->h_stats.size());
@@ -1636,6 +1754,7 @@ int mxp_chol_sched_diagnostics(mxp_plan_t p, uint64_t* out, int64_t count, int64
 }
 
 int mxp_chol_timeline(mxp_plan_t p, double* ms, int64_t count, int64_t* written) {
+    if (is_group(p)) return mxp_chol_timeline(p->group[0], ms, count, written);
     if (!p) return -1;
     if (!ms && count > 0) return -2;
     if (count < 0) return -3;
@@ -1647,6 +1766,7 @@ int mxp_chol_timeline(mxp_plan_t p, double* ms, int64_t count, int64_t* written)
 }
 
 int mxp_chol_kernel_stats(mxp_plan_t p, int cls, int64_t* launches, double* ms, double* flops) {
+    if (is_group(p)) return mxp_chol_kernel_stats(p->group[0], cls, launches, ms, flops);
     if (!p) return -1;
     if (cls < 0 || cls > 3) return -2;
     if (launches) *launches = p->st_launch[cls];
@@ -1656,6 +1776,25 @@ int mxp_chol_kernel_stats(mxp_plan_t p, int cls, int64_t* launches, double* ms, 
 }
 
 int mxp_chol_plan_get(mxp_plan_t p, mxp_attr_t key, int64_t* v) {
+    if (is_group(p)) {
+        if (!v) return -3;
+        if (key == MXP_ATTR_GPU_LAUNCHES || key == MXP_ATTR_H2D_BYTES || key == MXP_ATTR_D2H_BYTES) {
+            int64_t sum = 0;
+            for (auto* c : p->group) {
+                int64_t x = 0;
+                const int rc = mxp_chol_plan_get(c, key, &x);
+                if (rc != MXP_OK) return rc;
+                sum += x;
+            }
+            *v = sum;
+            return MXP_OK;
+        }
+        if (key == MXP_ATTR_NRANKS) {
+            *v = (int64_t)p->group.size();
+            return MXP_OK;
+        }
+        return mxp_chol_plan_get(p->group[0], key, v);
+    }
     if (!p) return -1;
     if (!v) return -3;
     switch (key) {
@@ -1669,6 +1808,7 @@ int mxp_chol_plan_get(mxp_plan_t p, mxp_attr_t key, int64_t* v) {
     case MXP_ATTR_TC_ENGINE: *v = p->tc_engine; return MXP_OK;
     case MXP_ATTR_FP64_ENGINE: *v = p->fp64_engine; return MXP_OK;
     case MXP_ATTR_OZ_SLICES: *v = p->oz_slices; return MXP_OK;
+    case MXP_ATTR_OZ_PREFETCH: *v = p->oz_prefetch; return MXP_OK;
     case MXP_ATTR_COMPACT_POOL: *v = p->compact_attr; return MXP_OK;
     case MXP_ATTR_COMPACT_USED: plan_images(p); *v = p->compact ? 1 : 0; return MXP_OK;
     case MXP_ATTR_OZ_IMAGE_SLOTS: plan_images(p); *v = p->oz_ooc ? p->oz_img_slots : 0; return MXP_OK;
@@ -1698,6 +1838,7 @@ int mxp_chol_plan_get(mxp_plan_t p, mxp_attr_t key, int64_t* v) {
 }
 
 int mxp_chol_workspace_size(mxp_plan_t p, size_t* bytes) {
+    if (is_group(p)) return mxp_chol_workspace_size(p->group[0], bytes);
     if (!p) return -1;
     if (!bytes) return -2;
     *bytes = workspace_need(p);
@@ -1705,6 +1846,10 @@ int mxp_chol_workspace_size(mxp_plan_t p, size_t* bytes) {
 }
 
 int mxp_chol_set_workspace(mxp_plan_t p, void* dev, size_t bytes) {
+    if (is_group(p)) {
+        g_last_error = "not for a group plan (ngpus > 1): it attaches its GPUs itself";
+        return MXP_ENOTSUP;
+    }
     if (!p) return -1;
     if (!dev || ((uintptr_t)dev & 255)) return -2;
     if (bytes < workspace_need(p)) return -3;
@@ -1734,6 +1879,8 @@ int mxp_chol_factor_device(mxp_plan_t p, double* A, int64_t lda, int64_t* info) 
     if (!A) return -2;
     if (lda < p->n) return -3;
     if (!info) return -4;
+    if (is_group(p))  // every rank packs its tile rows of A (peer reads), rank 0 writes L back
+        return group_run(p, info, [&](mxp_plan_s* c, int64_t* inf) { return mxp_chol_factor_device(c, A, lda, inf); });
     p->have_result = false;
     p->launches = p->h2d = p->d2h = 0;
     int cur = 0;
@@ -1778,9 +1925,12 @@ int mxp_chol_factor_device(mxp_plan_t p, double* A, int64_t lda, int64_t* info) 
         finish_pushes(p, s0);
         {
             Prof pr(p, s0, MXP_KCLASS_OTHER, 0.0, 3);
-            launch_unpack_f64(A, lda, p->n, p->pool, p->d_slot, p->Nt, p->nb, 0, p->Nt, s0, decode_args(p));
+            if (!p->in_group || p->rank == 0) {  // (a group's ranks share A: rank 0 writes L back)
+                launch_unpack_f64(A, lda, p->n, p->pool, p->d_slot, p->Nt, p->nb, 0, p->Nt, s0, decode_args(p));
+                p->launches += 1;
+            }
             launch_logdet_final(p->d_logdet_parts, p->Nt, p->d_logdet, s0);
-            p->launches += 2;
+            p->launches += 1;
             dbg(p, s0, "unpack");
         }
         int64_t hinfo = 0;
@@ -1816,6 +1966,22 @@ int mxp_chol_factor(mxp_plan_t p, double* A_host, int64_t lda, int64_t* info) {
     if (!A_host) return -2;
     if (lda < p->n) return -3;
     if (!info) return -4;
+    if (is_group(p)) {  // every rank streams its own tile rows; A pinned once, for every GPU
+        cudaPointerAttributes attr{};
+        const size_t host_bytes = sizeof(double) * ((size_t)lda * (size_t)(p->n - 1) + (size_t)p->n);
+        bool reg = false;
+        if (!(cudaPointerGetAttributes(&attr, A_host) == cudaSuccess && attr.type == cudaMemoryTypeHost)) {
+            cudaGetLastError();
+            if (cudaHostRegister(A_host, host_bytes, cudaHostRegisterPortable) != cudaSuccess) {
+                cudaGetLastError();
+                return MXP_EHOSTPIN;
+            }
+            reg = true;
+        }
+        const int rc = group_run(p, info, [&](mxp_plan_s* c, int64_t* inf) { return mxp_chol_factor(c, A_host, lda, inf); });
+        if (reg) cudaHostUnregister(A_host);
+        return rc;
+    }
     // Host-resident path (Alg. 2): tiles stream host->device on a copy
     // stream in schedule order while the static schedule runs; each finished
     // tile streams back as soon as it is final (lower triangle only).
@@ -1949,6 +2115,8 @@ int mxp_chol_factor_tiles(mxp_plan_t p, void* const* tiles, double* scales, int6
     if (!tiles) return -2;
     if (!scales) return -3;
     if (!info) return -4;
+    if (is_group(p))
+        return group_run(p, info, [&](mxp_plan_s* c, int64_t* inf) { return mxp_chol_factor_tiles(c, tiles, scales, inf); });
     // tile-packed host storage (the C5 input): tiles below FP64 travel as their codes,
     // which needs the compact pool (native engine); an all-FP64 map works on every engine
     if (p->nranks > 1) {
@@ -2033,6 +2201,7 @@ int mxp_chol_factor_tiles(mxp_plan_t p, void* const* tiles, double* scales, int6
 }
 
 int mxp_chol_logdet(mxp_plan_t p, double* logdet) {
+    if (is_group(p)) return mxp_chol_logdet(p->group[0], logdet);
     if (!p) return -1;
     if (!logdet) return -2;
     if (!p->have_result) return MXP_ESTATE;
@@ -2180,6 +2349,10 @@ int mxp_chol_factor_matern(mxp_plan_t p, const double* xy_dev, double sigma2, do
     if (!(range_a > 0.0)) return -4;
     if (!(nugget >= 0.0)) return -5;
     if (!info) return -6;
+    if (is_group(p))
+        return group_run(p, info, [&](mxp_plan_s* c, int64_t* inf) {
+            return mxp_chol_factor_matern(c, xy_dev, sigma2, range_a, nugget, inf);
+        });
     p->have_result = false;
     p->launches = p->h2d = p->d2h = 0;
     int cur = 0;
@@ -2243,6 +2416,7 @@ int mxp_chol_factor_matern(mxp_plan_t p, const double* xy_dev, double sigma2, do
 }
 
 int mxp_chol_describe(mxp_plan_t p, int streaming, int64_t* counts) {
+    if (is_group(p)) return mxp_chol_describe(p->group[0], streaming, counts);
     if (!p) return -1;
     if (!counts) return -3;
     const bool saved = p->host_mode;
@@ -2260,6 +2434,10 @@ int mxp_chol_describe(mxp_plan_t p, int streaming, int64_t* counts) {
 }
 
 int mxp_chol_ipc_handle(mxp_plan_t p, void* handle_out, uint64_t* ws_bytes) {
+    if (is_group(p)) {
+        g_last_error = "not for a group plan (ngpus > 1): it attaches its GPUs itself";
+        return MXP_ENOTSUP;
+    }
     if (!p) return -1;
     if (!handle_out) return -2;
     if (!ws_bytes) return -3;
@@ -2283,6 +2461,10 @@ int mxp_chol_ipc_handle(mxp_plan_t p, void* handle_out, uint64_t* ws_bytes) {
 }
 
 int mxp_chol_ipc_attach(mxp_plan_t p, int peer_rank, const void* handle, uint64_t ws_bytes) {
+    if (is_group(p)) {
+        g_last_error = "not for a group plan (ngpus > 1): it attaches its GPUs itself";
+        return MXP_ENOTSUP;
+    }
     if (!p) return -1;
     if (peer_rank < 0 || peer_rank >= p->nranks || peer_rank == p->rank) return -2;
     if (!handle) return -3;
@@ -2312,6 +2494,10 @@ int mxp_chol_ipc_attach(mxp_plan_t p, int peer_rank, const void* handle, uint64_
 }
 
 int mxp_chol_attach_peer_plan(mxp_plan_t p, int peer_rank, mxp_plan_t peer) {
+    if (is_group(p) || is_group(peer)) {
+        g_last_error = "not for a group plan (ngpus > 1): it attaches its GPUs itself";
+        return MXP_ENOTSUP;
+    }
     if (!p) return -1;
     if (peer_rank < 0 || peer_rank >= p->nranks || peer_rank == p->rank) return -2;
     if (!peer || peer == p) return -3;
@@ -2344,6 +2530,7 @@ int mxp_chol_attach_peer_plan(mxp_plan_t p, int peer_rank, mxp_plan_t peer) {
 }
 
 int mxp_chol_get_factor_device(mxp_plan_t p, double* L_dev, int64_t ldl) {
+    if (is_group(p)) return mxp_chol_get_factor_device(p->group[0], L_dev, ldl);
     if (!p) return -1;
     if (!L_dev) return -2;
     if (ldl < p->n) return -3;
@@ -2366,6 +2553,7 @@ int mxp_chol_get_factor_device(mxp_plan_t p, double* L_dev, int64_t ldl) {
 }
 
 int mxp_chol_solve_lower(mxp_plan_t p, const double* y_dev, double* z_dev, double* sumsq) {
+    if (is_group(p)) return mxp_chol_solve_lower(p->group[0], y_dev, z_dev, sumsq);
     if (!p) return -1;
     if (!y_dev) return -2;
     if (!p->have_result) return MXP_ESTATE;
@@ -2398,6 +2586,7 @@ int mxp_chol_solve_lower(mxp_plan_t p, const double* y_dev, double* z_dev, doubl
 }
 
 int mxp_chol_loglik(mxp_plan_t p, const double* y_dev, double* loglik) {
+    if (is_group(p)) return mxp_chol_loglik(p->group[0], y_dev, loglik);
     if (!p) return -1;
     if (!loglik) return -3;
     if (!p->have_result) return MXP_ESTATE;
@@ -2412,6 +2601,7 @@ int mxp_chol_loglik(mxp_plan_t p, const double* y_dev, double* loglik) {
 }
 
 int mxp_chol_tile_device_ptr(mxp_plan_t p, int64_t i, int64_t j, double** ptr) {
+    if (is_group(p)) return mxp_chol_tile_device_ptr(p->group[0], i, j, ptr);
     if (!p) return -1;
     if (i < 0 || i >= p->Nt) return -2;
     if (j < 0 || j > i) return -3;

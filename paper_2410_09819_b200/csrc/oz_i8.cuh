@@ -200,7 +200,7 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int* v) {
 // precomputed descriptors).
 template <int S, class Src>
 __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles, int kt, int64_t nb, uint8_t* smem,
-                             uint32_t tmem) {
+                             uint32_t tmem, int pf) {
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * STAGE_BYTES);
     uint64_t* done = full + STAGES;
@@ -218,11 +218,28 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
     // producer (warp 0): copies of K step g into its stage
     OzTile cur{};
     int cur_i = -1;
+    // L2 prefetch of K step g + pf (pf > 0): the operand chunks that miss L2 (~25 % of the
+    // sectors at C2) then wait one DRAM latency less than the 3-stage smem ring can hide
+    OzTile pcur{};
+    int pcur_i = -1;
     auto issue = [&](int g) {
         const int i = g / kt, kc = g - i * kt;
         if (i != cur_i) cur = src(i), cur_i = i;
         uint8_t* st = base + (g % STAGES) * STAGE_BYTES;
         uint64_t* fb = full + (g % STAGES);
+        const int gp = g + pf;
+        if (pf > 0 && gp < G) {
+            const int ip = gp / kt, kp = gp - ip * kt;
+            if (ip != pcur_i) pcur = src(ip), pcur_i = ip;
+            if (elect_one()) {
+#pragma unroll
+                for (int t = 0; t < S; ++t) {
+                    tc::bulk_prefetch_l2(pcur.a + t * sstride + (int64_t)kp * CHUNK, CHUNK);
+                    tc::bulk_prefetch_l2(pcur.b + t * sstride + (int64_t)kp * CHUNK, CHUNK_B);
+                }
+            }
+            __syncwarp();
+        }
         if (elect_one()) {
             tc::mbar_expect_tx(fb, (uint32_t)(S * (CHUNK + CHUNK_B)));
 #pragma unroll
@@ -329,13 +346,13 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
 constexpr int MIN_S = 4;  // slices supported by the compiled variants: MIN_S..MAX_S
 template <class Src>
 __device__ __forceinline__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, int s, int kt,
-                                           int64_t nb, uint8_t* smem, uint32_t tmem) {
+                                           int64_t nb, uint8_t* smem, uint32_t tmem, int pf) {
     switch (s) {
-    case 4: block_gemm_t<4>(C, ldc, src, ntiles, kt, nb, smem, tmem); break;
-    case 5: block_gemm_t<5>(C, ldc, src, ntiles, kt, nb, smem, tmem); break;
-    case 6: block_gemm_t<6>(C, ldc, src, ntiles, kt, nb, smem, tmem); break;
-    case 7: block_gemm_t<7>(C, ldc, src, ntiles, kt, nb, smem, tmem); break;
-    default: block_gemm_t<8>(C, ldc, src, ntiles, kt, nb, smem, tmem); break;
+    case 4: block_gemm_t<4>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf); break;
+    case 5: block_gemm_t<5>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf); break;
+    case 6: block_gemm_t<6>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf); break;
+    case 7: block_gemm_t<7>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf); break;
+    default: block_gemm_t<8>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf); break;
     }
 }
 

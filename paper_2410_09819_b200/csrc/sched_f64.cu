@@ -561,7 +561,7 @@ __device__ __noinline__ bool task_gemm_oz(const SchedArgs& a, int64_t m, int64_t
         return o;
     };
     double* Ct = tile_ptr(a.pool, a.slot, Nt, nb, m, k) + bi * 128 + bj * 64 * nb;
-    oz::block_gemm(Ct, nb, src, (int)(n1 - n0), s, (int)(nb / 32), nb, smem, tmem);
+    oz::block_gemm(Ct, nb, src, (int)(n1 - n0), s, (int)(nb / 32), nb, smem, tmem, a.oz_prefetch);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {

@@ -57,7 +57,15 @@ def test_argument_validation_without_gpu(mxp):
     h = ctypes.c_void_p()
     assert lib.mxp_chol_plan(0, 256, None, 1, ctypes.byref(h)) == -1
     assert lib.mxp_chol_plan(1024, 100, None, 1, ctypes.byref(h)) == -2
-    assert lib.mxp_chol_plan(1024, 256, None, 2, ctypes.byref(h)) == -4
+    assert lib.mxp_chol_plan(1024, 256, None, 0, ctypes.byref(h)) == -4
+    assert lib.mxp_chol_plan(1024, 256, None, 9, ctypes.byref(h)) == -4  # ngpus <= 8
+    import torch
+    g = ctypes.c_void_p()  # a group plan (ngpus > 1) needs a CUDA device to place its ranks
+    rc = lib.mxp_chol_plan(1024, 256, None, 2, ctypes.byref(g))
+    assert rc == (0 if torch.cuda.is_available() else -1001)
+    if rc == 0:
+        assert lib.mxp_chol_plan_set(g, 8, 1) == -1005  # MXP_ATTR_RANK: the group places its ranks
+        lib.mxp_chol_plan_destroy(g)
     bad = (ctypes.c_uint8 * 10)(*([1] + [0] * 9))  # FP32 diagonal tile -> invalid map
     assert lib.mxp_chol_plan(1024, 256, bad, 1, ctypes.byref(h)) == -3
     assert lib.mxp_chol_plan(1024, 256, None, 1, ctypes.byref(h)) == 0

@@ -18,7 +18,7 @@ def _ranks(n, nb, P, pmap=None, attrs=None):
     for pl in plans:  # (before attaching: attributes that re-size the workspace come first)
         for k, v in (attrs or {}).items():
             pl.set(k, v)
-    share = 148 // P
+    share = 147 // P  # one SM outside the partitions for same-GPU copy kernels (engine.cu group plans)
     for r, pl in enumerate(plans):
         pl.set("rank", r)
         pl.set("nranks", P)
@@ -174,3 +174,55 @@ def test_ranks_host_path_not_pd_large_nt():
     plans = _ranks(n, nb, P)
     res = _run(plans, lambda r, pl: pl.factor(Hs[r].T, stream_from_torch=False))
     assert res == [11, 11]
+
+
+# ---- group plans: mxp_chol_plan(..., ngpus > 1) runs every rank itself (one host
+# thread per rank, in-process peer pools); on this one-GPU box the ranks share the
+# device and split its SMs, the same code path as on several GPUs.
+@pytest.mark.parametrize("P", [2, 3])
+def test_group_plan_device_path_bitwise_equal_single(P):
+    import paper_2410_09819_b200 as m
+    from gpu_util import gpu_factor
+    n, nb = 2048, 256
+    A = w.plgsy(n, seed=17)
+    L1, info1, ld1, _ = gpu_factor(A, nb)
+    plan = m.Plan(n, nb, ngpus=P)
+    assert plan.get("nranks") == P
+    L, info, ld, _ = gpu_factor(A, nb, plan=plan)
+    assert info1 == info == 0
+    assert np.array_equal(L, L1) and ld == ld1
+    # repeat on the same group (epochs, re-attached peers)
+    L2, info2, ld2, _ = gpu_factor(A, nb, plan=plan)
+    assert info2 == 0 and np.array_equal(L2, L1) and ld2 == ld1
+
+
+def test_group_plan_host_path_and_not_pd():
+    import paper_2410_09819_b200 as m
+    from gpu_util import gpu_factor
+    n, nb = 3000, 256
+    A = w.plgsy(n, seed=23)
+    L1, _, ld1, _ = gpu_factor(A, nb, host=True)
+    plan = m.Plan(n, nb, ngpus=2)
+    L, info, ld, plan = gpu_factor(A, nb, host=True, plan=plan)
+    assert info == 0 and np.array_equal(L, L1) and ld == ld1
+    Nt = -(-n // nb)  # the ranks together stream the lower triangle once
+    assert plan.get("h2d_bytes") == 8 * sum(min(nb, n - i * nb) * min(nb, n - j * nb)
+                                            for j in range(Nt) for i in range(j, Nt))
+    B = A.copy()
+    B[1700, 1700] = -1.0
+    _, info, _, _ = gpu_factor(B, nb, host=True, plan=m.Plan(n, nb, ngpus=2))
+    Lo, oinfo = oracle.factor(B, nb)
+    assert info == oinfo == 1701
+
+
+def test_group_plan_generated_matern_logdet():
+    import torch
+
+    import paper_2410_09819_b200 as m
+    n, nb = 4096, 256
+    xy = torch.tensor(w.matern_locations(n, seed=1), device="cuda")
+    p1 = m.Plan(n, nb)
+    assert p1.factor_matern(xy, 1.0, 0.078809) == 0
+    pg = m.Plan(n, nb, ngpus=2)
+    assert pg.factor_matern(xy, 1.0, 0.078809) == 0
+    assert pg.logdet() == p1.logdet()
