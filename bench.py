@@ -284,6 +284,26 @@ def mxp_roofline(F, peaks):
     return sum(F.values()) / T / 1e12, T
 
 
+def ooc_variant_ledgers(m, n, nb, lower, fracs, h2d_measured, d2h_measured, streams=4):
+    """N3 (Alg. 3): host-link bytes of the paper's
+    OOC variants replayed over the same static task sequence with HBM for `frac` of the lower
+    triangle (mxp_ooc_variant_volume; 4 streams), beside the engine's own measured ledger."""
+    out = {"how": "mxp_ooc_variant_volume: Alg. 2's tasks dealt to 4 streams, a tile cache of frac x the "
+                  "lower triangle; sync/async/V1 have no cache, V2 = LRU cache table (remove_steal), V3 = V2 + "
+                  "L_kk pinned until the last TRSM of its column, static = this engine's dead-tile plan, MIN = "
+                  "Belady's optimal eviction; bytes are FP64 tiles (replayed ledgers, not executed variants)",
+           "engine_measured": {"h2d_bytes": h2d_measured, "d2h_bytes": d2h_measured}}
+    for frac in fracs:
+        row = {}
+        for v in ("sync", "async", "V1", "V2", "V3", "static", "MIN"):
+            r = m.ooc_variant_volume(n, nb, v, int(frac * lower), streams)
+            row[v] = None if r is None else {"h2d_gb": round(r["h2d_bytes"] / 1e9, 2),
+                                             "d2h_gb": round(r["d2h_bytes"] / 1e9, 2),
+                                             "total_over_lower": round((r["h2d_bytes"] + r["d2h_bytes"]) / lower, 3)}
+        out[f"hbm_{frac:.2f}_of_lower"] = row
+    return out
+
+
 def ooc_timeline_summary(tl, t_total):
     """The paper's Fig. 7 rows (C2G, G2C, Work) as per-column event times of a
     profiled out-of-core run, plus what they say about overlap: a column's loads finishing
@@ -871,6 +891,7 @@ def run_ours(args):
                                    **x_oc),
                "ooc_over_in_core": t_in / t_oc,
                "ooc_over_c2_device_in_core": (fl / t_oc / 1e12) / value,
+               "variants": ooc_variant_ledgers(m, no, nbo, lower, [args.ooc_frac, 0.35], hb_oc, db_oc),
                "timeline": ooc_timeline_summary(x_pr.get("timeline"), t_pr),
                "note": "C4 (n=262144, 276 GB lower triangle) exceeds this box's 196 GB host RAM; the same "
                        "streaming/recycling path is timed with the pool capped below the lower triangle"}

@@ -691,7 +691,7 @@ Layout layout(const mxp_plan_s* p) {
     L.wbuf = off;
     off += align_up(sizeof(double) * (size_t)p->Nt * p->nb * 128, 256);
     L.stats = off;
-    off += align_up(sizeof(unsigned long long) * (size_t)(16 + 3 * p->Nt), 256);
+    off += align_up(sizeof(unsigned long long) * (size_t)(STAT_POTRF + 3 * p->Nt), 256);
     L.prec = off;
     off += align_up((size_t)p->T, 256);
     L.amax_s = off;
@@ -1211,7 +1211,7 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     for (int q = 0; q < MAX_RANKS; ++q)
         a.peer_dinfo[q] = (q != p->rank && q < p->nranks && p->peer_ws[q]) ? (int64_t*)p->peer_ws[q] : nullptr;
     a.stats = nullptr;
-    const size_t nstat = 16 + 3 * (size_t)Nt;
+    const size_t nstat = STAT_POTRF + 3 * (size_t)Nt;
     if (p->profile) {
         std::vector<unsigned long long> init(nstat, 0ull);
         init[STAT_T0] = ~0ull;
@@ -1946,7 +1946,7 @@ int mxp_chol_factor_device(mxp_plan_t p, double* A, int64_t lda, int64_t* info) 
         }
         prof_collect(p);
         if (p->profile) {
-            p->h_stats.resize(16 + 3 * (size_t)p->Nt);
+            p->h_stats.resize(STAT_POTRF + 3 * (size_t)p->Nt);
             CK(cudaMemcpy(p->h_stats.data(), p->d_stats, sizeof(unsigned long long) * p->h_stats.size(),
                           cudaMemcpyDeviceToHost));
         }
@@ -2093,7 +2093,7 @@ int mxp_chol_factor(mxp_plan_t p, double* A_host, int64_t lda, int64_t* info) {
         CK(cudaStreamSynchronize(s0));
         prof_collect(p);
         if (p->profile) {
-            p->h_stats.resize(16 + 3 * (size_t)p->Nt);
+            p->h_stats.resize(STAT_POTRF + 3 * (size_t)p->Nt);
             CK(cudaMemcpy(p->h_stats.data(), p->d_stats, sizeof(unsigned long long) * p->h_stats.size(),
                           cudaMemcpyDeviceToHost));
         }
@@ -2400,7 +2400,7 @@ int mxp_chol_factor_matern(mxp_plan_t p, const double* xy_dev, double sigma2, do
         }
         prof_collect(p);
         if (p->profile) {
-            p->h_stats.resize(16 + 3 * (size_t)p->Nt);
+            p->h_stats.resize(STAT_POTRF + 3 * (size_t)p->Nt);
             CK(cudaMemcpy(p->h_stats.data(), p->d_stats, sizeof(unsigned long long) * p->h_stats.size(),
                           cudaMemcpyDeviceToHost));
         }

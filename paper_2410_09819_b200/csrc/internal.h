@@ -123,7 +123,12 @@ enum {
     // POTRF phases (ns summed over columns): block-column update, unblocked
     // factor, W_J inverse (+ write-back), in-tile TRSM
     STAT_PF_UPD = 9, STAT_PF_CHOL = 10, STAT_PF_INV = 11, STAT_PF_TRSM = 12,
-    STAT_POTRF = 16  // + 3k: kernel start, wait done, end
+    // Ozaki GEMM tasks (k_tc): the issuing thread's waits for operand stages (full) and for
+    // MMA completion before refills (done), and the per-tile drains (tile MMAs end -> fp64)
+    STAT_OZ_FULL = 13, STAT_OZ_DONE = 14, STAT_OZ_DRAIN = 15,
+    // busy ns of the GEMM tasks by output precision (FP64, FP32, FP16, FP8) and their counts
+    STAT_GEMM_P = 16, STAT_GEMM_PN = 20,
+    STAT_POTRF = 24  // + 3k: kernel start, wait done, end
 };
 int sched_ctas_per_sm();
 // load every kernel of the library eagerly (one call per file; see preload_sched)

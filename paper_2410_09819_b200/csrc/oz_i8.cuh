@@ -198,9 +198,16 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int* v) {
 // All 128 threads call; thread 0 issues the bulk copies and the MMAs (S
 // compile-time: the S(S+1)/2 MMAs of a K step are straight-line code on
 // precomputed descriptors).
+__device__ __forceinline__ uint64_t oz_clock() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// stats (MXP_ATTR_PROFILE): [STAT_OZ_FULL], [STAT_OZ_DONE], [STAT_OZ_DRAIN] in ns, or nullptr
 template <int S, class Src>
 __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles, int kt, int64_t nb, uint8_t* smem,
-                             uint32_t tmem, int pf) {
+                             uint32_t tmem, int pf, unsigned long long* stats) {
+    uint64_t t_full = 0, t_done = 0, t_drain = 0;
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * STAGE_BYTES);
     uint64_t* done = full + STAGES;
@@ -267,7 +274,9 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
             __syncwarp();
             for (int kc = 0; kc < kt; ++kc) {
                 const int g = i * kt + kc, stage = g % STAGES;
+                const uint64_t w0 = stats ? oz_clock() : 0;
                 tc::mbar_wait(full + stage, (uint32_t)((g / STAGES) & 1));
+                if (stats) t_full += oz_clock() - w0;
                 tc::fence_after();
                 const uint32_t sa = tc::smem_u32(base + stage * STAGE_BYTES);
                 const uint64_t ad0 = make_desc(sa), bd0 = make_desc(sa + MAX_S * CHUNK);
@@ -293,7 +302,9 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
                 // (this step's MMAs stay queued behind them meanwhile)
                 if (g >= 1 && g - 1 + STAGES < G) {
                     const int pg = g - 1;
+                    const uint64_t w1 = stats ? oz_clock() : 0;
                     tc::mbar_wait(done + (pg % STAGES), (uint32_t)((pg / STAGES) & 1));
+                    if (stats) t_done += oz_clock() - w1;
                     issue(pg + STAGES);
                 }
             }
@@ -303,6 +314,7 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
         // drain: ACC levels of tile i -> fp64, scaled by the row scales
         // (threads 0..127 = TMEM lanes; in k_tc warp 4 only join the barriers)
         const bool wk = tid < 128;
+        const uint64_t d0 = (stats && tid == 0) ? oz_clock() : 0;
         if (tid < BN) s_sb[tid] = __ldcg(src(i).sb + tid);
         const double sa_r = wk ? __ldcg(src(i).sa + tid) : 0.0;
         if (wk) tc::mbar_wait(tbar, (uint32_t)(i & 1));
@@ -328,6 +340,12 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
         }
         tc::fence_before();
         __syncthreads();  // TMEM and s_sb free for tile i + 1
+        if (stats && tid == 0) t_drain += oz_clock() - d0;
+    }
+    if (stats && tid == 0) {
+        atomicAdd(stats + STAT_OZ_FULL, (unsigned long long)t_full);
+        atomicAdd(stats + STAT_OZ_DONE, (unsigned long long)t_done);
+        atomicAdd(stats + STAT_OZ_DRAIN, (unsigned long long)t_drain);
     }
     if (tid < 128) {
 #pragma unroll
@@ -346,13 +364,14 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
 constexpr int MIN_S = 4;  // slices supported by the compiled variants: MIN_S..MAX_S
 template <class Src>
 __device__ __forceinline__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, int s, int kt,
-                                           int64_t nb, uint8_t* smem, uint32_t tmem, int pf) {
+                                           int64_t nb, uint8_t* smem, uint32_t tmem, int pf,
+                                           unsigned long long* stats) {
     switch (s) {
-    case 4: block_gemm_t<4>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf); break;
-    case 5: block_gemm_t<5>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf); break;
-    case 6: block_gemm_t<6>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf); break;
-    case 7: block_gemm_t<7>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf); break;
-    default: block_gemm_t<8>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf); break;
+    case 4: block_gemm_t<4>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats); break;
+    case 5: block_gemm_t<5>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats); break;
+    case 6: block_gemm_t<6>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats); break;
+    case 7: block_gemm_t<7>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats); break;
+    default: block_gemm_t<8>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats); break;
     }
 }
 

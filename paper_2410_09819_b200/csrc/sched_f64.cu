@@ -127,6 +127,15 @@ struct CastPost {
 
 // ---------------------------------------------------------------- GEMM task
 // C(m,k)[block b] -= sum_{n in chunk c} A(m,n)[rows] A(k,n)[cols]^T
+// GEMM task busy time, in total and by the output tile's precision (MXP_ATTR_PROFILE)
+__device__ __forceinline__ void gemm_busy(const SchedArgs& a, int64_t t, uint64_t tw0) {
+    const unsigned long long dt = globaltimer() - tw0;
+    atomicAdd(a.stats + STAT_GEMM_BUSY, dt);
+    const int p = a.prec ? a.prec[t] : P_FP64;
+    atomicAdd(a.stats + STAT_GEMM_P + p, dt);
+    atomicAdd(a.stats + STAT_GEMM_PN + p, 1ull);
+}
+
 template <bool CAST>
 __device__ __forceinline__ bool task_gemm(const SchedArgs& a, int64_t m, int64_t k, int64_t b, int64_t c, double* smem,
                           int* s_flag) {
@@ -208,7 +217,7 @@ __device__ __forceinline__ bool task_gemm(const SchedArgs& a, int64_t m, int64_t
         st_release(chunk_flag, (int)c + 1);
         atom_add_release(a.gemm_done + t, 1);
         if (a.stats) {
-            atomicAdd(a.stats + STAT_GEMM_BUSY, globaltimer() - tw0);
+            gemm_busy(a, t, tw0);
             atomicAdd(a.stats + STAT_GEMM_N, 1ull);
         }
     }
@@ -380,7 +389,7 @@ __device__ __noinline__ bool task_gemm_tc(const SchedArgs& a, int64_t m, int64_t
         st_release(chunk_flag, (int)c + 1);
         atom_add_release(a.gemm_done + t, 1);
         if (a.stats) {
-            atomicAdd(a.stats + STAT_GEMM_BUSY, globaltimer() - tw0);
+            gemm_busy(a, t, tw0);
             atomicAdd(a.stats + STAT_GEMM_N, 1ull);
         }
     }
@@ -450,7 +459,7 @@ __device__ __noinline__ bool task_gemm_img(const SchedArgs& a, int64_t m, int64_
         st_release(chunk_flag, (int)c + 1);
         atom_add_release(a.gemm_done + t, 1);
         if (a.stats) {
-            atomicAdd(a.stats + STAT_GEMM_BUSY, globaltimer() - tw0);
+            gemm_busy(a, t, tw0);
             atomicAdd(a.stats + STAT_GEMM_N, 1ull);
         }
     }
@@ -511,7 +520,7 @@ __device__ __noinline__ bool task_gemm_nat(const SchedArgs& a, int64_t m, int64_
         st_release(chunk_flag, (int)c + 1);
         atom_add_release(a.gemm_done + t, 1);
         if (a.stats) {
-            atomicAdd(a.stats + STAT_GEMM_BUSY, globaltimer() - tw0);
+            gemm_busy(a, t, tw0);
             atomicAdd(a.stats + STAT_GEMM_N, 1ull);
         }
     }
@@ -561,14 +570,14 @@ __device__ __noinline__ bool task_gemm_oz(const SchedArgs& a, int64_t m, int64_t
         return o;
     };
     double* Ct = tile_ptr(a.pool, a.slot, Nt, nb, m, k) + bi * 128 + bj * 64 * nb;
-    oz::block_gemm(Ct, nb, src, (int)(n1 - n0), s, (int)(nb / 32), nb, smem, tmem, a.oz_prefetch);
+    oz::block_gemm(Ct, nb, src, (int)(n1 - n0), s, (int)(nb / 32), nb, smem, tmem, a.oz_prefetch, a.stats);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
         st_release(chunk_flag, (int)c + 1);
         atom_add_release(a.gemm_done + t, 1);
         if (a.stats) {
-            atomicAdd(a.stats + STAT_GEMM_BUSY, globaltimer() - tw0);
+            gemm_busy(a, t, tw0);
             atomicAdd(a.stats + STAT_GEMM_N, 1ull);
         }
     }

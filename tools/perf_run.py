@@ -15,6 +15,21 @@ import paper_2410_09819_b200 as m  # noqa: E402
 import workloads as w  # noqa: E402
 
 
+def report(plan):
+    if os.environ.get("PROFILE") != "1":
+        return
+    d = plan.sched_diagnostics()
+    d.pop("potrf_timeline_ms", None)
+    ctas = max(1, d.get("ctas", 1))
+    print("sched:", {k: (round(v, 1) if isinstance(v, float) else v) for k, v in d.items()})
+    print("per-CTA ms: gemm busy %.1f wait %.1f, trsm busy %.1f wait %.1f" % (
+        d["gemm_busy_ms"] / ctas, d["gemm_wait_ms"] / ctas, d["trsm_busy_ms"] / ctas, d["trsm_wait_ms"] / ctas))
+    print("ozaki loop ms per CTA:", {k: round(v / ctas, 1) for k, v in d["ozaki_ms"].items()})
+    print("gemm busy ms per CTA by precision:", {k: round(v / ctas, 1) for k, v in d["gemm_busy_ms_by_precision"].items()},
+          "tasks:", d["gemm_tasks_by_precision"])
+    print("kernels:", plan.kernel_stats())
+
+
 def main():
     mode = sys.argv[1]
     reps = int(os.environ.get("REPS", "1"))
@@ -26,6 +41,7 @@ def main():
         m.generate_plgsy_device(A0, seed=42)
         A = torch.empty_like(A0)
         plan = m.Plan(n, nb)
+        plan.set("profile", int(os.environ.get("PROFILE", "0")))
         plan.set("fp64_engine", int(os.environ.get("ENGINE", "1")))
         if "OZ_PF" in os.environ:
             plan.set("oz_prefetch", int(os.environ["OZ_PF"]))
@@ -37,6 +53,7 @@ def main():
             torch.cuda.synchronize()
         print(f"c2 n={n} nb={nb} info={info} ms={ev0.elapsed_time(ev1):.1f} "
               f"TF/s={n ** 3 / 3 / ev0.elapsed_time(ev1) / 1e9:.2f} engine={plan.get('fp64_engine_used')}")
+        report(plan)
     else:
         n = int(sys.argv[2]) if len(sys.argv) > 2 else 32768
         eps = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-5
@@ -45,6 +62,7 @@ def main():
         xy = torch.tensor(w.matern_locations(n, seed=1), device="cuda")
         pmap, _ = m.precision_map_matern_device(xy, nb, eps, 1.0, a)
         plan = m.Plan(n, nb, pmap)
+        plan.set("profile", int(os.environ.get("PROFILE", "0")))
         plan.set("fp64_engine", 1)
         for r in range(reps):
             ev0.record()
@@ -53,6 +71,7 @@ def main():
             torch.cuda.synchronize()
         print(f"mxp n={n} eps={eps} info={info} ms={ev0.elapsed_time(ev1):.1f} "
               f"TF/s={n ** 3 / 3 / ev0.elapsed_time(ev1) / 1e9:.2f} tc_engine={plan.get('tc_engine_used')}")
+        report(plan)
 
 
 if __name__ == "__main__":
