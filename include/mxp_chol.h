@@ -386,11 +386,12 @@ int mxp_ooc_variant_volume(int64_t n, int64_t nb, int variant, int streams, int6
  * [2] TRSM busy, [3] TRSM wait, [4] #GEMM tasks, [5] #TRSM tasks, [6] first
  * CTA start, [7] last CTA end, [8] #CTAs that ran tasks, [9..12] POTRF phases, [13..15]
  * Ozaki GEMM loop (stage waits, MMA-completion waits, per-tile drains), [16..19] GEMM busy
- * by output precision (FP64, FP32, FP16, FP8), [20..23] their task counts; then for each
- * column k at [24+3k]: POTRF kernel start, Ready-wait done, end.
+ * by output precision (FP64, FP32, FP16, FP8), [20..23] their task counts, [24..26] Ozaki
+ * issuing thread in MMA issue, bulk-copy issue, whole K loop; then for each column k at
+ * [28+3k]: POTRF kernel start, Ready-wait done, end.
  *   out      host array of `count` entries (may be NULL when count = 0) (arg 2)
  *   count    capacity of out                                           (arg 3)
- *   written  receives the number of entries available (24 + 3 Nt)       (arg 4)
+ *   written  receives the number of entries available (28 + 3 Nt)       (arg 4)
  */
 int mxp_chol_sched_diagnostics(mxp_plan_t plan, uint64_t* out, int64_t count, int64_t* written);
 

@@ -128,7 +128,9 @@ enum {
     STAT_OZ_FULL = 13, STAT_OZ_DONE = 14, STAT_OZ_DRAIN = 15,
     // busy ns of the GEMM tasks by output precision (FP64, FP32, FP16, FP8) and their counts
     STAT_GEMM_P = 16, STAT_GEMM_PN = 20,
-    STAT_POTRF = 24  // + 3k: kernel start, wait done, end
+    // Ozaki GEMM loop: time of the issuing thread in MMA issue, in bulk-copy issue, and in the loop
+    STAT_OZ_MMA = 24, STAT_OZ_COPY = 25, STAT_OZ_LOOP = 26,
+    STAT_POTRF = 28  // + 3k: kernel start, wait done, end
 };
 int sched_ctas_per_sm();
 // load every kernel of the library eagerly (one call per file; see preload_sched)

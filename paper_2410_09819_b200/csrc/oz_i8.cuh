@@ -207,7 +207,7 @@ __device__ __forceinline__ uint64_t oz_clock() {
 template <int S, class Src>
 __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles, int kt, int64_t nb, uint8_t* smem,
                              uint32_t tmem, int pf, unsigned long long* stats) {
-    uint64_t t_full = 0, t_done = 0, t_drain = 0;
+    uint64_t t_full = 0, t_done = 0, t_drain = 0, t_mma = 0, t_copy = 0, t_loop = 0;
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * STAGE_BYTES);
     uint64_t* done = full + STAGES;
@@ -230,6 +230,7 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
     OzTile pcur{};
     int pcur_i = -1;
     auto issue = [&](int g) {
+        const uint64_t c0 = stats ? oz_clock() : 0;
         const int i = g / kt, kc = g - i * kt;
         if (i != cur_i) cur = src(i), cur_i = i;
         uint8_t* st = base + (g % STAGES) * STAGE_BYTES;
@@ -257,9 +258,15 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
             }
         }
         __syncwarp();
+        if (stats) t_copy += oz_clock() - c0;
     };
+    // Warp-specialized: warp 1 produces (bulk copies into the ring, refilling a
+    // stage once the MMAs that read it have completed), warp 0 issues the MMAs;
+    // one elected lane each.  (A single thread doing both spent ~650 cycles per
+    // 32-K step issuing the 10 MMAs and ~630 issuing the 14 copies: more than
+    // the ~900 cycles of tensor work they feed -- measured, DESIGN 5.7.)
     const int warp = tid >> 5;
-    if (warp == 0) {  // warp 0 (converged) drives the copies and MMAs; one elected lane issues them
+    if (warp == 1) {
         __syncwarp();
         for (int g = 0; g < STAGES && g < G; ++g) issue(g);
     }
@@ -272,6 +279,7 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
     for (int i = 0; i < ntiles; ++i) {
         if (warp == 0) {
             __syncwarp();
+            const uint64_t l0 = stats ? oz_clock() : 0;
             for (int kc = 0; kc < kt; ++kc) {
                 const int g = i * kt + kc, stage = g % STAGES;
                 const uint64_t w0 = stats ? oz_clock() : 0;
@@ -281,25 +289,36 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
                 const uint32_t sa = tc::smem_u32(base + stage * STAGE_BYTES);
                 const uint64_t ad0 = make_desc(sa), bd0 = make_desc(sa + MAX_S * CHUNK);
                 const uint32_t acc0 = kc > 0 ? 1u : 0u;
+                const uint64_t m0 = stats ? oz_clock() : 0;
                 // A slice t meets B slices u = 0 .. S-1-t, i.e. levels t .. S-1.  The B
                 // slices sit 2 KB apart in smem (64 rows each): B slices u0 .. u0+m-1
                 // stacked are ONE K-major operand of N = 64 m rows, and its product
                 // lands in the m consecutive level accumulators (t+u0) .. (t+u0+m-1)
                 // -- so each A slice needs ceil((S-t)/4) MMAs of N <= 256 instead of
                 // S-t MMAs of N = 64 (12 instead of 36 for S = 8; A read 12x, not 36x).
+                if (elect_one()) {
 #pragma unroll
-                for (int t = 0; t < S; ++t)
+                    for (int t = 0; t < S; ++t)
 #pragma unroll
-                    for (int u0 = 0; u0 + t < S; u0 += 4) {
-                        const int m = (S - t - u0) < 4 ? (S - t - u0) : 4;
-                        if (elect_one())
+                        for (int u0 = 0; u0 + t < S; u0 += 4) {
+                            const int m = (S - t - u0) < 4 ? (S - t - u0) : 4;
                             mma_i8(tmem + (uint32_t)((t + u0) * BN), ad0 + (uint64_t)(t * (CHUNK >> 4)),
                                    bd0 + (uint64_t)(u0 * (CHUNK_B >> 4)), idesc_i8(BN * m), t > 0 ? 1u : acc0);
-                    }
-                if (elect_one()) tc::commit(done + stage);
+                        }
+                    tc::commit(done + stage);
+                }
                 __syncwarp();
-                // refill the previous step's stage once its MMAs have read it
-                // (this step's MMAs stay queued behind them meanwhile)
+                if (stats) t_mma += oz_clock() - m0;
+            }
+            if (elect_one()) tc::commit(tbar);  // every MMA of tile i
+            __syncwarp();
+            if (stats) t_loop += oz_clock() - l0;
+        } else if (warp == 1) {
+            // refill the stage of step g - 1 once its MMAs have read it (step g's MMAs
+            // stay queued behind them meanwhile)
+            __syncwarp();
+            for (int kc = 0; kc < kt; ++kc) {
+                const int g = i * kt + kc;
                 if (g >= 1 && g - 1 + STAGES < G) {
                     const int pg = g - 1;
                     const uint64_t w1 = stats ? oz_clock() : 0;
@@ -308,8 +327,6 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
                     issue(pg + STAGES);
                 }
             }
-            if (elect_one()) tc::commit(tbar);  // every MMA of tile i
-            __syncwarp();
         }
         // drain: ACC levels of tile i -> fp64, scaled by the row scales
         // (threads 0..127 = TMEM lanes; in k_tc warp 4 only join the barriers)
@@ -342,10 +359,13 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
         __syncthreads();  // TMEM and s_sb free for tile i + 1
         if (stats && tid == 0) t_drain += oz_clock() - d0;
     }
-    if (stats && tid == 0) {
+    if (stats && (tid == 0 || tid == 32)) {  // (warp 0: MMA side; warp 1: copy side)
         atomicAdd(stats + STAT_OZ_FULL, (unsigned long long)t_full);
         atomicAdd(stats + STAT_OZ_DONE, (unsigned long long)t_done);
         atomicAdd(stats + STAT_OZ_DRAIN, (unsigned long long)t_drain);
+        atomicAdd(stats + STAT_OZ_MMA, (unsigned long long)t_mma);
+        atomicAdd(stats + STAT_OZ_COPY, (unsigned long long)t_copy);
+        atomicAdd(stats + STAT_OZ_LOOP, (unsigned long long)t_loop);
     }
     if (tid < 128) {
 #pragma unroll
