@@ -1253,7 +1253,7 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
         CK(cudaStreamWaitEvent(p->sT, p->ev_join, 0));
         {
             Prof pr(p, p->sT, MXP_KCLASS_CHAIN, chain_flops - trsm_flops);
-            launch_tc(p->d_args, nsm, p->sT);
+            launch_tc(p->d_args, nsm, p->sT, p->nat_on);
             ++p->launches;
         }
         dbg(p, p->sT, "tc");  // (debug_sync = 1: k_tc then runs the whole schedule alone)

@@ -144,7 +144,7 @@ void launch_input_quantize(double* pool, const int32_t* slot, const uint8_t* pre
                            int nranks = 1);
 void launch_sched(const SchedArgs& a, const SchedArgs* a_dev, bool mxp, int grid, cudaStream_t s);  // a_dev: device copy of a
 // tensor-core GEMM kernel of the Ozaki mode (one CTA per SM, beside k_sched)
-void launch_tc(const SchedArgs* a_dev, int grid, cudaStream_t s);
+void launch_tc(const SchedArgs* a_dev, int grid, cudaStream_t s, bool native);
 int tc_ctas_per_sm();
 void launch_potrf_tile(const SchedArgs& a, int64_t k, cudaStream_t s);
 

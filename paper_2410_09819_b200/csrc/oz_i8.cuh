@@ -193,7 +193,10 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int* v) {
 }
 
 // C(128 x 64, fp64, column-major ldc) -= sum over ntiles tiles of A_n B_n^T,
-// each tile of K = 32 * kt (kt = nb / 32) emulated with S slices (kt * 32 <= 16384).
+// each tile of K = 32 * kt (kt = nb / 32) emulated with S slices (kt * 32 <= 16384);
+// C is updated once per tile of K (C <- C - P_n, one fp64 rounding each, in the
+// fixed tile order): no 64-double register accumulator, so k_tc fits 5 warps
+// beside a k_sched CTA (the 5th warp issues the native engine's MMAs).
 // smem: >= SMEM_BYTES dynamic shared memory; tmem: 512 allocated columns.
 // All 128 threads call; thread 0 issues the bulk copies and the MMAs (S
 // compile-time: the S(S+1)/2 MMAs of a K step are straight-line code on
@@ -204,7 +207,10 @@ __device__ __forceinline__ uint64_t oz_clock() {
     return t;
 }
 // stats (MXP_ATTR_PROFILE): [STAT_OZ_FULL], [STAT_OZ_DONE], [STAT_OZ_DRAIN] in ns, or nullptr
-template <int S, class Src>
+// RACC (the 4-warp k_tc of FP64 maps): the tiles' products accumulate in 64
+// fp64 registers per thread and C is updated once per task; otherwise (the
+// 5-warp k_tc of MxP maps, 168 registers) C is updated once per tile of K.
+template <int S, bool RACC, class Src>
 __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles, int kt, int64_t nb, uint8_t* smem,
                              uint32_t tmem, int pf, unsigned long long* stats) {
     uint64_t t_full = 0, t_done = 0, t_drain = 0, t_mma = 0, t_copy = 0, t_loop = 0;
@@ -271,10 +277,10 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
         for (int g = 0; g < STAGES && g < G; ++g) issue(g);
     }
 
-    double acc[BN];
+    const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    double acc[RACC ? BN : 1];
 #pragma unroll
-    for (int j = 0; j < BN; ++j) acc[j] = 0.0;
-    const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+    for (int j = 0; j < (RACC ? BN : 1); ++j) acc[j] = 0.0;
 
     for (int i = 0; i < ntiles; ++i) {
         if (warp == 0) {
@@ -338,7 +344,7 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
         tc::fence_after();
         __syncthreads();  // s_sb visible
         __syncwarp();     // (converged warp for the .sync.aligned TMEM loads)
-        if (wk) {
+        if (wk && RACC) {
 #pragma unroll
         for (int g8 = 0; g8 < BN / 8; ++g8) {
             int x[S][8];
@@ -351,13 +357,41 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
 #pragma unroll
                 for (int c = S - 1; c >= 0; --c)  // smallest weight first; 2^(-8c) exact
                     v = fma(i2d(x[c][j]), __longlong_as_double((long long)(1023 - 8 * c) << 52), v);
-                acc[g8 * 8 + j] = fma(v * sa_r, s_sb[g8 * 8 + j], acc[g8 * 8 + j]);
+                acc[(g8 * 8 + j) % (RACC ? BN : 1)] =
+                    fma(v * sa_r, s_sb[g8 * 8 + j], acc[(g8 * 8 + j) % (RACC ? BN : 1)]);
+            }
+        }
+        } else if (wk) {  // C -= (this tile's product), one fp64 rounding per tile of K
+            double* crow = C + tid;
+#pragma unroll
+        for (int g8 = 0; g8 < BN / 8; ++g8) {
+            int x[S][8];
+#pragma unroll
+            for (int c = 0; c < S; ++c) tmem_ld8(tl + (uint32_t)(c * BN + g8 * 8), x[c]);
+            double cv[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) cv[j] = __ldcg(crow + (int64_t)(g8 * 8 + j) * ldc);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                double v = 0.0;
+#pragma unroll
+                for (int c = S - 1; c >= 0; --c)  // smallest weight first; 2^(-8c) exact
+                    v = fma(i2d(x[c][j]), __longlong_as_double((long long)(1023 - 8 * c) << 52), v);
+                __stcg(crow + (int64_t)(g8 * 8 + j) * ldc, fma(-(v * sa_r), s_sb[g8 * 8 + j], cv[j]));
             }
         }
         }
         tc::fence_before();
         __syncthreads();  // TMEM and s_sb free for tile i + 1
         if (stats && tid == 0) t_drain += oz_clock() - d0;
+    }
+    if (RACC && tid < 128) {
+#pragma unroll
+        for (int j = 0; j < (RACC ? BN : 1); ++j) {
+            double* p = C + tid + (int64_t)j * ldc;
+            __stcg(p, __ldcg(p) - acc[j]);
+        }
     }
     if (stats && (tid == 0 || tid == 32)) {  // (warp 0: MMA side; warp 1: copy side)
         atomicAdd(stats + STAT_OZ_FULL, (unsigned long long)t_full);
@@ -367,13 +401,6 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
         atomicAdd(stats + STAT_OZ_COPY, (unsigned long long)t_copy);
         atomicAdd(stats + STAT_OZ_LOOP, (unsigned long long)t_loop);
     }
-    if (tid < 128) {
-#pragma unroll
-        for (int j = 0; j < BN; ++j) {
-            double* p = C + tid + (int64_t)j * ldc;
-            __stcg(p, __ldcg(p) - acc[j]);
-        }
-    }
     __syncthreads();
     if (tid == 0) {
         for (int i = 0; i < STAGES; ++i) tc::mbar_inval(full + i), tc::mbar_inval(done + i);
@@ -382,16 +409,16 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
 }
 
 constexpr int MIN_S = 4;  // slices supported by the compiled variants: MIN_S..MAX_S
-template <class Src>
+template <bool RACC, class Src>
 __device__ __forceinline__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, int s, int kt,
                                            int64_t nb, uint8_t* smem, uint32_t tmem, int pf,
                                            unsigned long long* stats) {
     switch (s) {
-    case 4: block_gemm_t<4>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats); break;
-    case 5: block_gemm_t<5>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats); break;
-    case 6: block_gemm_t<6>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats); break;
-    case 7: block_gemm_t<7>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats); break;
-    default: block_gemm_t<8>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats); break;
+    case 4: block_gemm_t<4, RACC>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats); break;
+    case 5: block_gemm_t<5, RACC>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats); break;
+    case 6: block_gemm_t<6, RACC>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats); break;
+    case 7: block_gemm_t<7, RACC>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats); break;
+    default: block_gemm_t<8, RACC>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats); break;
     }
 }
 

@@ -531,6 +531,7 @@ __device__ __noinline__ bool task_gemm_nat(const SchedArgs& a, int64_t m, int64_
 // §8(f) N4): C(m,k)[128x64 block b] -= sum over the chunk of L(m,n) L(k,n)^T,
 // operands from the int8 slice images written by the QUANT tasks, levels
 // drained to fp64 after every tile of K.
+template <bool RACC>
 __device__ __noinline__ bool task_gemm_oz(const SchedArgs& a, int64_t m, int64_t k, int64_t b, int64_t c,
                                           uint8_t* smem, uint32_t tmem, int* s_flag) {
     const int64_t Nt = a.Nt, nb = a.nb, SR = nb / 128;
@@ -570,7 +571,7 @@ __device__ __noinline__ bool task_gemm_oz(const SchedArgs& a, int64_t m, int64_t
         return o;
     };
     double* Ct = tile_ptr(a.pool, a.slot, Nt, nb, m, k) + bi * 128 + bj * 64 * nb;
-    oz::block_gemm(Ct, nb, src, (int)(n1 - n0), s, (int)(nb / 32), nb, smem, tmem, a.oz_prefetch, a.stats);
+    oz::block_gemm<RACC>(Ct, nb, src, (int)(n1 - n0), s, (int)(nb / 32), nb, smem, tmem, a.oz_prefetch, a.stats);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1247,10 +1248,12 @@ __global__ void __launch_bounds__(CC::NT, 3) k_sched(const SchedArgs a_param, co
 // k_sched holds for it), and k_sched only takes work off it -- a task claimed
 // by k_sched depends on earlier tasks only, which k_tc or k_sched finish.
 // (Profilers that serialize kernels run k_tc alone: still correct.)
-// (4 warps: with one k_sched CTA beside it every SM sub-partition holds one
-// warp of each kernel -- 255 + 168 registers x 32 lanes fit its 16K registers;
-// a fifth warp would not, and k_tc would wait for k_sched to exit)
-__global__ void __launch_bounds__(128, 1) k_tc(const SchedArgs* __restrict__ ap) {
+// (5 warps at <= 168 registers: with one k_sched CTA (4 warps, 168 registers)
+// beside it, SM sub-partition 0 holds k_tc's warps 0 and 4 and one k_sched warp,
+// 3 x 168 x 32 <= 16K registers.  Warps 0-3 are the TMEM lanes 0-127; warp 4
+// issues the native engine's copies and MMAs and otherwise joins the barriers.)
+template <int NW>
+__device__ __forceinline__ void k_tc_body(const SchedArgs* __restrict__ ap) {
     const SchedArgs& a = *ap;
     const int id = (int)smid();
     if (id < a.sm_lo + a.reserved_sms || id >= a.sm_hi) return;
@@ -1290,15 +1293,15 @@ __global__ void __launch_bounds__(128, 1) k_tc(const SchedArgs* __restrict__ ap)
             const int cp = a.prec[tile_index(a.Nt, m, k)];
             if (threadIdx.x == 0) atomicAdd(a.tdiag + 12, 1);
             if (cp == P_FP64)
-                task_gemm_oz(a, m, k, it.w >> 16, it.w & 0xFFFF, smem_t, tmem, &s_flag);
+                task_gemm_oz<NW == 4>(a, m, k, it.w >> 16, it.w & 0xFFFF, smem_t, tmem, &s_flag);
             else if (cp == P_FP32 && a.native)
-                task_gemm_nat<nat::K_F32X2>(a, m, k, it.w >> 16, it.w & 0xFFFF, smem_t, tmem, &s_flag);
+                { if constexpr (NW == 5) task_gemm_nat<nat::K_F32X2>(a, m, k, it.w >> 16, it.w & 0xFFFF, smem_t, tmem, &s_flag); else if (threadIdx.x == 0) atomicExch(a.err, 1); }
             else if (cp == P_FP32)
                 task_gemm_img<true, 4>(a, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_t, tmem, &s_flag);
             else if (a.native && cp == P_FP16)
-                task_gemm_nat<nat::K_F16>(a, m, k, it.w >> 16, it.w & 0xFFFF, smem_t, tmem, &s_flag);
+                { if constexpr (NW == 5) task_gemm_nat<nat::K_F16>(a, m, k, it.w >> 16, it.w & 0xFFFF, smem_t, tmem, &s_flag); else if (threadIdx.x == 0) atomicExch(a.err, 1); }
             else if (a.native)
-                task_gemm_nat<nat::K_F8>(a, m, k, it.w >> 16, it.w & 0xFFFF, smem_t, tmem, &s_flag);
+                { if constexpr (NW == 5) task_gemm_nat<nat::K_F8>(a, m, k, it.w >> 16, it.w & 0xFFFF, smem_t, tmem, &s_flag); else if (threadIdx.x == 0) atomicExch(a.err, 1); }
             else
                 task_gemm_img<false, 4>(a, m, k, it.w >> 16, it.w & 0xFFFF, cp, smem_t, tmem, &s_flag);
             if (threadIdx.x == 0) atomicAdd(a.tdiag + 13, 1);
@@ -1322,6 +1325,10 @@ __global__ void __launch_bounds__(128, 1) k_tc(const SchedArgs* __restrict__ ap)
     if (threadIdx.x < 32) tc::tmem_dealloc(tmem, oz::TMEM_COLS);
     if (a.stats && threadIdx.x == 0) atomicMax(a.stats + STAT_TEND, globaltimer());
 }
+// the 4-warp variant (255 registers, register accumulators in the Ozaki
+// engine) for maps without native-width tiles; the 5-warp variant for the rest
+__global__ void __launch_bounds__(128, 1) k_tc4(const SchedArgs* __restrict__ ap) { k_tc_body<4>(ap); }
+__global__ void __maxnreg__(168) k_tc5(const SchedArgs* __restrict__ ap) { k_tc_body<5>(ap); }
 
 // ------------------------------------------------- POTRF of a diagonal tile
 // One CTA (256 threads) on a reserved SM: waits until every GEMM/SYRK task of
@@ -1419,12 +1426,14 @@ void configure_sched() {
     cudaFuncSetAttribute(k_sched<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM_BYTES);
     cudaFuncSetAttribute(k_sched<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM_BYTES);
     cudaFuncSetAttribute(k_potrf_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, POTRF_SMEM);
-    cudaFuncSetAttribute(k_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    cudaFuncSetAttribute(k_tc4, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    cudaFuncSetAttribute(k_tc5, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
     // every SM configured for the full 228 KB of shared memory: the Ozaki mode
     // co-schedules one k_tc CTA (~150 KB) and one k_sched CTA (~78 KB) per SM,
     // which a smaller carve-out picked for whichever kernel lands first would
     // forbid (the second kernel's CTAs would then wait for the first to exit)
-    cudaFuncSetAttribute(k_tc, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_tc4, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_tc5, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(k_sched<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(k_sched<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(k_potrf_tile, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -1447,13 +1456,14 @@ void launch_sched(const SchedArgs& a, const SchedArgs* a_dev, bool mxp, int grid
 int tc_ctas_per_sm() {
     int occ = 0;
     configure_sched();
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tc, 128, TC_SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tc5, 160, TC_SMEM);
     return occ;
 }
 
-void launch_tc(const SchedArgs* a_dev, int grid, cudaStream_t s) {
+void launch_tc(const SchedArgs* a_dev, int grid, cudaStream_t s, bool native) {
     configure_sched();
-    k_tc<<<grid, 128, TC_SMEM, s>>>(a_dev);
+    if (native) k_tc5<<<grid, 160, TC_SMEM, s>>>(a_dev);
+    else k_tc4<<<grid, 128, TC_SMEM, s>>>(a_dev);
 }
 
 void launch_potrf_tile(const SchedArgs& a, int64_t k, cudaStream_t s) {
@@ -1469,7 +1479,8 @@ void preload_sched() {
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, (const void*)k_sched<true>);
     cudaFuncGetAttributes(&fa, (const void*)k_sched<false>);
-    cudaFuncGetAttributes(&fa, (const void*)k_tc);
+    cudaFuncGetAttributes(&fa, (const void*)k_tc4);
+    cudaFuncGetAttributes(&fa, (const void*)k_tc5);
     cudaFuncGetAttributes(&fa, (const void*)k_potrf_tile);
     cudaFuncGetAttributes(&fa, (const void*)k_matern_tile_norms);
     cudaFuncGetAttributes(&fa, (const void*)k_tile_amax);

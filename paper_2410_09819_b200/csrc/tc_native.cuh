@@ -133,13 +133,14 @@ __device__ __forceinline__ void drain_tile(uint32_t tl, int buf, bool first, con
 
 // C(128 x 128, fp64, column-major ldc) -= sum over ntiles K tiles of
 // (A_n B_n^T) = codes products * inv;  kt = chunks per K tile (nb / KE).
-// All 128 threads call; tmem: >= 384 allocated columns (two accumulators + the
-// running sum).  One elected thread of warp 0 issues the bulk copies and the
-// MMAs; warps 0-3 drain their TMEM lanes (= output rows): warps 1-3 as soon as
-// a K tile's accumulator is complete, warp 0 after it has queued the MMAs of
-// the next K tile (the tensor core works through them meanwhile).  Four
-// warps, not five: k_tc must stay co-resident with a k_sched CTA, and a fifth
-// 255-register warp fills one SM sub-partition's register file.
+// All 160 threads of k_tc call; tmem: >= 384 allocated columns (two
+// accumulators + the running sum).  Warp 4 is the producer and MMA issuer (one
+// lane: bulk copies into the ring, the MMAs of each step, refilling a stage as
+// soon as the MMAs that read it complete); warps 0-3 (= TMEM lanes 0-127 =
+// output rows) drain each K tile's accumulator while the tensor core runs the
+// next one.  (Round 2 first had warp 0 issue and drain: while it drained, no
+// MMA was issued -- the drains of the warp that feeds the tensor core were
+// serialized with the MMAs.)
 template <int KIND, class Src>
 __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, int kt, uint8_t* smem, uint32_t tmem) {
     constexpr int NS = nstages(KIND), SB = stage_bytes(KIND);
@@ -150,40 +151,33 @@ __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, i
     uint64_t* tempty = tfull + 2;   // [2] accumulator drained (4 warps arrive)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int G = ntiles * kt;
-    const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+    const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     if (tid == 0) {
         for (int i = 0; i < NS; ++i) tc::mbar_init(full + i, 1), tc::mbar_init(empty + i, 1);
         for (int i = 0; i < 2; ++i) tc::mbar_init(tfull + i, 1), tc::mbar_init(tempty + i, 4);
         tc::fence_mbar_init();
     }
     __syncthreads();
-    if (warp == 0) {
-        NatTile cur{}, curm{};
-        int cur_i = -1;
-        auto issue = [&](int g) {  // bulk copies of K step g into its stage (elected lane)
-            const int st = g % NS, i = g / kt, kc = g - i * kt;
-            if (i != cur_i) cur = src(i), cur_i = i;
-            uint8_t* sa = base + st * SB;
-            const int64_t o = (int64_t)kc * CHUNK;
-            uint32_t bytes = 2 * CHUNK;
-            if (KIND == K_F32X2) bytes += (cur.al ? CHUNK : 0) + (cur.bl ? CHUNK : 0);
-            tc::mbar_expect_tx(full + st, bytes);
-            tc::bulk_g2s(sa, cur.a + o, CHUNK, full + st);
-            tc::bulk_g2s(sa + CHUNK, cur.b + o, CHUNK, full + st);
-            if (KIND == K_F32X2 && cur.al) tc::bulk_g2s(sa + 2 * CHUNK, cur.al + o, CHUNK, full + st);
-            if (KIND == K_F32X2 && cur.bl) tc::bulk_g2s(sa + 3 * CHUNK, cur.bl + o, CHUNK, full + st);
-        };
-        auto refill = [&](int g) {  // stage of step g (its MMAs issued) -> step g + NS
-            if (g >= 0 && g + NS < G) {
-                tc::mbar_wait(empty + (g % NS), (uint32_t)((g / NS) & 1));
-                issue(g + NS);
-            }
-        };
-        if (lane == 0)
+    if (warp == 4) {
+        if (lane == 0) {
+            NatTile cur{}, curm{};
+            int cur_i = -1;
+            auto issue = [&](int g) {  // bulk copies of K step g into its stage
+                const int st = g % NS, i = g / kt, kc = g - i * kt;
+                if (i != cur_i) cur = src(i), cur_i = i;
+                uint8_t* sa = base + st * SB;
+                const int64_t o = (int64_t)kc * CHUNK;
+                uint32_t bytes = 2 * CHUNK;
+                if (KIND == K_F32X2) bytes += (cur.al ? CHUNK : 0) + (cur.bl ? CHUNK : 0);
+                tc::mbar_expect_tx(full + st, bytes);
+                tc::bulk_g2s(sa, cur.a + o, CHUNK, full + st);
+                tc::bulk_g2s(sa + CHUNK, cur.b + o, CHUNK, full + st);
+                if (KIND == K_F32X2 && cur.al) tc::bulk_g2s(sa + 2 * CHUNK, cur.al + o, CHUNK, full + st);
+                if (KIND == K_F32X2 && cur.bl) tc::bulk_g2s(sa + 3 * CHUNK, cur.bl + o, CHUNK, full + st);
+            };
             for (int g = 0; g < NS && g < G; ++g) issue(g);
-        for (int i = 0; i < ntiles; ++i) {
-            const int buf = i & 1;
-            if (lane == 0) {
+            for (int i = 0; i < ntiles; ++i) {
+                const int buf = i & 1;
                 if (KIND == K_F32X2) curm = src(i);
                 if (i >= 2) tc::mbar_wait(tempty + buf, (uint32_t)(((i >> 1) - 1) & 1));
                 tc::fence_after();
@@ -203,41 +197,19 @@ __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, i
                         }
                     }
                     tc::commit(empty + st);
-                    // refill the previous step's stage once its MMAs have read it (this step's
-                    // MMAs stay queued behind them); at the last step of a K tile the refill
-                    // waits until after this warp's drain
-                    if (kc + 1 < kt || i == 0) refill(g - 1);
+                    // refill the previous step's stage once its MMAs have read it (this
+                    // step's MMAs stay queued behind them meanwhile)
+                    const int pg = g - 1;
+                    if (pg >= 0 && pg + NS < G) {
+                        tc::mbar_wait(empty + (pg % NS), (uint32_t)((pg / NS) & 1));
+                        issue(pg + NS);
+                    }
                 }
                 tc::commit(tfull + buf);
             }
-            __syncwarp();
-            if (i >= 1) {  // drain K tile i-1 while the tensor core runs tile i
-                const int pb = (i - 1) & 1;
-                const NatTile t = src(i - 1);
-                tc::mbar_wait(tfull + pb, (uint32_t)(((i - 1) >> 1) & 1));
-                tc::fence_after();
-                __syncwarp();
-                drain_tile(tl, pb, i == 1, t);
-                tc::fence_before();
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(tempty + pb);
-                    refill(i * kt + kt - 2);  // the refill deferred at tile i's last step
-                }
-                __syncwarp();
-            }
         }
-        {  // the last K tile
-            const int i = ntiles - 1, pb = i & 1;
-            const NatTile t = src(i);
-            tc::mbar_wait(tfull + pb, (uint32_t)((i >> 1) & 1));
-            tc::fence_after();
-            __syncwarp();
-            drain_tile(tl, pb, i == 0, t);
-            tc::fence_before();
-            __syncwarp();
-        }
-    } else {  // warps 1-3: drain every K tile as soon as it is complete
+        __syncwarp();
+    } else {  // warps 0-3: drain every K tile as soon as it is complete
         for (int i = 0; i < ntiles; ++i) {
             const int buf = i & 1;
             const NatTile t = src(i);
@@ -249,9 +221,7 @@ __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, i
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty + buf);
         }
-    }
-    // C -= R (fp64 read-modify-write of this thread's output row)
-    {
+        // C -= R (fp64 read-modify-write of this thread's output row)
         const uint32_t tr = tl + 2 * BN;
         const int row = tid;
 #pragma unroll 1
