@@ -387,11 +387,12 @@ int mxp_ooc_variant_volume(int64_t n, int64_t nb, int variant, int streams, int6
  * CTA start, [7] last CTA end, [8] #CTAs that ran tasks, [9..12] POTRF phases, [13..15]
  * Ozaki GEMM loop (stage waits, MMA-completion waits, per-tile drains), [16..19] GEMM busy
  * by output precision (FP64, FP32, FP16, FP8), [20..23] their task counts, [24..26] Ozaki
- * issuing thread in MMA issue, bulk-copy issue, whole K loop; then for each column k at
- * [28+3k]: POTRF kernel start, Ready-wait done, end.
+ * issuing thread in MMA issue, bulk-copy issue, whole K loop, [28..32] native engine
+ * (issuer waits for stages / refills / drained accumulators, drain time of warp 0, final
+ * C update); then for each column k at [36+3k]: POTRF kernel start, Ready-wait done, end.
  *   out      host array of `count` entries (may be NULL when count = 0) (arg 2)
  *   count    capacity of out                                           (arg 3)
- *   written  receives the number of entries available (28 + 3 Nt)       (arg 4)
+ *   written  receives the number of entries available (36 + 3 Nt)       (arg 4)
  */
 int mxp_chol_sched_diagnostics(mxp_plan_t plan, uint64_t* out, int64_t count, int64_t* written);
 

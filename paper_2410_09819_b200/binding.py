@@ -327,9 +327,9 @@ class Plan:
         buf = (ctypes.c_uint64 * n.value)()
         _check("mxp_chol_sched_diagnostics", lib().mxp_chol_sched_diagnostics(self._h, buf, n.value, ctypes.byref(n)))
         v = list(buf)
-        nt = (len(v) - 28) // 3
+        nt = (len(v) - 36) // 3
         span = (v[7] - v[6]) / 1e6 if v[7] > v[6] else 0.0
-        pot = [((v[28 + 3 * k] - v[6]) / 1e6, (v[29 + 3 * k] - v[6]) / 1e6, (v[30 + 3 * k] - v[6]) / 1e6)
+        pot = [((v[36 + 3 * k] - v[6]) / 1e6, (v[37 + 3 * k] - v[6]) / 1e6, (v[38 + 3 * k] - v[6]) / 1e6)
                for k in range(nt)]
         return {"gemm_busy_ms": v[0] / 1e6, "gemm_wait_ms": v[1] / 1e6, "trsm_busy_ms": v[2] / 1e6,
                 "trsm_wait_ms": v[3] / 1e6, "gemm_tasks": v[4], "trsm_tasks": v[5], "span_ms": span,
@@ -337,6 +337,8 @@ class Plan:
                                                   "trsm": v[12] / 1e6},
                 "ozaki_ms": {"stage_wait": v[13] / 1e6, "mma_done_wait": v[14] / 1e6, "drain": v[15] / 1e6,
                              "mma_issue": v[24] / 1e6, "copy_issue": v[25] / 1e6, "k_loop": v[26] / 1e6},
+                "native_ms": {"stage_wait": v[28] / 1e6, "refill_wait": v[29] / 1e6, "drained_wait": v[30] / 1e6,
+                              "drain": v[31] / 1e6, "final_c": v[32] / 1e6},
                 "gemm_busy_ms_by_precision": {p: v[16 + i] / 1e6 for i, p in enumerate(("fp64", "fp32", "fp16", "fp8"))},
                 "gemm_tasks_by_precision": {p: v[20 + i] for i, p in enumerate(("fp64", "fp32", "fp16", "fp8"))},
                 "potrf_timeline_ms": pot}

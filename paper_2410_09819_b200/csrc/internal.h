@@ -130,7 +130,10 @@ enum {
     STAT_GEMM_P = 16, STAT_GEMM_PN = 20,
     // Ozaki GEMM loop: time of the issuing thread in MMA issue, in bulk-copy issue, and in the loop
     STAT_OZ_MMA = 24, STAT_OZ_COPY = 25, STAT_OZ_LOOP = 26,
-    STAT_POTRF = 28  // + 3k: kernel start, wait done, end
+    // native engine: issuer waits for stages (full), for refills (empty), for drained
+    // accumulators (tempty); drain warps' time in drains; the final C update
+    STAT_NAT_FULL = 28, STAT_NAT_EMPTY = 29, STAT_NAT_TEMPTY = 30, STAT_NAT_DRAIN = 31, STAT_NAT_FINAL = 32,
+    STAT_POTRF = 36  // + 3k: kernel start, wait done, end
 };
 int sched_ctas_per_sm();
 // load every kernel of the library eagerly (one call per file; see preload_sched)

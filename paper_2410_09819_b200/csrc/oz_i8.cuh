@@ -386,11 +386,14 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
         __syncthreads();  // TMEM and s_sb free for tile i + 1
         if (stats && tid == 0) t_drain += oz_clock() - d0;
     }
-    if (RACC && tid < 128) {
+    if (RACC && tid < 128) {  // (16 loads in flight, then the stores: see tc_native.cuh)
 #pragma unroll
-        for (int j = 0; j < (RACC ? BN : 1); ++j) {
-            double* p = C + tid + (int64_t)j * ldc;
-            __stcg(p, __ldcg(p) - acc[j]);
+        for (int j0 = 0; j0 < (RACC ? BN : 1); j0 += 16) {
+            double cv[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) cv[j] = __ldcg(C + tid + (int64_t)(j0 + j) * ldc);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) __stcg(C + tid + (int64_t)(j0 + j) * ldc, cv[j] - acc[(j0 + j) % (RACC ? BN : 1)]);
         }
     }
     if (stats && (tid == 0 || tid == 32)) {  // (warp 0: MMA side; warp 1: copy side)

@@ -200,17 +200,28 @@ __device__ __forceinline__ bool task_gemm(const SchedArgs& a, int64_t m, int64_t
         gemm_mainloop<CC>(acc, src, nb, nb, nk, smem, post);
     }
     double* Ct = tile_ptr(pool, slot, Nt, nb, m, k) + roff + coff * nb;
+    // (loads of a fragment row first, then the stores: an interleaved
+    // load-subtract-store per element is serialized by possible aliasing)
 #pragma unroll
-    for (int mi = 0; mi < CC::MI; ++mi)
+    for (int mi = 0; mi < CC::MI; ++mi) {
+        double cv[CC::NI][2];
 #pragma unroll
         for (int ni = 0; ni < CC::NI; ++ni)
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
                 int r, cc;
                 frag_pos<CC>(mi, ni, i, r, cc);
-                double* p = Ct + r + (int64_t)cc * nb;
-                __stcg(p, __ldcg(p) - acc[mi][ni][i]);
+                cv[ni][i] = __ldcg(Ct + r + (int64_t)cc * nb);
             }
+#pragma unroll
+        for (int ni = 0; ni < CC::NI; ++ni)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                int r, cc;
+                frag_pos<CC>(mi, ni, i, r, cc);
+                __stcg(Ct + r + (int64_t)cc * nb, cv[ni][i] - acc[mi][ni][i]);
+            }
+    }
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -267,16 +278,25 @@ __device__ __forceinline__ bool task_trsm(const SchedArgs& a, int64_t m, int64_t
         }
         double* XJ = X + J * 128 * nb;
 #pragma unroll
-        for (int mi = 0; mi < CC::MI; ++mi)
+        for (int mi = 0; mi < CC::MI; ++mi) {  // (loads first, then stores: see task_gemm)
+            double cv[CC::NI][2];
 #pragma unroll
             for (int ni = 0; ni < CC::NI; ++ni)
 #pragma unroll
                 for (int i = 0; i < 2; ++i) {
                     int rr, cc;
                     frag_pos<CC>(mi, ni, i, rr, cc);
-                    double* p = XJ + rr + (int64_t)cc * nb;
-                    __stcg(p, __ldcg(p) - acc[mi][ni][i]);
+                    cv[ni][i] = __ldcg(XJ + rr + (int64_t)cc * nb);
                 }
+#pragma unroll
+            for (int ni = 0; ni < CC::NI; ++ni)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    int rr, cc;
+                    frag_pos<CC>(mi, ni, i, rr, cc);
+                    __stcg(XJ + rr + (int64_t)cc * nb, cv[ni][i] - acc[mi][ni][i]);
+                }
+        }
         __threadfence_block();
         sync_workers();
         zero_acc<CC>(acc);
@@ -513,7 +533,7 @@ __device__ __noinline__ bool task_gemm_nat(const SchedArgs& a, int64_t m, int64_
         return o;
     };
     double* Ct = tile_ptr(a.pool, a.slot, Nt, nb, m, k) + bi * 128 + bj * 128 * nb;
-    nat::block_gemm<KIND>(Ct, nb, src, (int)(n1 - n0), (int)(nb / nat::ke(KIND)), smem, tmem);
+    nat::block_gemm<KIND>(Ct, nb, src, (int)(n1 - n0), (int)(nb / nat::ke(KIND)), smem, tmem, a.stats);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {

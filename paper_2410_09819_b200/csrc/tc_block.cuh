@@ -117,9 +117,12 @@ __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int nsteps, i
         float v[32];
         tmem_ld32(tl + c0, v);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            double* p = C + row + (int64_t)(c0 + i) * ldc;
-            __stcg(p, __ldcg(p) - (double)v[i]);
+        for (int i0 = 0; i0 < 32; i0 += 8) {  // (loads first, then stores: aliasing would serialize)
+            double cv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) cv[i] = __ldcg(C + row + (int64_t)(c0 + i0 + i) * ldc);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) __stcg(C + row + (int64_t)(c0 + i0 + i) * ldc, cv[i] - (double)v[i0 + i]);
         }
     }
     fence_before();
@@ -242,9 +245,12 @@ __device__ void block_gemm_img(double* C, int64_t ldc, const Src& src, int nstep
             float v[32];
             tmem_ld32(tl + c0, v);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                double* p = C + row + (int64_t)(c0 + i) * ldc;
-                __stcg(p, __ldcg(p) - (double)v[i]);
+            for (int i0 = 0; i0 < 32; i0 += 8) {  // (loads first, then stores: aliasing would serialize)
+                double cv[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) cv[i] = __ldcg(C + row + (int64_t)(c0 + i0 + i) * ldc);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) __stcg(C + row + (int64_t)(c0 + i0 + i) * ldc, cv[i] - (double)v[i0 + i]);
             }
         }
     }

@@ -141,8 +141,15 @@ __device__ __forceinline__ void drain_tile(uint32_t tl, int buf, bool first, con
 // next one.  (Round 2 first had warp 0 issue and drain: while it drained, no
 // MMA was issued -- the drains of the warp that feeds the tensor core were
 // serialized with the MMAs.)
+__device__ __forceinline__ uint64_t nat_clock() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 template <int KIND, class Src>
-__device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, int kt, uint8_t* smem, uint32_t tmem) {
+__device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, int kt, uint8_t* smem, uint32_t tmem,
+                           unsigned long long* stats = nullptr) {
+    uint64_t w_full = 0, w_empty = 0, w_tempty = 0, t_drain = 0, t_final = 0;
     constexpr int NS = nstages(KIND), SB = stage_bytes(KIND);
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(base + NS * SB);
@@ -179,12 +186,16 @@ __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, i
             for (int i = 0; i < ntiles; ++i) {
                 const int buf = i & 1;
                 if (KIND == K_F32X2) curm = src(i);
+                const uint64_t q0 = stats ? nat_clock() : 0;
                 if (i >= 2) tc::mbar_wait(tempty + buf, (uint32_t)(((i >> 1) - 1) & 1));
+                if (stats) w_tempty += nat_clock() - q0;
                 tc::fence_after();
                 const uint32_t d = tmem + (uint32_t)(buf * BN);
                 for (int kc = 0; kc < kt; ++kc) {
                     const int g = i * kt + kc, st = g % NS;
+                    const uint64_t q1 = stats ? nat_clock() : 0;
                     tc::mbar_wait(full + st, (uint32_t)((g / NS) & 1));
+                    if (stats) w_full += nat_clock() - q1;
                     tc::fence_after();
                     const uint32_t sa = tc::smem_u32(base + st * SB);
                     const uint64_t ad = make_desc(sa), bd = make_desc(sa + CHUNK);
@@ -201,7 +212,9 @@ __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, i
                     // step's MMAs stay queued behind them meanwhile)
                     const int pg = g - 1;
                     if (pg >= 0 && pg + NS < G) {
+                        const uint64_t q2 = stats ? nat_clock() : 0;
                         tc::mbar_wait(empty + (pg % NS), (uint32_t)((pg / NS) & 1));
+                        if (stats) w_empty += nat_clock() - q2;
                         issue(pg + NS);
                     }
                 }
@@ -216,27 +229,44 @@ __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, i
             tc::mbar_wait(tfull + buf, (uint32_t)((i >> 1) & 1));
             tc::fence_after();
             __syncwarp();
+            const uint64_t q3 = stats ? nat_clock() : 0;
             drain_tile(tl, buf, i == 0, t);
             tc::fence_before();
             __syncwarp();
+            if (stats) t_drain += nat_clock() - q3;
             if (lane == 0) mbar_arrive(tempty + buf);
         }
         // C -= R (fp64 read-modify-write of this thread's output row)
+        const uint64_t q4 = stats ? nat_clock() : 0;
         const uint32_t tr = tl + 2 * BN;
         const int row = tid;
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 32) {
             float r[32];
             tc::tmem_ld32(tr + (uint32_t)c0, r);
+            // loads first, then the stores: interleaved load-subtract-store per element was
+            // serialized by possible aliasing (~1 L2 round trip per element: measured 58 us per
+            // 128 x 128 block, 45 % of the native engine's time at C3)
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                double* p = C + row + (int64_t)(c0 + j) * ldc;
-                __stcg(p, __ldcg(p) - (double)r[j]);
+            for (int j0 = 0; j0 < 32; j0 += 16) {
+                double cv[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) cv[j] = __ldcg(C + row + (int64_t)(c0 + j0 + j) * ldc);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) __stcg(C + row + (int64_t)(c0 + j0 + j) * ldc, cv[j] - (double)r[j0 + j]);
             }
         }
         tc::fence_before();
+        if (stats) t_final += nat_clock() - q4;
     }
     __syncthreads();
+    if (stats && (tid == 0 || tid == 128)) {  // (warp 0: drains; warp 4: issuer)
+        atomicAdd(stats + STAT_NAT_FULL, (unsigned long long)w_full);
+        atomicAdd(stats + STAT_NAT_EMPTY, (unsigned long long)w_empty);
+        atomicAdd(stats + STAT_NAT_TEMPTY, (unsigned long long)w_tempty);
+        atomicAdd(stats + STAT_NAT_DRAIN, (unsigned long long)t_drain);
+        atomicAdd(stats + STAT_NAT_FINAL, (unsigned long long)t_final);
+    }
     if (tid == 0) {
         for (int i = 0; i < NS; ++i) tc::mbar_inval(full + i), tc::mbar_inval(empty + i);
         for (int i = 0; i < 2; ++i) tc::mbar_inval(tfull + i), tc::mbar_inval(tempty + i);

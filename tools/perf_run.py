@@ -25,6 +25,7 @@ def report(plan):
     print("per-CTA ms: gemm busy %.1f wait %.1f, trsm busy %.1f wait %.1f" % (
         d["gemm_busy_ms"] / ctas, d["gemm_wait_ms"] / ctas, d["trsm_busy_ms"] / ctas, d["trsm_wait_ms"] / ctas))
     print("ozaki loop ms per CTA:", {k: round(v / ctas, 1) for k, v in d["ozaki_ms"].items()})
+    print("native ms per CTA:", {k: round(v / ctas, 1) for k, v in d["native_ms"].items()})
     print("gemm busy ms per CTA by precision:", {k: round(v / ctas, 1) for k, v in d["gemm_busy_ms_by_precision"].items()},
           "tasks:", d["gemm_tasks_by_precision"])
     print("kernels:", plan.kernel_stats())
