@@ -59,7 +59,7 @@ typedef enum mxp_attr {
     MXP_ATTR_DEVICE = 0,          /* CUDA device ordinal (default: current device at plan time) */
     MXP_ATTR_STREAM = 1,          /* cudaStream_t (as int64) all work is ordered after/before; 0 = legacy default */
     MXP_ATTR_HBM_BYTES_CAP = 2,   /* cap on the tile pool; forces out-of-core when the lower triangle exceeds it */
-    MXP_ATTR_SPLITK_TILES = 3,    /* K chunk of one GEMM task, in tiles (default 8); results are bitwise
+    MXP_ATTR_SPLITK_TILES = 3,    /* K chunk of one GEMM task, in tiles (default 16); results are bitwise
                                      deterministic for a fixed value */
     MXP_ATTR_LOOKAHEAD = 4,       /* reserved (the task list always carries one column of lookahead) */
     MXP_ATTR_DEBUG_SYNC = 5,      /* 1 = synchronize and check after every kernel; 2 = GEMM-throughput

@@ -67,7 +67,7 @@ struct mxp_plan_s {
     int device = 0;
     cudaStream_t user_stream = 0;
     int64_t hbm_cap = 0;
-    int64_t splitk_tiles = 8;  // bulk K chunk of a GEMM task, in tiles (swept: 1,2,4,8 -> 8 best)
+    int64_t splitk_tiles = 16;  // bulk K chunk of a GEMM task, in tiles (swept at C3 MxP: 4/8/16/32 -> 263/280/286/291 TF/s; C2 equal at 8 and 16)
     int lookahead = 1;
     int debug_sync = 0;
 

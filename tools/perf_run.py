@@ -42,6 +42,8 @@ def main():
         m.generate_plgsy_device(A0, seed=42)
         A = torch.empty_like(A0)
         plan = m.Plan(n, nb)
+        if "SPLITK" in os.environ:
+            plan.set("splitk_tiles", int(os.environ["SPLITK"]))
         plan.set("profile", int(os.environ.get("PROFILE", "0")))
         plan.set("fp64_engine", int(os.environ.get("ENGINE", "1")))
         if "OZ_PF" in os.environ:
@@ -63,6 +65,8 @@ def main():
         xy = torch.tensor(w.matern_locations(n, seed=1), device="cuda")
         pmap, _ = m.precision_map_matern_device(xy, nb, eps, 1.0, a)
         plan = m.Plan(n, nb, pmap)
+        if "SPLITK" in os.environ:
+            plan.set("splitk_tiles", int(os.environ["SPLITK"]))
         plan.set("profile", int(os.environ.get("PROFILE", "0")))
         plan.set("fp64_engine", 1)
         for r in range(reps):
