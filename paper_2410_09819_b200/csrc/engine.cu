@@ -183,6 +183,7 @@ struct mxp_plan_s {
     double st_ms[4] = {0, 0, 0, 0}, st_flops[4] = {0, 0, 0, 0};
     bool have_result = false;
     double logdet = 0.0;
+    int solve_seq = 0;              // forward solves run on this plan (publication tags of the diagonal solves)
     // single-process multi-GPU (mxp_chol_plan with ngpus > 1): the group plan owns one sub-plan
     // per GPU (rank r, device r mod #devices) and runs them from one host thread each
     std::vector<mxp_plan_s*> group;
@@ -712,8 +713,8 @@ Layout layout(const mxp_plan_s* p) {
     off += align_up(sizeof(long long) * (size_t)p->T, 256);
     L.in_scale = off;
     off += align_up(sizeof(double) * (size_t)p->T, 256);
-    L.solve = off;  // forward solve: r, z (Nt*nb each) + scalars
-    off += align_up(sizeof(double) * (2 * (size_t)p->Nt * p->nb + 8), 256);
+    L.solve = off;  // forward solve: r, z (Nt*nb each) + scalars + 32 ints of diagonal-solve flags
+    off += align_up(sizeof(double) * (2 * (size_t)p->Nt * p->nb + 8 + 16), 256);
     L.shadow = off;
     off += align_up(p->shadow_bytes, 1024);
     L.pool = off;
@@ -2569,7 +2570,8 @@ int mxp_chol_solve_lower(mxp_plan_t p, const double* y_dev, double* z_dev, doubl
         cudaStream_t s = p->user_stream;
         CK(cudaMemsetAsync(r, 0, sizeof(double) * N, s));
         CK(cudaMemcpyAsync(r, y_dev, sizeof(double) * p->n, cudaMemcpyDeviceToDevice, s));
-        launch_forward_solve(p->pool, p->d_slot, p->d_wbuf, p->Nt, p->nb, r, z, s, decode_args(p));
+        launch_forward_solve(p->pool, p->d_slot, p->d_wbuf, p->Nt, p->nb, r, z, s, decode_args(p),
+                             reinterpret_cast<int*>(sc + 8), ++p->solve_seq);
         launch_sumsq(z, p->n, sc, s);
         CK(cudaGetLastError());
         if (z_dev) CK(cudaMemcpyAsync(z_dev, z, sizeof(double) * p->n, cudaMemcpyDeviceToDevice, s));

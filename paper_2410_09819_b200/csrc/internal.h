@@ -163,8 +163,11 @@ struct TileCodes {
 
 // ---- forward solve / log-likelihood (solve.cu) -----------
 // z = L^-1 r on the resident factor (r, z: Nt*nb, padded with zeros; r is consumed)
+// flags: >= nb/128 ints of device memory for the parallel diagonal solves (publication tags
+// seq * Nt + k + 1; seq distinct per call), or nullptr for the one-CTA diagonal solve
 void launch_forward_solve(const double* pool, const int32_t* slot, const double* wbuf, int64_t Nt, int64_t nb,
-                          double* r, double* z, cudaStream_t s, TileCodes codes = TileCodes{});
+                          double* r, double* z, cudaStream_t s, TileCodes codes = TileCodes{},
+                          int* flags = nullptr, int seq = 0);
 void launch_sumsq(const double* z, int64_t n, double* out, cudaStream_t s);
 
 // ---- layout / utility kernels --------------------------------------------

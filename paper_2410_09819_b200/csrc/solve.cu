@@ -101,6 +101,64 @@ __global__ void __launch_bounds__(256) k_trsv_diag(const double* __restrict__ po
     for (int64_t c = threadIdx.x; c < nb; c += blockDim.x) z[k * nb + c] = sz[c];
 }
 
+// z_k = L_kk^-1 r_k with one CTA per 128-row block J of the tile (the blocks
+// run concurrently): CTA J accumulates L[J, I] z_I for I < J as each z_I is
+// published (flags[I] == tag, release/acquire), then z_J = W_J (r_J - sum).
+// The single-CTA version streamed the whole half tile (~4.5 MB) through one SM
+// on the critical path of every column.
+__global__ void __launch_bounds__(256) k_trsv_diag_par(const double* __restrict__ pool,
+                                                        const int32_t* __restrict__ slot,
+                                                        const double* __restrict__ wbuf, int64_t Nt, int64_t nb,
+                                                        int64_t k, const double* __restrict__ r, double* z,
+                                                        int* flags, int tag) {
+    __shared__ double zs[128], sv[128], part[256];
+    const int J = blockIdx.x, tid = threadIdx.x, row = tid & 127, h = tid >> 7;
+    const int64_t S = nb / 128;
+    const double* Lkk = pool + (int64_t)slot[tile_index(Nt, k, k)] * nb * nb;
+    const double* LJ = Lkk + J * 128 + row;  // row J*128 + row of the tile, column c at LJ[c * nb]
+    double a0 = 0.0, a1 = 0.0;
+    for (int I = 0; I < J; ++I) {
+        const int64_t c0 = (int64_t)I * 128 + h * 64;
+        double l[16];  // (the first loads of this block go out before the wait)
+#pragma unroll
+        for (int q = 0; q < 16; ++q) l[q] = __ldcs(LJ + (c0 + q) * nb);
+        if (tid == 0) {
+            int v;
+            do {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flags + I) : "memory");
+            } while (v != tag);
+        }
+        __syncthreads();
+        if (tid < 128) zs[tid] = __ldcg(z + k * nb + I * 128 + tid);
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 16; q += 2) {
+            a0 = fma(l[q], zs[h * 64 + q], a0);
+            a1 = fma(l[q + 1], zs[h * 64 + q + 1], a1);
+        }
+#pragma unroll 4
+        for (int c = 16; c < 64; c += 2) {
+            a0 = fma(__ldcs(LJ + (c0 + c) * nb), zs[h * 64 + c], a0);
+            a1 = fma(__ldcs(LJ + (c0 + c + 1) * nb), zs[h * 64 + c + 1], a1);
+        }
+        __syncthreads();  // (zs is rewritten for the next block)
+    }
+    part[tid] = a0 + a1;
+    __syncthreads();
+    if (h == 0) sv[row] = r[k * nb + J * 128 + row] - (part[row] + part[row + 128]);
+    __syncthreads();
+    const double* W = wbuf + (k * S + J) * (128 * 128);  // column-major, lower triangular
+    double b0 = 0.0;
+    const int kk0 = h == 0 ? 0 : (row + 1) / 2, kk1 = h == 0 ? (row + 1) / 2 : row + 1;
+    for (int kk = kk0; kk < kk1; ++kk) b0 = fma(W[row + kk * 128], sv[kk], b0);
+    part[tid] = b0;
+    __syncthreads();
+    if (h == 0) z[k * nb + J * 128 + row] = part[row] + part[row + 128];
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flags + J), "r"(tag) : "memory");
+}
+
 // out = sum z_i^2 over i < n (fixed-order tree in one CTA)
 __global__ void __launch_bounds__(1024) k_sumsq(const double* __restrict__ z, int64_t n, double* out) {
     __shared__ double red[1024];
@@ -118,7 +176,7 @@ __global__ void __launch_bounds__(1024) k_sumsq(const double* __restrict__ z, in
 }  // namespace
 
 void launch_forward_solve(const double* pool, const int32_t* slot, const double* wbuf, int64_t Nt, int64_t nb,
-                          double* r, double* z, cudaStream_t s, TileCodes codes) {
+                          double* r, double* z, cudaStream_t s, TileCodes codes, int* flags, int seq) {
     const size_t sm_diag = sizeof(double) * (nb + 128 + 256), sm_gemv = sizeof(double) * (nb + 256);
     static bool configured = false;
     if (!configured) {
@@ -127,8 +185,13 @@ void launch_forward_solve(const double* pool, const int32_t* slot, const double*
         configured = true;
     }
     for (int64_t k = 0; k < Nt; ++k) {
-        MXP_CARVEOUT_MAX(k_trsv_diag);
-        k_trsv_diag<<<1, 256, sm_diag, s>>>(pool, slot, wbuf, Nt, nb, k, r, z);
+        if (flags) {
+            k_trsv_diag_par<<<(unsigned)(nb / 128), 256, 0, s>>>(pool, slot, wbuf, Nt, nb, k, r, z, flags,
+                                                                 (int)(seq * Nt + k + 1));
+        } else {
+            MXP_CARVEOUT_MAX(k_trsv_diag);
+            k_trsv_diag<<<1, 256, sm_diag, s>>>(pool, slot, wbuf, Nt, nb, k, r, z);
+        }
         MXP_CARVEOUT_MAX(k_trsv_gemv);
         if (k + 1 < Nt) k_trsv_gemv<<<(unsigned)((Nt - k - 1) * (nb / 128)), 256, sm_gemv, s>>>(pool, slot, Nt, nb, k, r, z, codes);
     }
@@ -146,6 +209,7 @@ void launch_sumsq(const double* z, int64_t n, double* out, cudaStream_t s) {
 void preload_solve() {
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, (const void*)k_trsv_diag);
+    cudaFuncGetAttributes(&fa, (const void*)k_trsv_diag_par);
     cudaFuncGetAttributes(&fa, (const void*)k_trsv_gemv);
     cudaFuncGetAttributes(&fa, (const void*)k_sumsq);
     cudaGetLastError();

@@ -57,6 +57,14 @@ def main():
         print(f"c2 n={n} nb={nb} info={info} ms={ev0.elapsed_time(ev1):.1f} "
               f"TF/s={n ** 3 / 3 / ev0.elapsed_time(ev1) / 1e9:.2f} engine={plan.get('fp64_engine_used')}")
         report(plan)
+        if os.environ.get("SOLVE") == "1":  # forward solve / log-likelihood on the resident factor
+            y = torch.randn(n, dtype=torch.float64, device="cuda")
+            for r in range(3):
+                ev0.record()
+                ll = plan.loglik(y)
+                ev1.record()
+                torch.cuda.synchronize()
+            print(f"loglik ms={ev0.elapsed_time(ev1):.2f} GB/s={(n * n / 2 * 8) / ev0.elapsed_time(ev1) / 1e6:.0f} ll={ll:.6e}")
     else:
         n = int(sys.argv[2]) if len(sys.argv) > 2 else 32768
         eps = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-5
