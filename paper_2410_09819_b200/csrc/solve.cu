@@ -24,21 +24,22 @@ __device__ __forceinline__ double tile_elem(const double* L, const uint8_t* code
 template <int P>
 __device__ __forceinline__ double row_dot(const double* L, const uint8_t* codes, double inv, int64_t nb, int64_t row,
                                           int64_t c0, int64_t c1, const double* sz) {
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // 4 chains, 8 loads in flight per thread
+    // 8 chains, 16 loads in flight per thread (a CTA streams 1 MB: with 8 loads in flight it was
+    // latency-bound at ~10 GB/s, which bounded every column's update)
+    double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll 2
-    for (int64_t c = c0; c < c1; c += 4) {
-        s0 = fma(tile_elem<P>(L, codes, row + c * nb, inv), sz[c], s0);
-        s1 = fma(tile_elem<P>(L, codes, row + (c + 1) * nb, inv), sz[c + 1], s1);
-        s2 = fma(tile_elem<P>(L, codes, row + (c + 2) * nb, inv), sz[c + 2], s2);
-        s3 = fma(tile_elem<P>(L, codes, row + (c + 3) * nb, inv), sz[c + 3], s3);
+    for (int64_t c = c0; c < c1; c += 8) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s[q] = fma(tile_elem<P>(L, codes, row + (c + q) * nb, inv), sz[c + q], s[q]);
     }
-    return (s0 + s1) + (s2 + s3);
+    return ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
 }
 
-__global__ void __launch_bounds__(256) k_trsv_gemv(const double* __restrict__ pool, const int32_t* __restrict__ slot,
-                                                   int64_t Nt, int64_t nb, int64_t k, double* r,
-                                                   const double* __restrict__ z, TileCodes codes) {
-    extern __shared__ double sz[];  // z_k (nb) + 256 partial sums
+constexpr int GEMV_T = 512;  // 4 column quarters x 128 rows
+__global__ void __launch_bounds__(GEMV_T) k_trsv_gemv(const double* __restrict__ pool, const int32_t* __restrict__ slot,
+                                                      int64_t Nt, int64_t nb, int64_t k, double* r,
+                                                      const double* __restrict__ z, TileCodes codes) {
+    extern __shared__ double sz[];  // z_k (nb) + GEMV_T partial sums
     double* part = sz + nb;
     const int64_t RB = nb / 128;
     const int64_t m = k + 1 + blockIdx.x / RB, rb = blockIdx.x % RB;
@@ -47,7 +48,7 @@ __global__ void __launch_bounds__(256) k_trsv_gemv(const double* __restrict__ po
     const int row = threadIdx.x & 127, h = threadIdx.x >> 7;
     const int64_t t = tile_index(Nt, m, k);
     const double* L = pool + (int64_t)slot[t] * nb * nb;
-    const int64_t c0 = h * (nb / 2), c1 = c0 + nb / 2, grow = rb * 128 + row;
+    const int64_t c0 = h * (nb / 4), c1 = c0 + nb / 4, grow = rb * 128 + row;
     // compact pool: tiles below FP64 are read at their storage precision (fewer bytes)
     const int p = (codes.sto && codes.sto[t] >= 0) ? codes.prec[t] : P_FP64;
     const uint8_t* cp = p != P_FP64 ? codes.shadow + codes.sto[t] : nullptr;
@@ -61,7 +62,7 @@ __global__ void __launch_bounds__(256) k_trsv_gemv(const double* __restrict__ po
     }
     part[threadIdx.x] = dot;
     __syncthreads();
-    if (h == 0) r[m * nb + rb * 128 + row] -= part[row] + part[row + 128];
+    if (h == 0) r[m * nb + rb * 128 + row] -= (part[row] + part[row + 128]) + (part[row + 256] + part[row + 384]);
 }
 
 // z_k = L_kk^-1 r_k: for J = 0..nb/128-1:  s = r_J - L[J, <J] z_<J;  z_J = W_J s
@@ -136,10 +137,16 @@ __global__ void __launch_bounds__(256) k_trsv_diag_par(const double* __restrict_
             a0 = fma(l[q], zs[h * 64 + q], a0);
             a1 = fma(l[q + 1], zs[h * 64 + q + 1], a1);
         }
-#pragma unroll 4
-        for (int c = 16; c < 64; c += 2) {
-            a0 = fma(__ldcs(LJ + (c0 + c) * nb), zs[h * 64 + c], a0);
-            a1 = fma(__ldcs(LJ + (c0 + c + 1) * nb), zs[h * 64 + c + 1], a1);
+#pragma unroll
+        for (int c = 16; c < 64; c += 16) {
+            double lv[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) lv[q] = __ldcs(LJ + (c0 + c + q) * nb);
+#pragma unroll
+            for (int q = 0; q < 16; q += 2) {
+                a0 = fma(lv[q], zs[h * 64 + c + q], a0);
+                a1 = fma(lv[q + 1], zs[h * 64 + c + q + 1], a1);
+            }
         }
         __syncthreads();  // (zs is rewritten for the next block)
     }
@@ -148,10 +155,17 @@ __global__ void __launch_bounds__(256) k_trsv_diag_par(const double* __restrict_
     if (h == 0) sv[row] = r[k * nb + J * 128 + row] - (part[row] + part[row + 128]);
     __syncthreads();
     const double* W = wbuf + (k * S + J) * (128 * 128);  // column-major, lower triangular
-    double b0 = 0.0;
+    // (a fixed trip count with predicated loads, 4 chains: a data-dependent loop bound
+    // serialized the 64 loads behind each other on every column's critical path)
     const int kk0 = h == 0 ? 0 : (row + 1) / 2, kk1 = h == 0 ? (row + 1) / 2 : row + 1;
-    for (int kk = kk0; kk < kk1; ++kk) b0 = fma(W[row + kk * 128], sv[kk], b0);
-    part[tid] = b0;
+    double bq[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 16
+    for (int q = 0; q < 64; ++q) {
+        const int kk = kk0 + q;  // <= 127
+        const double w = kk < kk1 ? __ldg(W + row + kk * 128) : 0.0;
+        bq[q & 3] = fma(w, sv[kk], bq[q & 3]);
+    }
+    part[tid] = (bq[0] + bq[1]) + (bq[2] + bq[3]);
     __syncthreads();
     if (h == 0) z[k * nb + J * 128 + row] = part[row] + part[row + 128];
     __threadfence();
@@ -177,7 +191,7 @@ __global__ void __launch_bounds__(1024) k_sumsq(const double* __restrict__ z, in
 
 void launch_forward_solve(const double* pool, const int32_t* slot, const double* wbuf, int64_t Nt, int64_t nb,
                           double* r, double* z, cudaStream_t s, TileCodes codes, int* flags, int seq) {
-    const size_t sm_diag = sizeof(double) * (nb + 128 + 256), sm_gemv = sizeof(double) * (nb + 256);
+    const size_t sm_diag = sizeof(double) * (nb + 128 + 256), sm_gemv = sizeof(double) * (nb + GEMV_T);
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(k_trsv_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -193,7 +207,8 @@ void launch_forward_solve(const double* pool, const int32_t* slot, const double*
             k_trsv_diag<<<1, 256, sm_diag, s>>>(pool, slot, wbuf, Nt, nb, k, r, z);
         }
         MXP_CARVEOUT_MAX(k_trsv_gemv);
-        if (k + 1 < Nt) k_trsv_gemv<<<(unsigned)((Nt - k - 1) * (nb / 128)), 256, sm_gemv, s>>>(pool, slot, Nt, nb, k, r, z, codes);
+        if (k + 1 < Nt)
+            k_trsv_gemv<<<(unsigned)((Nt - k - 1) * (nb / 128)), GEMV_T, sm_gemv, s>>>(pool, slot, Nt, nb, k, r, z, codes);
     }
 }
 
