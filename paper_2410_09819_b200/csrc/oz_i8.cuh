@@ -97,6 +97,46 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// The 10 MMAs of one 32-K step for S = 7 as ONE PTX block: the descriptors
+// and TMEM addresses are formed by adds inside it, so the uniform-register
+// moves happen once per step instead of once per MMA (the per-MMA form cost
+// ~100 issue cycles each).  (t, u0, m): A slice t against the m stacked B
+// slices u0 .. u0+m-1 into levels t+u0 .. t+u0+m-1 -- the same list as the
+// generic loop of block_gemm_t.
+__device__ __forceinline__ void mma_step7(uint32_t tmem, uint64_t ad0, uint64_t bd0, uint32_t acc0) {
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t.reg .b64 a, b;\n\t.reg .b32 d;\n\t"
+        "setp.ne.b32 p, %3, 0;\n\tsetp.eq.b32 q, 0, 0;\n\t"
+        // t = 0: (u0 0, m 4) -> level 0; (u0 4, m 3) -> level 4
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %4, p;\n\t"
+        "add.s64 b, %2, 512;\n\tadd.u32 d, %0, 256;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [d], %1, b, %5, p;\n\t"
+        // t = 1: (0, 4) -> level 1; (4, 2) -> level 5
+        "add.s64 a, %1, 256;\n\tadd.u32 d, %0, 64;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [d], a, %2, %4, q;\n\t"
+        "add.u32 d, %0, 320;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [d], a, b, %6, q;\n\t"
+        // t = 2: (0, 4) -> level 2; (4, 1) -> level 6
+        "add.s64 a, %1, 512;\n\tadd.u32 d, %0, 128;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [d], a, %2, %4, q;\n\t"
+        "add.u32 d, %0, 384;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [d], a, b, %7, q;\n\t"
+        // t = 3: (0, 4) -> level 3
+        "add.s64 a, %1, 768;\n\tadd.u32 d, %0, 192;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [d], a, %2, %4, q;\n\t"
+        // t = 4: (0, 3) -> level 4
+        "add.s64 a, %1, 1024;\n\tadd.u32 d, %0, 256;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [d], a, %2, %5, q;\n\t"
+        // t = 5: (0, 2) -> level 5
+        "add.s64 a, %1, 1280;\n\tadd.u32 d, %0, 320;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [d], a, %2, %6, q;\n\t"
+        // t = 6: (0, 1) -> level 6
+        "add.s64 a, %1, 1536;\n\tadd.u32 d, %0, 384;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [d], a, %2, %7, q;\n\t}\n" ::"r"(tmem),
+        "l"(ad0), "l"(bd0), "r"(acc0), "r"(idesc_i8(256)), "r"(idesc_i8(192)), "r"(idesc_i8(128)),
+        "r"(idesc_i8(64)));
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
@@ -303,14 +343,18 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
                 // -- so each A slice needs ceil((S-t)/4) MMAs of N <= 256 instead of
                 // S-t MMAs of N = 64 (12 instead of 36 for S = 8; A read 12x, not 36x).
                 if (elect_one()) {
+                    if constexpr (S == 7) {
+                        mma_step7(tmem, ad0, bd0, acc0);
+                    } else {
 #pragma unroll
-                    for (int t = 0; t < S; ++t)
+                        for (int t = 0; t < S; ++t)
 #pragma unroll
-                        for (int u0 = 0; u0 + t < S; u0 += 4) {
-                            const int m = (S - t - u0) < 4 ? (S - t - u0) : 4;
-                            mma_i8(tmem + (uint32_t)((t + u0) * BN), ad0 + (uint64_t)(t * (CHUNK >> 4)),
-                                   bd0 + (uint64_t)(u0 * (CHUNK_B >> 4)), idesc_i8(BN * m), t > 0 ? 1u : acc0);
-                        }
+                            for (int u0 = 0; u0 + t < S; u0 += 4) {
+                                const int m = (S - t - u0) < 4 ? (S - t - u0) : 4;
+                                mma_i8(tmem + (uint32_t)((t + u0) * BN), ad0 + (uint64_t)(t * (CHUNK >> 4)),
+                                       bd0 + (uint64_t)(u0 * (CHUNK_B >> 4)), idesc_i8(BN * m), t > 0 ? 1u : acc0);
+                            }
+                    }
                     tc::commit(done + stage);
                 }
                 __syncwarp();

@@ -81,6 +81,46 @@ __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t adesc, uint64_t bd
             "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
 }
 
+// The 4 MMAs of one stage (K = 4 x 32 bytes: descriptors advance by 2 in their
+// 16-byte address field) as one PTX block: the descriptor adds stay in uniform
+// registers instead of a register-to-uniform move per MMA.
+template <int KIND>
+__device__ __forceinline__ void mma4(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+    if constexpr (KIND != K_F8)
+        asm volatile(
+            "{\n\t.reg .pred p, t;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+            "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+            "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, t;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n\t}\n" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+    else
+        asm volatile(
+            "{\n\t.reg .pred p, t;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+            "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+            "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a1, b1, %3, t;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a2, b2, %3, t;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a3, b3, %3, t;\n\t}\n" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+}
+// one lane of a converged warp (the lowest active)
+__device__ __forceinline__ bool elect1() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\t"
+        "elect.sync rx|px, %1;\n\t"
+        "@px mov.s32 %0, 1;\n\t}\n"
+        : "+r"(pred)
+        : "r"(0xFFFFFFFFu));
+    return pred != 0;
+}
+
 // 32 consecutive fp32 columns of this thread's TMEM lane <- v (then wait for the store)
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
     asm volatile(
@@ -165,8 +205,8 @@ __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, i
         tc::fence_mbar_init();
     }
     __syncthreads();
-    if (warp == 4) {
-        if (lane == 0) {
+    if (warp == 4) {  // (all 32 lanes walk the loop converged; one elected lane issues)
+        {
             NatTile cur{}, curm{};
             int cur_i = -1;
             auto issue = [&](int g) {  // bulk copies of K step g into its stage
@@ -176,11 +216,14 @@ __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, i
                 const int64_t o = (int64_t)kc * CHUNK;
                 uint32_t bytes = 2 * CHUNK;
                 if (KIND == K_F32X2) bytes += (cur.al ? CHUNK : 0) + (cur.bl ? CHUNK : 0);
-                tc::mbar_expect_tx(full + st, bytes);
-                tc::bulk_g2s(sa, cur.a + o, CHUNK, full + st);
-                tc::bulk_g2s(sa + CHUNK, cur.b + o, CHUNK, full + st);
-                if (KIND == K_F32X2 && cur.al) tc::bulk_g2s(sa + 2 * CHUNK, cur.al + o, CHUNK, full + st);
-                if (KIND == K_F32X2 && cur.bl) tc::bulk_g2s(sa + 3 * CHUNK, cur.bl + o, CHUNK, full + st);
+                if (elect1()) {
+                    tc::mbar_expect_tx(full + st, bytes);
+                    tc::bulk_g2s(sa, cur.a + o, CHUNK, full + st);
+                    tc::bulk_g2s(sa + CHUNK, cur.b + o, CHUNK, full + st);
+                    if (KIND == K_F32X2 && cur.al) tc::bulk_g2s(sa + 2 * CHUNK, cur.al + o, CHUNK, full + st);
+                    if (KIND == K_F32X2 && cur.bl) tc::bulk_g2s(sa + 3 * CHUNK, cur.bl + o, CHUNK, full + st);
+                }
+                __syncwarp();
             };
             for (int g = 0; g < NS && g < G; ++g) issue(g);
             for (int i = 0; i < ntiles; ++i) {
@@ -199,15 +242,17 @@ __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, i
                     tc::fence_after();
                     const uint32_t sa = tc::smem_u32(base + st * SB);
                     const uint64_t ad = make_desc(sa), bd = make_desc(sa + CHUNK);
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {  // 32 bytes of K per MMA: +2 in the 16-byte address field
-                        mma<KIND>(d, ad + 2 * kk, bd + 2 * kk, (kc | kk) ? 1u : 0u);
-                        if (KIND == K_F32X2) {
-                            if (curm.bl) mma<KIND>(d, ad + 2 * kk, make_desc(sa + 3 * CHUNK) + 2 * kk, 1u);
-                            if (curm.al) mma<KIND>(d, make_desc(sa + 2 * CHUNK) + 2 * kk, bd + 2 * kk, 1u);
+                    if (elect1()) {
+                        if constexpr (KIND != K_F32X2) {
+                            mma4<KIND>(d, ad, bd, kc ? 1u : 0u);
+                        } else {
+                            mma4<KIND>(d, ad, bd, kc ? 1u : 0u);  // h h
+                            if (curm.bl) mma4<KIND>(d, ad, make_desc(sa + 3 * CHUNK), 1u);  // h l
+                            if (curm.al) mma4<KIND>(d, make_desc(sa + 2 * CHUNK), bd, 1u);  // l h
                         }
+                        tc::commit(empty + st);
                     }
-                    tc::commit(empty + st);
+                    __syncwarp();
                     // refill the previous step's stage once its MMAs have read it (this
                     // step's MMAs stay queued behind them meanwhile)
                     const int pg = g - 1;
@@ -218,7 +263,8 @@ __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, i
                         issue(pg + NS);
                     }
                 }
-                tc::commit(tfull + buf);
+                if (elect1()) tc::commit(tfull + buf);
+                __syncwarp();
             }
         }
         __syncwarp();
