@@ -19,7 +19,14 @@ def report(plan):
     if os.environ.get("PROFILE") != "1":
         return
     d = plan.sched_diagnostics()
-    d.pop("potrf_timeline_ms", None)
+    tl = d.pop("potrf_timeline_ms", None)
+    if tl:  # per column: POTRF compute (end - inputs ready) and the gap to the next column's inputs
+        comp = [e - w for (_, w, e) in tl]
+        gap = [tl[k + 1][1] - tl[k][2] for k in range(len(tl) - 1)]
+        q = lambda v: [round(sorted(v)[int(f * (len(v) - 1))], 2) for f in (0.1, 0.5, 0.9)]
+        print("potrf compute ms p10/50/90:", q(comp), "sum", round(sum(comp), 1),
+              "| inputs-ready gap after previous POTRF p10/50/90:", q(gap), "sum", round(sum(gap), 1),
+              "| last 8 columns (compute, gap):", [(round(comp[k], 2), round(gap[k], 2)) for k in range(len(gap) - 8, len(gap))])
     ctas = max(1, d.get("ctas", 1))
     print("sched:", {k: (round(v, 1) if isinstance(v, float) else v) for k, v in d.items()})
     print("per-CTA ms: gemm busy %.1f wait %.1f, trsm busy %.1f wait %.1f" % (
