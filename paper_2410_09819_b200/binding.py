@@ -336,7 +336,8 @@ class Plan:
                 "ctas": v[8], "potrf_phase_ms": {"update": v[9] / 1e6, "chol": v[10] / 1e6, "inverse": v[11] / 1e6,
                                                   "trsm": v[12] / 1e6},
                 "ozaki_ms": {"stage_wait": v[13] / 1e6, "mma_done_wait": v[14] / 1e6, "drain": v[15] / 1e6,
-                             "mma_issue": v[24] / 1e6, "copy_issue": v[25] / 1e6, "k_loop": v[26] / 1e6},
+                             "mma_issue": v[24] / 1e6, "copy_issue": v[25] / 1e6, "k_loop": v[26] / 1e6,
+                             "drain_tile_wait": v[33] / 1e6},
                 "native_ms": {"stage_wait": v[28] / 1e6, "refill_wait": v[29] / 1e6, "drained_wait": v[30] / 1e6,
                               "drain": v[31] / 1e6, "final_c": v[32] / 1e6},
                 "gemm_busy_ms_by_precision": {p: v[16 + i] / 1e6 for i, p in enumerate(("fp64", "fp32", "fp16", "fp8"))},

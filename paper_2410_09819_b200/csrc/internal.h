@@ -133,6 +133,7 @@ enum {
     // native engine: issuer waits for stages (full), for refills (empty), for drained
     // accumulators (tempty); drain warps' time in drains; the final C update
     STAT_NAT_FULL = 28, STAT_NAT_EMPTY = 29, STAT_NAT_TEMPTY = 30, STAT_NAT_DRAIN = 31, STAT_NAT_FINAL = 32,
+    STAT_OZ_TBAR = 33,  // Ozaki: drain warps waiting for a tile's last MMAs (the rest of STAT_OZ_DRAIN is the drain)
     STAT_POTRF = 36  // + 3k: kernel start, wait done, end
 };
 int sched_ctas_per_sm();

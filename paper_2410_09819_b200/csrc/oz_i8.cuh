@@ -204,6 +204,30 @@ __device__ __forceinline__ void write_slices16(uint8_t* img, int64_t nb, int s, 
                    make_uint4(w[t][0], w[t][1], w[t][2], w[t][3]));
 }
 
+// sum_c 2^(-8c) ACC_c of one element.  S = 7: levels 0-2 and 3-5 are first
+// combined exactly in int64 (|.| < 2^47) and converted with the 2^52 + 2^51
+// magic number, so 3 conversions and 3 fma replace 7 + 7 on the FP64 pipe (the
+// drain is ~15 % of a C2 GEMM task); the value differs from the per-level sum
+// only in the order of exact partial sums (no extra rounding below 2^-53 of
+// the partials).  Other S: the per-level sum, smallest weight first.
+template <int S>
+__device__ __forceinline__ double combine_levels(const int (&x)[S][8], int j) {
+    if constexpr (S == 7) {
+        const long long hi = ((long long)x[0][j] << 16) + ((long long)x[1][j] << 8) + (long long)x[2][j];
+        const long long lo = ((long long)x[3][j] << 16) + ((long long)x[4][j] << 8) + (long long)x[5][j];
+        const double m = 6755399441055744.0;  // 2^52 + 2^51
+        const double hd = __longlong_as_double(0x4338000000000000LL + hi) - m;
+        const double ld = __longlong_as_double(0x4338000000000000LL + lo) - m;
+        return fma(hd, 0x1p-16, fma(ld, 0x1p-40, i2d(x[6][j]) * 0x1p-48));
+    } else {
+        double v = 0.0;
+#pragma unroll
+        for (int c = S - 1; c >= 0; --c)  // smallest weight first; 2^(-8c) exact
+            v = fma(i2d(x[c][j]), __longlong_as_double((long long)(1023 - 8 * c) << 52), v);
+        return v;
+    }
+}
+
 // ------------------------------------------------------------ block GEMM
 // One operand tile of the K walk: chunk (t = 0, kc = 0) of the A rows / B rows
 // of this block, the byte stride between slices, and the row scales.
@@ -253,7 +277,7 @@ __device__ __forceinline__ uint64_t oz_clock() {
 template <int S, bool RACC, class Src>
 __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles, int kt, int64_t nb, uint8_t* smem,
                              uint32_t tmem, int pf, unsigned long long* stats) {
-    uint64_t t_full = 0, t_done = 0, t_drain = 0, t_mma = 0, t_copy = 0, t_loop = 0;
+    uint64_t t_full = 0, t_done = 0, t_drain = 0, t_mma = 0, t_copy = 0, t_loop = 0, t_tbar = 0;
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * STAGE_BYTES);
     uint64_t* done = full + STAGES;
@@ -388,6 +412,7 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
         tc::fence_after();
         __syncthreads();  // s_sb visible
         __syncwarp();     // (converged warp for the .sync.aligned TMEM loads)
+        if (stats && tid == 0) t_tbar += oz_clock() - d0;
         if (wk && RACC) {
 #pragma unroll
         for (int g8 = 0; g8 < BN / 8; ++g8) {
@@ -397,10 +422,7 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
             tmem_wait_ld();
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                double v = 0.0;
-#pragma unroll
-                for (int c = S - 1; c >= 0; --c)  // smallest weight first; 2^(-8c) exact
-                    v = fma(i2d(x[c][j]), __longlong_as_double((long long)(1023 - 8 * c) << 52), v);
+                const double v = combine_levels<S>(x, j);
                 acc[(g8 * 8 + j) % (RACC ? BN : 1)] =
                     fma(v * sa_r, s_sb[g8 * 8 + j], acc[(g8 * 8 + j) % (RACC ? BN : 1)]);
             }
@@ -447,6 +469,7 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
         atomicAdd(stats + STAT_OZ_MMA, (unsigned long long)t_mma);
         atomicAdd(stats + STAT_OZ_COPY, (unsigned long long)t_copy);
         atomicAdd(stats + STAT_OZ_LOOP, (unsigned long long)t_loop);
+        atomicAdd(stats + STAT_OZ_TBAR, (unsigned long long)t_tbar);
     }
     __syncthreads();
     if (tid == 0) {
