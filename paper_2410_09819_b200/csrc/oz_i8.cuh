@@ -440,10 +440,7 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
             tmem_wait_ld();
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                double v = 0.0;
-#pragma unroll
-                for (int c = S - 1; c >= 0; --c)  // smallest weight first; 2^(-8c) exact
-                    v = fma(i2d(x[c][j]), __longlong_as_double((long long)(1023 - 8 * c) << 52), v);
+                const double v = combine_levels<S>(x, j);
                 __stcg(crow + (int64_t)(g8 * 8 + j) * ldc, fma(-(v * sa_r), s_sb[g8 * 8 + j], cv[j]));
             }
         }
