@@ -68,8 +68,7 @@ struct mxp_plan_s {
     cudaStream_t user_stream = 0;
     int64_t hbm_cap = 0;
     int64_t splitk_tiles = 16;  // bulk K chunk of a GEMM task, in tiles (swept at C3 MxP: 4/8/16/32 -> 263/280/286/291 TF/s; C2 equal at 8 and 16)
-    int lookahead = 2;              // MXP_ATTR_LOOKAHEAD (in core; out of core uses 1)
-    int la_used = 1;
+    int lookahead = 1;
     int debug_sync = 0;
 
     // workspace
@@ -253,33 +252,22 @@ bool gemm_block_needed(const mxp_plan_s* p, int64_t m, int64_t k, int64_t b) {
     return block_needed(m, k, b, nb);
 }
 
-// chunks of column k with lookahead LA: ceil((k-LA)/KC) fixed-size chunks over [0, k-LA), then
-// the single columns {k-LA}, ..., {k-1} (sched_f64.cu chunk_range)
-int64_t nchunks(int64_t k, int64_t KC, int64_t LA) {
+// chunks of column k: ceil((k-1)/KC) fixed-size chunks over [0, k-1), then {k-1}
+int64_t nchunks(int64_t k, int64_t KC) {
     if (k == 0) return 0;
-    const int64_t tail = k < LA ? k : LA, bend = k - tail;
-    const int64_t nfull = bend > 0 ? (bend + KC - 1) / KC : 0;
-    return nfull + tail;
+    int64_t nfull = k >= 2 ? (k - 1 + KC - 1) / KC : 0;
+    return nfull + 1;
 }
-int64_t pool_slots(const mxp_plan_s* p);
-// lookahead the task list uses: MXP_ATTR_LOOKAHEAD (2 = two columns) in core; host streaming out
-// of core keeps one column (its slot plans free a slot two or three columns after its tile)
-int eff_lookahead(const mxp_plan_s* p) { return (p->lookahead >= 2 && pool_slots(p) == p->T) ? 2 : 1; }
 
 // The static task list (Alg. 1 enumerated column by column):
 //   iteration k:  (a) last GEMM chunk (n = k-1) of column k, diagonal tile first
-//                 (b) bulk GEMM chunks (n < k) of column k+1   [lookahead 1]
-//                     or: chunk {k-1} of column k+1, bulk chunks (n < k) of column k+2 [lookahead 2:
-//                     the work of two columns is available while column k's TRSM / QUANT / POTRF
-//                     chain runs -- at C3 MxP the GEMM CTAs had waited 28 % of the time]
+//                 (b) bulk GEMM chunks (n < k) of column k+1   [lookahead]
 //                 (c) TRSM row tasks of column k
 // POTRF(k) runs beside it (k_potrf_tile) once (a) has finished on tile (k,k).
 void plan_images(mxp_plan_s* p);
 void build_task_list(mxp_plan_s* p) {
     plan_images(p);
     const int64_t Nt = p->Nt, nb = p->nb, KC = p->splitk_tiles, NB = blocks_per_tile(nb);
-    const int64_t LA = eff_lookahead(p);
-    p->la_used = (int)LA;
     p->items.clear();
     p->items2.clear();
     p->expected.assign(p->T, 0);
@@ -307,28 +295,19 @@ void build_task_list(mxp_plan_s* p) {
         for (int64_t m = k; m < Nt; ++m)
             if (owned(m)) push(make_int4(ITEM_PREP, (int)m, (int)k, 0));
     };
-    if (p->host_mode)
-        for (int64_t j = 0; j < LA && j < Nt; ++j) prep_col(j);
+    if (p->host_mode) prep_col(0);
     for (int64_t k = 0; k < Nt; ++k) {
-        if (p->host_mode && k + LA < Nt) prep_col(k + LA);  // before any GEMM on column k+LA
+        if (p->host_mode && k + 1 < Nt) prep_col(k + 1);  // before any GEMM on column k+1
         if (k >= 1) {
-            int64_t last = nchunks(k, KC, LA) - 1;
+            int64_t last = nchunks(k, KC) - 1;
             gemm_col(k, last, last + 1);
         }
         // POTRF(k): normally claimed by the dedicated kernel; listed so the
         // schedule can also complete on its own (fallback, see sched_f64.cu)
         if (owned(k)) push(make_int4(ITEM_POTRF, (int)k, (int)k, 0));
-        if (LA == 1) {
-            if (k + 1 < Nt) {
-                int64_t nb1 = nchunks(k + 1, KC, 1) - 1;  // bulk chunks of column k+1
-                gemm_col(k + 1, 0, nb1);
-            }
-        } else {
-            if (k + 1 < Nt && k + 1 >= 2) {  // chunk {k-1} of column k+1
-                const int64_t c = nchunks(k + 1, KC, 2) - 2;
-                gemm_col(k + 1, c, c + 1);
-            }
-            if (k + 2 < Nt) gemm_col(k + 2, 0, nchunks(k + 2, KC, 2) - 2);  // bulk of column k+2
+        if (k + 1 < Nt) {
+            int64_t nb1 = nchunks(k + 1, KC) - 1;  // bulk chunks of column k+1
+            gemm_col(k + 1, 0, nb1);
         }
         if (p->debug_sync == 2) continue;  // GEMM-throughput probe: no TRSM tasks
         for (int64_t m = k + 1; m < Nt; ++m)
@@ -366,7 +345,7 @@ int64_t plan_compact(const mxp_plan_s* p, std::vector<int32_t>& slot, std::vecto
     // all (Ozaki out of core): slots freed by columns <= j-3 -- the tiles of column j are
     // loaded during iteration j-2 (for the lookahead GEMMs of iteration j-1), while column
     // j-2's tiles become final and stream back (D2H) about one column later (measured)
-    const int64_t lag = all ? 3 : eff_lookahead(p) + 1;
+    const int64_t lag = all ? 3 : 2;
     for (int64_t j = 0; j < Nt; ++j) {
         if (j >= lag)
             for (int32_t x : freed_at[j - lag]) freelist.push_back(x);
@@ -605,7 +584,7 @@ size_t list_bytes(const mxp_plan_s* p) {
     for (int64_t k = 1; k < Nt; ++k) {
         int64_t per = diag_blocks;
         for (int64_t m = k + 1; m < Nt; ++m) per += gemm_blocks(p, m, k);
-        cnt += nchunks(k, p->splitk_tiles, 2) * per;  // (>= the count at lookahead 1)
+        cnt += nchunks(k, p->splitk_tiles) * per;
     }
     cnt += (Nt * (Nt - 1) / 2) * (nb / 64);
     for (int64_t t = 0; t < p->T; ++t) cnt += p->qtile[t] * (nb / 64);
@@ -1201,7 +1180,6 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     a.prec = (p->mxp || p->oz_on) ? p->d_prec : nullptr;
     a.oz_img = p->oz_on ? p->d_oz_img : nullptr;
     a.oz_slices = p->oz_slices;
-    a.lookahead = p->la_used;
     a.oz_prefetch = p->oz_prefetch;
     a.img_prev = p->oz_ooc ? p->d_img_prev : nullptr;
     a.ring_all = p->oz_ooc ? 1 : 0;
@@ -1688,12 +1666,7 @@ int mxp_chol_plan_set(mxp_plan_t p, mxp_attr_t key, int64_t v) {
         }
         p->splitk_tiles = v;
         return MXP_OK;
-    case MXP_ATTR_LOOKAHEAD:
-        if (v < 1 || v > 2) return -3;
-        p->lookahead = (int)v;
-        p->list_uploaded = false;
-        p->img_key = -1;  // (the compact ring's lag depends on it)
-        return MXP_OK;
+    case MXP_ATTR_LOOKAHEAD: p->lookahead = v ? 1 : 0; return MXP_OK;
     case MXP_ATTR_DEBUG_SYNC:
         if (v < 0 || v > 3) return -3;
         if ((v == 2) != (p->debug_sync == 2)) p->list_uploaded = false;

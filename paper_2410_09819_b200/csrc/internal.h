@@ -89,7 +89,6 @@ struct SchedArgs {
     const long long* oz_img;   // [T] byte offset of the tile's int8 slice image in `shadow` (-1: none);
                                //     nullptr: the Ozaki engine is off
     int oz_slices;             // s (slices per operand, 1..8)
-    int lookahead;             // chunk structure of the GEMM chains (chunk_range): 1 or 2 columns
     int oz_prefetch;           // L2 prefetch distance of the Ozaki operand ring, in K steps (0: off)
     const int32_t* img_prev;   // Ozaki out of core: [T] previous owner of t's slice-image slot (its QUANT
                                //     waits until that tile's row died: column complete); nullptr in core

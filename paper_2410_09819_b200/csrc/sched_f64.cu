@@ -81,17 +81,14 @@ __device__ __forceinline__ double matern_entry(const SchedArgs& a, int64_t i, in
 }
 
 // chunk c of column k: fixed-size chunks over [0, k-1), then the singleton {k-1}
-// chunk c of column k (lookahead LA): fixed-size chunks over [0, k-LA), then {k-LA}, ..., {k-1}
-__device__ __forceinline__ void chunk_range(int64_t k, int64_t c, int64_t KC, int64_t LA, int64_t& n0,
-                                            int64_t& n1) {
-    const int64_t tail = k < LA ? k : LA, bend = k - tail;
-    const int64_t nfull = bend > 0 ? (bend + KC - 1) / KC : 0;
+__device__ __forceinline__ void chunk_range(int64_t k, int64_t c, int64_t KC, int64_t& n0, int64_t& n1) {
+    int64_t nfull = k >= 2 ? (k - 1 + KC - 1) / KC : 0;
     if (c < nfull) {
         n0 = c * KC;
-        n1 = n0 + KC < bend ? n0 + KC : bend;
+        n1 = n0 + KC < k - 1 ? n0 + KC : k - 1;
     } else {
-        n0 = bend + (c - nfull);
-        n1 = n0 + 1;
+        n0 = k - 1;
+        n1 = k;
     }
 }
 
@@ -147,7 +144,7 @@ __device__ __forceinline__ bool task_gemm(const SchedArgs& a, int64_t m, int64_t
     const int64_t bi = b % SR, bj = b / SR;
     const int64_t t = tile_index(Nt, m, k);
     int64_t n0, n1;
-    chunk_range(k, c, a.KC, a.lookahead, n0, n1);
+    chunk_range(k, c, a.KC, n0, n1);
     int* chunk_flag = a.blk_chunk + t * a.NB + b;
     uint64_t tw0 = 0;
     if (threadIdx.x == 0) {
@@ -363,7 +360,7 @@ __device__ __noinline__ bool task_gemm_tc(const SchedArgs& a, int64_t m, int64_t
     const int64_t bi = b % S, bj = b / S;
     const int64_t t = tile_index(Nt, m, k);
     int64_t n0, n1;
-    chunk_range(k, c, a.KC, a.lookahead, n0, n1);
+    chunk_range(k, c, a.KC, n0, n1);
     int* chunk_flag = a.blk_chunk + t * a.NB + b;
     uint64_t tw0 = 0;
     if (threadIdx.x == 0) {
@@ -430,7 +427,7 @@ __device__ __noinline__ bool task_gemm_img(const SchedArgs& a, int64_t m, int64_
     const int64_t bi = b % S, bj = b / S;
     const int64_t t = tile_index(Nt, m, k);
     int64_t n0, n1;
-    chunk_range(k, c, a.KC, a.lookahead, n0, n1);
+    chunk_range(k, c, a.KC, n0, n1);
     int* chunk_flag = a.blk_chunk + t * a.NB + b;
     uint64_t tw0 = 0;
     if (threadIdx.x == 0) {
@@ -499,7 +496,7 @@ __device__ __noinline__ bool task_gemm_nat(const SchedArgs& a, int64_t m, int64_
     const int64_t bi = b % S, bj = b / S;
     const int64_t t = tile_index(Nt, m, k);
     int64_t n0, n1;
-    chunk_range(k, c, a.KC, a.lookahead, n0, n1);
+    chunk_range(k, c, a.KC, n0, n1);
     int* chunk_flag = a.blk_chunk + t * a.NB + b;
     uint64_t tw0 = 0;
     if (threadIdx.x == 0) {
@@ -561,7 +558,7 @@ __device__ __noinline__ bool task_gemm_oz(const SchedArgs& a, int64_t m, int64_t
     const int64_t bi = b % SR, bj = b / SR;  // 128-row block bi, 64-column block bj
     const int64_t t = tile_index(Nt, m, k);
     int64_t n0, n1;
-    chunk_range(k, c, a.KC, a.lookahead, n0, n1);
+    chunk_range(k, c, a.KC, n0, n1);
     int* chunk_flag = a.blk_chunk + t * a.NB + b;
     uint64_t tw0 = 0;
     if (threadIdx.x == 0) {
