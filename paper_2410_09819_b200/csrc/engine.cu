@@ -128,6 +128,7 @@ struct mxp_plan_s {
     int64_t ring_slots = 0, oz_img_slots = 0;
     std::vector<int32_t> ring_slot, ring_prev, img_prev;
     int32_t* d_img_prev = nullptr;
+    int* d_oz_flag = nullptr;       // Ozaki: tiles whose row scales grew (SchedArgs::oz_flag)
     double* d_solve = nullptr;      // forward-solve work vectors (r | z | scalars)
     std::vector<int4> items2;       // GEMM list of k_tc (Ozaki mode)
     cudaStream_t sT = 0;
@@ -667,7 +668,7 @@ bool plan_slots(mxp_plan_s* p, int64_t C) {
 
 struct Layout {
     size_t slot, prev, epoch, flags, flags_bytes, expected, items, wbuf, stats, prec, amax_x, amax_s, iscale, args,
-        qtile, img, ozimg, imgprev, sto, in_scale, solve, shadow, pool, total;
+        qtile, img, ozimg, imgprev, ozflag, sto, in_scale, solve, shadow, pool, total;
 };
 
 Layout layout(const mxp_plan_s* p) {
@@ -709,6 +710,8 @@ Layout layout(const mxp_plan_s* p) {
     off += align_up(sizeof(long long) * (size_t)p->T, 256);
     L.imgprev = off;
     off += align_up(sizeof(int32_t) * (size_t)p->T, 256);
+    L.ozflag = off;
+    off += align_up(sizeof(int) * (size_t)p->T, 256);
     L.sto = off;
     off += align_up(sizeof(long long) * (size_t)p->T, 256);
     L.in_scale = off;
@@ -777,6 +780,7 @@ void bind_workspace(mxp_plan_s* p) {
     p->d_img = (long long*)(p->ws + L.img);
     p->d_oz_img = (long long*)(p->ws + L.ozimg);
     p->d_img_prev = (int32_t*)(p->ws + L.imgprev);
+    p->d_oz_flag = (int*)(p->ws + L.ozflag);
     p->d_sto = (long long*)(p->ws + L.sto);
     p->d_in_scale = (double*)(p->ws + L.in_scale);
     p->d_solve = (double*)(p->ws + L.solve);
@@ -1180,6 +1184,8 @@ void factor_incore_f64(mxp_plan_s* p, cudaStream_t s0, bool host_mode, double* A
     a.prec = (p->mxp || p->oz_on) ? p->d_prec : nullptr;
     a.oz_img = p->oz_on ? p->d_oz_img : nullptr;
     a.oz_slices = p->oz_slices;
+    a.oz_flag = p->oz_on ? p->d_oz_flag : nullptr;
+    if (a.oz_flag) CK(cudaMemsetAsync(p->d_oz_flag, 0, sizeof(int) * (size_t)T, s0));
     a.oz_prefetch = p->oz_prefetch;
     a.img_prev = p->oz_ooc ? p->d_img_prev : nullptr;
     a.ring_all = p->oz_ooc ? 1 : 0;

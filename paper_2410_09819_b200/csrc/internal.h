@@ -89,6 +89,10 @@ struct SchedArgs {
     const long long* oz_img;   // [T] byte offset of the tile's int8 slice image in `shadow` (-1: none);
                                //     nullptr: the Ozaki engine is off
     int oz_slices;             // s (slices per operand, 1..8)
+    // Ozaki running row scales (oz_slice_rows): oz_flag[t] = 1 when a row of tile t = (m, k) needed
+    // a larger scale than in tile (m, k-1); a GEMM chunk with no flagged tile after its first
+    // accumulates across its K tiles in int32 TMEM and drains once.  nullptr: per-tile scales.
+    int* oz_flag;              // [T]
     int oz_prefetch;           // L2 prefetch distance of the Ozaki operand ring, in K steps (0: off)
     const int32_t* img_prev;   // Ozaki out of core: [T] previous owner of t's slice-image slot (its QUANT
                                //     waits until that tile's row died: column complete); nullptr in core

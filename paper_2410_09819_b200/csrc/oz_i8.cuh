@@ -274,9 +274,15 @@ __device__ __forceinline__ uint64_t oz_clock() {
 // RACC (the 4-warp k_tc of FP64 maps): the tiles' products accumulate in 64
 // fp64 registers per thread and C is updated once per task; otherwise (the
 // 5-warp k_tc of MxP maps, 168 registers) C is updated once per tile of K.
+// uniform: every tile of the chunk carries the same row scales (running row scales, no flagged
+// tile after the first): the int32 level accumulators run across up to `maxt` tiles of K before one drain
+// (|ACC_c| <= S 2^14 K must stay below 2^31), instead of one drain per tile of K.
 template <int S, bool RACC, class Src>
 __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles, int kt, int64_t nb, uint8_t* smem,
-                             uint32_t tmem, int pf, unsigned long long* stats) {
+                             uint32_t tmem, int pf, unsigned long long* stats, bool uniform) {
+    const long long lim = 2147483647LL / ((long long)S * 16384 * 32 * kt);
+    const int maxt = uniform ? (lim < 1 ? 1 : (int)lim) : 1;
+    int ndrain = 0;
     uint64_t t_full = 0, t_done = 0, t_drain = 0, t_mma = 0, t_copy = 0, t_loop = 0, t_tbar = 0;
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * STAGE_BYTES);
@@ -358,7 +364,7 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
                 tc::fence_after();
                 const uint32_t sa = tc::smem_u32(base + stage * STAGE_BYTES);
                 const uint64_t ad0 = make_desc(sa), bd0 = make_desc(sa + MAX_S * CHUNK);
-                const uint32_t acc0 = kc > 0 ? 1u : 0u;
+                const uint32_t acc0 = (kc > 0 || i % maxt != 0) ? 1u : 0u;
                 const uint64_t m0 = stats ? oz_clock() : 0;
                 // A slice t meets B slices u = 0 .. S-1-t, i.e. levels t .. S-1.  The B
                 // slices sit 2 KB apart in smem (64 rows each): B slices u0 .. u0+m-1
@@ -384,8 +390,10 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
                 __syncwarp();
                 if (stats) t_mma += oz_clock() - m0;
             }
-            if (elect_one()) tc::commit(tbar);  // every MMA of tile i
-            __syncwarp();
+            if ((i + 1) % maxt == 0 || i + 1 == ntiles) {
+                if (elect_one()) tc::commit(tbar);  // every MMA up to tile i
+                __syncwarp();
+            }
             if (stats) t_loop += oz_clock() - l0;
         } else if (warp == 1) {
             // refill the stage of step g - 1 once its MMAs have read it (step g's MMAs
@@ -402,13 +410,15 @@ __device__ void block_gemm_t(double* C, int64_t ldc, const Src& src, int ntiles,
                 }
             }
         }
-        // drain: ACC levels of tile i -> fp64, scaled by the row scales
-        // (threads 0..127 = TMEM lanes; in k_tc warp 4 only join the barriers)
+        // drain: ACC levels of tile i (of tiles i-maxt+1 .. i when uniform) -> fp64, scaled by
+        // the row scales (threads 0..127 = TMEM lanes; in k_tc warp 4 only join the barriers)
+        if ((i + 1) % maxt != 0 && i + 1 != ntiles) continue;
         const bool wk = tid < 128;
         const uint64_t d0 = (stats && tid == 0) ? oz_clock() : 0;
         if (tid < BN) s_sb[tid] = __ldcg(src(i).sb + tid);
         const double sa_r = wk ? __ldcg(src(i).sa + tid) : 0.0;
-        if (wk) tc::mbar_wait(tbar, (uint32_t)(i & 1));
+        if (wk) tc::mbar_wait(tbar, (uint32_t)(ndrain & 1));
+        ++ndrain;
         tc::fence_after();
         __syncthreads();  // s_sb visible
         __syncwarp();     // (converged warp for the .sync.aligned TMEM loads)
@@ -479,13 +489,13 @@ constexpr int MIN_S = 4;  // slices supported by the compiled variants: MIN_S..M
 template <bool RACC, class Src>
 __device__ __forceinline__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, int s, int kt,
                                            int64_t nb, uint8_t* smem, uint32_t tmem, int pf,
-                                           unsigned long long* stats) {
+                                           unsigned long long* stats, bool uniform) {
     switch (s) {
-    case 4: block_gemm_t<4, RACC>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats); break;
-    case 5: block_gemm_t<5, RACC>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats); break;
-    case 6: block_gemm_t<6, RACC>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats); break;
-    case 7: block_gemm_t<7, RACC>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats); break;
-    default: block_gemm_t<8, RACC>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats); break;
+    case 4: block_gemm_t<4, RACC>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats, uniform); break;
+    case 5: block_gemm_t<5, RACC>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats, uniform); break;
+    case 6: block_gemm_t<6, RACC>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats, uniform); break;
+    case 7: block_gemm_t<7, RACC>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats, uniform); break;
+    default: block_gemm_t<8, RACC>(C, ldc, src, ntiles, kt, nb, smem, tmem, pf, stats, uniform); break;
     }
 }
 

@@ -554,6 +554,7 @@ __device__ __noinline__ bool task_gemm_nat(const SchedArgs& a, int64_t m, int64_
 template <bool RACC>
 __device__ __noinline__ bool task_gemm_oz(const SchedArgs& a, int64_t m, int64_t k, int64_t b, int64_t c,
                                           uint8_t* smem, uint32_t tmem, int* s_flag) {
+    __shared__ int s_uni;
     const int64_t Nt = a.Nt, nb = a.nb, SR = nb / 128;
     const int64_t bi = b % SR, bj = b / SR;  // 128-row block bi, 64-column block bj
     const int64_t t = tile_index(Nt, m, k);
@@ -568,6 +569,12 @@ __device__ __noinline__ bool task_gemm_oz(const SchedArgs& a, int64_t m, int64_t
             ok = wait_flag(a.ready + tile_index(Nt, m, n), a.epoch, a, k) &&
                  wait_flag(a.ready + tile_index(Nt, k, n), a.epoch, a, k);
         if (ok) ok = wait_flag(chunk_flag, (int)c, a, k);
+        // one drain for the chunk when no row scale changes inside it (oz_flag of the tiles after
+        // the first, set by their QUANTs before the Ready words just acquired)
+        int uni = (ok && a.oz_flag) ? 1 : 0;
+        for (int64_t n = n0 + 1; n < n1 && uni; ++n)
+            if (__ldcg(a.oz_flag + tile_index(Nt, m, n)) | __ldcg(a.oz_flag + tile_index(Nt, k, n))) uni = 0;
+        s_uni = uni;
         *s_flag = ok;
         if (a.stats) {
             uint64_t tw1 = globaltimer();
@@ -577,6 +584,7 @@ __device__ __noinline__ bool task_gemm_oz(const SchedArgs& a, int64_t m, int64_t
     }
     __syncthreads();
     if (!*s_flag) return false;
+    const bool uniform = s_uni != 0;
     const int s = a.oz_slices;
     const int64_t sc_off = (int64_t)s * nb * nb;
     auto src = [&](int i) {
@@ -591,7 +599,8 @@ __device__ __noinline__ bool task_gemm_oz(const SchedArgs& a, int64_t m, int64_t
         return o;
     };
     double* Ct = tile_ptr(a.pool, a.slot, Nt, nb, m, k) + bi * 128 + bj * 64 * nb;
-    oz::block_gemm<RACC>(Ct, nb, src, (int)(n1 - n0), s, (int)(nb / 32), nb, smem, tmem, a.oz_prefetch, a.stats);
+    oz::block_gemm<RACC>(Ct, nb, src, (int)(n1 - n0), s, (int)(nb / 32), nb, smem, tmem, a.oz_prefetch, a.stats,
+                         uniform);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -608,7 +617,8 @@ __device__ __noinline__ bool task_gemm_oz(const SchedArgs& a, int64_t m, int64_t
 // Int8 slice image of rows [64r, 64r+64) of a final tile (Ozaki operands):
 // per-row scale 2^(E-6) from the row max, then s digits per element.  Thread
 // (row = tid & 63, half = tid >> 6) covers half of the row's columns.
-__device__ void oz_slice_rows(const SchedArgs& a, const double* X, int64_t r, uint8_t* img, double* red) {
+__device__ void oz_slice_rows(const SchedArgs& a, const double* X, int64_t m, int64_t k, int64_t r, uint8_t* img,
+                              double* red) {
     const int64_t nb = a.nb;
     const int s = a.oz_slices;
     const int tid = threadIdx.x, row = tid & 63, half = tid >> 6;
@@ -618,7 +628,31 @@ __device__ void oz_slice_rows(const SchedArgs& a, const double* X, int64_t r, ui
     red[tid] = mx;
     sync_workers();
     double inv;
-    const double sc = oz::row_scale(fmax(red[row], red[row + 64]), inv);
+    const double rmax = fmax(red[row], red[row + 64]);
+    double sc = oz::row_scale(rmax, inv);
+    if (a.oz_flag && !(rmax > 0.0)) {  // a zero row: the smallest scale, replaced by any later one
+        sc = 0x1p-1000;
+        inv = 0x1p994;
+    } else if (a.oz_flag) {  // two binades of headroom, so the running scale rarely has to grow
+        sc *= 4.0;
+        inv *= 0.25;
+    }
+    if (a.oz_flag && k > 0) {
+        // Running row scales: a row keeps the scale it had in tile (m, k-1) unless this tile holds
+        // a larger entry, so consecutive tiles of a row usually share their scales and a GEMM
+        // chunk over them can accumulate in int32 TMEM across its K tiles (one drain); a tile
+        // whose scales changed is flagged (oz_flag) and its chunk drains per tile.  A scale is
+        // then >= the tile's own row max (as precise, or one binade coarser for the smaller rows
+        // of a tile), and exactly the row max where the row max grew.
+        const uint8_t* pimg = a.shadow + a.oz_img[tile_index(a.Nt, m, k - 1)];
+        const double ps = __ldcg(reinterpret_cast<const double*>(pimg + (int64_t)s * nb * nb) + r * 64 + row);
+        if (ps >= 0.25 * sc) {  // (the previous scale still covers this row's max)
+            sc = ps;
+            inv = 1.0 / (64.0 * ps);  // ps = 2^(E-6): inv = 2^-E, exact
+        } else if (half == 0) {
+            atomicOr(a.oz_flag + tile_index(a.Nt, m, k), 1);
+        }
+    }
     if (half == 0) reinterpret_cast<double*>(img + (int64_t)s * nb * nb)[r * 64 + row] = sc;
     for (int64_t k0 = c0; k0 < c1; k0 += 16) {
         double x[16];
@@ -772,7 +806,7 @@ __device__ __noinline__ bool task_quant(const SchedArgs& a, int64_t m, int64_t k
         __threadfence_block();
         sync_workers();
         if (!*s_flag) return false;
-        oz_slice_rows(a, X, r, a.shadow + a.oz_img[t], red);
+        oz_slice_rows(a, X, m, k, r, a.shadow + a.oz_img[t], red);
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");  // images are read by bulk copies
     __threadfence();
