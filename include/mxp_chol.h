@@ -92,10 +92,11 @@ typedef enum mxp_attr {
                                      1 = Ozaki scheme I on the int8 tensor cores (tcgen05 kind::i8): every
                                        off-diagonal tile is split once, exactly, into s int8 slices with a
                                        power-of-two scale per row (8s - 2 bits + sign, balanced base-256
-                                       digits), the s(s+1)/2 slice products of weight >= 2^-8(s-1) are
-                                       accumulated exactly in int32 TMEM, and the
-                                       levels are combined in fp64 after every tile of K (fp64 accumulation
-                                       across tiles).  Single rank.  In core the pool keeps every fp64 tile
+                                       digits; a row keeps its scale from tile to tile unless a larger
+                                       entry needs more, with two binades of headroom), the s(s+1)/2 slice
+                                       products of weight >= 2^-8(s-1) are accumulated exactly in int32
+                                       TMEM across the K tiles that share their scales, and the levels are
+                                       combined in fp64 (fp64 accumulation across those groups).  Single rank.  In core the pool keeps every fp64 tile
                                        beside the slice images.  Out of core (FP64 map, HBM cap below the
                                        lower triangle; mxp_chol_factor / _factor_tiles / _factor_matern) an
                                        fp64 tile lives in a ring slot only while it is computed and a final
