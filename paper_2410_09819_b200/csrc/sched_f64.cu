@@ -533,7 +533,8 @@ __device__ __noinline__ bool task_gemm_nat(const SchedArgs& a, int64_t m, int64_
         return o;
     };
     double* Ct = tile_ptr(a.pool, a.slot, Nt, nb, m, k) + bi * 128 + bj * 128 * nb;
-    nat::block_gemm<KIND>(Ct, nb, src, (int)(n1 - n0), (int)(nb / nat::ke(KIND)), smem, tmem, a.stats);
+    nat::block_gemm<KIND>(Ct, nb, src, (int)(n1 - n0), (int)(nb / nat::ke(KIND)), smem, tmem, a.stats,
+                          a.oz_prefetch);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {

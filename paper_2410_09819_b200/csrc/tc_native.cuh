@@ -188,7 +188,7 @@ __device__ __forceinline__ uint64_t nat_clock() {
 }
 template <int KIND, class Src>
 __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, int kt, uint8_t* smem, uint32_t tmem,
-                           unsigned long long* stats = nullptr) {
+                           unsigned long long* stats = nullptr, int pf = 0) {
     uint64_t w_full = 0, w_empty = 0, w_tempty = 0, t_drain = 0, t_final = 0;
     constexpr int NS = nstages(KIND), SB = stage_bytes(KIND);
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
@@ -207,8 +207,8 @@ __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, i
     __syncthreads();
     if (warp == 4) {  // (all 32 lanes walk the loop converged; one elected lane issues)
         {
-            NatTile cur{}, curm{};
-            int cur_i = -1;
+            NatTile cur{}, curm{}, pcur{};
+            int cur_i = -1, pcur_i = -1;
             auto issue = [&](int g) {  // bulk copies of K step g into its stage
                 const int st = g % NS, i = g / kt, kc = g - i * kt;
                 if (i != cur_i) cur = src(i), cur_i = i;
@@ -216,6 +216,19 @@ __device__ void block_gemm(double* C, int64_t ldc, const Src& src, int ntiles, i
                 const int64_t o = (int64_t)kc * CHUNK;
                 uint32_t bytes = 2 * CHUNK;
                 if (KIND == K_F32X2) bytes += (cur.al ? CHUNK : 0) + (cur.bl ? CHUNK : 0);
+                const int gp = g + pf;  // L2 prefetch of the operands pf K steps ahead (MXP_ATTR_OZ_PREFETCH)
+                if (pf > 0 && gp < G) {
+                    const int ip = gp / kt, kp = gp - ip * kt;
+                    if (ip != pcur_i) pcur = src(ip), pcur_i = ip;
+                    if (elect1()) {
+                        const int64_t op = (int64_t)kp * CHUNK;
+                        tc::bulk_prefetch_l2(pcur.a + op, CHUNK);
+                        tc::bulk_prefetch_l2(pcur.b + op, CHUNK);
+                        if (KIND == K_F32X2 && pcur.al) tc::bulk_prefetch_l2(pcur.al + op, CHUNK);
+                        if (KIND == K_F32X2 && pcur.bl) tc::bulk_prefetch_l2(pcur.bl + op, CHUNK);
+                    }
+                    __syncwarp();
+                }
                 if (elect1()) {
                     tc::mbar_expect_tx(full + st, bytes);
                     tc::bulk_g2s(sa, cur.a + o, CHUNK, full + st);

@@ -80,6 +80,8 @@ def main():
         xy = torch.tensor(w.matern_locations(n, seed=1), device="cuda")
         pmap, _ = m.precision_map_matern_device(xy, nb, eps, 1.0, a)
         plan = m.Plan(n, nb, pmap)
+        if "OZ_PF" in os.environ:
+            plan.set("oz_prefetch", int(os.environ["OZ_PF"]))
         if "SPLITK" in os.environ:
             plan.set("splitk_tiles", int(os.environ["SPLITK"]))
         plan.set("profile", int(os.environ.get("PROFILE", "0")))
