@@ -177,6 +177,7 @@ struct mxp_plan_s {
     // (the paper's C2G / G2C / Work rows): per column k, events after its H2D loads,
     // after its D2H write-backs and after its POTRF; tl_ms = ms since the factorization start
     std::vector<cudaEvent_t> ev_tl;
+    std::vector<cudaEvent_t> ev_solve;  // forward solve: two streams' column events
     std::vector<char> tl_rec;
     std::vector<double> tl_ms;
     bool tl_on = false;
@@ -203,6 +204,7 @@ mxp_plan_s::~mxp_plan_s() {
     for (auto e : ev_bulk) cudaEventDestroy(e);
     for (auto e : ev_pool) cudaEventDestroy(e);
     for (auto e : ev_tl) cudaEventDestroy(e);
+    for (auto e : ev_solve) cudaEventDestroy(e);
     if (ev_start) cudaEventDestroy(ev_start);
     if (ev_done) cudaEventDestroy(ev_done);
     if (sU) cudaStreamDestroy(sU);
@@ -2576,8 +2578,17 @@ int mxp_chol_solve_lower(mxp_plan_t p, const double* y_dev, double* z_dev, doubl
         cudaStream_t s = p->user_stream;
         CK(cudaMemsetAsync(r, 0, sizeof(double) * N, s));
         CK(cudaMemcpyAsync(r, y_dev, sizeof(double) * p->n, cudaMemcpyDeviceToDevice, s));
+        ensure_streams(p);
+        while (p->ev_solve.size() < 2 * (size_t)p->Nt) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            p->ev_solve.push_back(e);
+        }
+        // (s2 = the auxiliary stream, joined after the caller's pending work)
+        CK(cudaEventRecord(p->ev_done, s));
+        CK(cudaStreamWaitEvent(p->sAux, p->ev_done, 0));
         launch_forward_solve(p->pool, p->d_slot, p->d_wbuf, p->Nt, p->nb, r, z, s, decode_args(p),
-                             reinterpret_cast<int*>(sc + 8), ++p->solve_seq);
+                             reinterpret_cast<int*>(sc + 8), ++p->solve_seq, p->sAux, p->ev_solve.data());
         launch_sumsq(z, p->n, sc, s);
         CK(cudaGetLastError());
         if (z_dev) CK(cudaMemcpyAsync(z_dev, z, sizeof(double) * p->n, cudaMemcpyDeviceToDevice, s));

@@ -170,9 +170,11 @@ struct TileCodes {
 // z = L^-1 r on the resident factor (r, z: Nt*nb, padded with zeros; r is consumed)
 // flags: >= nb/128 ints of device memory for the parallel diagonal solves (publication tags
 // seq * Nt + k + 1; seq distinct per call), or nullptr for the one-CTA diagonal solve
+// s2 / ev (2 Nt events): the updates of the rows below the next tile row run on s2, overlapping
+// the diagonal solves on s (bitwise the same result); s2 == nullptr: one stream
 void launch_forward_solve(const double* pool, const int32_t* slot, const double* wbuf, int64_t Nt, int64_t nb,
                           double* r, double* z, cudaStream_t s, TileCodes codes = TileCodes{},
-                          int* flags = nullptr, int seq = 0);
+                          int* flags = nullptr, int seq = 0, cudaStream_t s2 = nullptr, cudaEvent_t* ev = nullptr);
 void launch_sumsq(const double* z, int64_t n, double* out, cudaStream_t s);
 
 // ---- layout / utility kernels --------------------------------------------

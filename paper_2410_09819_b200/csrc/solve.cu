@@ -37,12 +37,12 @@ __device__ __forceinline__ double row_dot(const double* L, const uint8_t* codes,
 
 constexpr int GEMV_T = 512;  // 4 column quarters x 128 rows
 __global__ void __launch_bounds__(GEMV_T) k_trsv_gemv(const double* __restrict__ pool, const int32_t* __restrict__ slot,
-                                                      int64_t Nt, int64_t nb, int64_t k, double* r,
+                                                      int64_t Nt, int64_t nb, int64_t k, int64_t m0, double* r,
                                                       const double* __restrict__ z, TileCodes codes) {
     extern __shared__ double sz[];  // z_k (nb) + GEMV_T partial sums
     double* part = sz + nb;
     const int64_t RB = nb / 128;
-    const int64_t m = k + 1 + blockIdx.x / RB, rb = blockIdx.x % RB;
+    const int64_t m = m0 + blockIdx.x / RB, rb = blockIdx.x % RB;  // tile rows m0, m0+1, ...
     for (int64_t c = threadIdx.x; c < nb; c += blockDim.x) sz[c] = z[k * nb + c];
     __syncthreads();
     const int row = threadIdx.x & 127, h = threadIdx.x >> 7;
@@ -190,7 +190,8 @@ __global__ void __launch_bounds__(1024) k_sumsq(const double* __restrict__ z, in
 }  // namespace
 
 void launch_forward_solve(const double* pool, const int32_t* slot, const double* wbuf, int64_t Nt, int64_t nb,
-                          double* r, double* z, cudaStream_t s, TileCodes codes, int* flags, int seq) {
+                          double* r, double* z, cudaStream_t s, TileCodes codes, int* flags, int seq, cudaStream_t s2,
+                          cudaEvent_t* ev) {
     const size_t sm_diag = sizeof(double) * (nb + 128 + 256), sm_gemv = sizeof(double) * (nb + GEMV_T);
     static bool configured = false;
     if (!configured) {
@@ -198,18 +199,37 @@ void launch_forward_solve(const double* pool, const int32_t* slot, const double*
         cudaFuncSetAttribute(k_trsv_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         configured = true;
     }
+    const unsigned RB = (unsigned)(nb / 128);
+    // Two streams (ev: 2 Nt events, s2 != nullptr): s runs the chain -- diagonal solve of column
+    // k, then the update of tile row k+1 by z_k -- and s2 the update of tile rows >= k+2, which
+    // thus overlaps the next diagonal solves.  Each r_m still receives its updates in column
+    // order: the s2 update by z_k (rows >= k+2) precedes the s update of row k+2 by z_{k+1}
+    // (s waits for it), so the result is bitwise that of the one-stream order.
     for (int64_t k = 0; k < Nt; ++k) {
+        if (s2 && k >= 2) cudaStreamWaitEvent(s, ev[Nt + k - 2], 0);  // r_k got its z_{k-2} share (s2)
         if (flags) {
-            k_trsv_diag_par<<<(unsigned)(nb / 128), 256, 0, s>>>(pool, slot, wbuf, Nt, nb, k, r, z, flags,
-                                                                 (int)(seq * Nt + k + 1));
+            k_trsv_diag_par<<<RB, 256, 0, s>>>(pool, slot, wbuf, Nt, nb, k, r, z, flags, (int)(seq * Nt + k + 1));
         } else {
             MXP_CARVEOUT_MAX(k_trsv_diag);
             k_trsv_diag<<<1, 256, sm_diag, s>>>(pool, slot, wbuf, Nt, nb, k, r, z);
         }
         MXP_CARVEOUT_MAX(k_trsv_gemv);
-        if (k + 1 < Nt)
-            k_trsv_gemv<<<(unsigned)((Nt - k - 1) * (nb / 128)), GEMV_T, sm_gemv, s>>>(pool, slot, Nt, nb, k, r, z, codes);
+        if (k + 1 >= Nt) continue;
+        if (!s2) {
+            k_trsv_gemv<<<(unsigned)(Nt - k - 1) * RB, GEMV_T, sm_gemv, s>>>(pool, slot, Nt, nb, k, k + 1, r, z, codes);
+            continue;
+        }
+        if (k + 2 < Nt) {  // rows >= k+2 on s2, after z_k is final
+            cudaEventRecord(ev[k], s);
+            cudaStreamWaitEvent(s2, ev[k], 0);
+            k_trsv_gemv<<<(unsigned)(Nt - k - 2) * RB, GEMV_T, sm_gemv, s2>>>(pool, slot, Nt, nb, k, k + 2, r, z,
+                                                                              codes);
+            cudaEventRecord(ev[Nt + k], s2);
+        }
+        if (k >= 1) cudaStreamWaitEvent(s, ev[Nt + k - 1], 0);  // row k+1's z_{k-1} share came first
+        k_trsv_gemv<<<RB, GEMV_T, sm_gemv, s>>>(pool, slot, Nt, nb, k, k + 1, r, z, codes);
     }
+    if (s2 && Nt >= 3) cudaStreamWaitEvent(s, ev[Nt + Nt - 3], 0);  // (the last s2 update)
 }
 
 void launch_sumsq(const double* z, int64_t n, double* out, cudaStream_t s) {
